@@ -1,0 +1,464 @@
+"""bench.py — throughput of the Helios mini-batch preparation hot path on B200.
+
+A step = one whole mini-batch through every §8(a) row: seeds -> L-hop sampling (K1/K2) -> cache
+lookup + gather of N_L's feature rows from the HBM / pinned-host / file tiers (K3/K4, K5/K6).
+Default workload: the papers100M-shaped config (C3; = the C5 sweep config at N=1), inputs resident
+in HBM / pinned host memory before the timed region.  Under torchrun each rank takes the batches
+b = rank (mod N) with its own key, the HBM tier is sharded over the ranks (peer rows over NVLink),
+NCCL is used only for setup (hotness all-reduce, IPC-handle all-gather).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl helios|reference]
+
+Prints ONE JSON line (rank 0).  See DESIGN.md §Measurement for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import mmap
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+import workloads  # noqa: E402
+
+HBM_PEAK_FALLBACK = 6650.0  # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def log(*a):
+    if int(os.environ.get("RANK", "0")) == 0:
+        print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+def host_buffer(nbytes: int, shm_name: str | None = None, create: bool = True):
+    """Page-aligned host buffer for the canonical feature table: anonymous memory with transparent
+    huge pages (N=1) or a /dev/shm file shared by all ranks (N>1)."""
+    if shm_name is None:
+        m = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+        try:
+            m.madvise(mmap.MADV_HUGEPAGE)
+        except Exception:
+            pass
+        return m
+    path = f"/dev/shm/{shm_name}"
+    if create:
+        fd = os.open(path, os.O_CREAT | os.O_RDWR | os.O_TRUNC, 0o600)
+        os.ftruncate(fd, nbytes)
+    else:
+        fd = os.open(path, os.O_RDWR)
+    m = mmap.mmap(fd, nbytes, flags=mmap.MAP_SHARED)
+    os.close(fd)
+    try:
+        m.madvise(mmap.MADV_HUGEPAGE)
+    except Exception:
+        pass
+    return m
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                pass
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+                for n, v in zip(names, f[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def pcie_h2d_peak(torch, nbytes: int = 1 << 30) -> float:
+    """Pinned host -> device copy-engine bandwidth (GB/s, best of 5): the PCIe roofline denominator."""
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    best = 1e9
+    for _ in range(6):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        d.copy_(h, non_blocking=True)
+        b.record()
+        b.synchronize()
+        best = min(best, a.elapsed_time(b))
+    del h, d
+    return nbytes / best / 1e6
+
+
+def pick_scale(cfg: workloads.Config, world: int) -> float:
+    """Capacity rule: shrink V, E by s if host RAM cannot hold the canonical table."""
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except Exception:
+        return 1.0
+    need = cfg.V * cfg.R + cfg.E * 4 * 3 + cfg.V * 8 * 4
+    return 1.0 if need < 0.8 * avail else max(0.01, math.floor(0.8 * avail / need * 100) / 100)
+
+
+# ---------------------------------------------------------------------------------------------
+
+def run_oracle_baseline(inp, keys, budget_s: float, check=None) -> dict:
+    """The oracle as it stands (single-threaded C++), on a bounded sample of the same batches."""
+    import oracle
+    cfg = inp.cfg
+    t0 = time.perf_counter()
+    done, rows = 0, 0
+    for b, (seeds, key) in enumerate(zip(inp.batches, keys)):
+        ob = oracle.sample(inp.graph.indptr, inp.graph.indices, seeds, cfg.fanouts, key)
+        feats = oracle.gather(ob.nodes, cfg.R, table=inp.table)
+        if check is not None:
+            check(b, ob, feats)
+        done += 1
+        rows += len(ob.nodes)
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"batches": done, "seconds": dt, "value": done / dt, "gbs": rows * cfg.R / dt / 1e9}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--scale", type=float, default=0.0, help="V,E scale factor (0 = auto from host RAM)")
+    ap.add_argument("--impl", default="helios", choices=["helios", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parity-batches", type=int, default=2)
+    ap.add_argument("--profile", action="store_true", help="short run for ncu: no baseline, no parity")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg0 = workloads.CONFIGS[args.config]
+    s = args.scale if args.scale > 0 else pick_scale(cfg0, world)
+    cfg = workloads.scaled(cfg0, s)
+
+    if args.impl == "reference":
+        return reference_arm(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2310_00837_b200 import helios as H
+
+    # ---- inputs (rank 0 generates; shared through /dev/shm when N > 1) ----
+    t_setup = time.time()
+    shm = f"helios_bench_{os.getppid()}" if world > 1 else None
+    tab_bytes = cfg.V * cfg.R
+    if rank == 0:
+        buf = host_buffer(tab_bytes, f"{shm}_feat" if shm else None, create=True)
+        table = np.frombuffer(buf, dtype=np.float32).reshape(cfg.V, cfg.dim)
+        inp = workloads.make_inputs(cfg, table=True, table_buffer=table)
+        if world > 1:
+            np.save(f"/dev/shm/{shm}_indptr.npy", inp.graph.indptr)
+            np.save(f"/dev/shm/{shm}_indices.npy", inp.graph.indices)
+    if world > 1:
+        dist.barrier()
+        if rank != 0:
+            buf = host_buffer(tab_bytes, f"{shm}_feat", create=False)
+            table = np.frombuffer(buf, dtype=np.float32).reshape(cfg.V, cfg.dim)
+            gr = synth.Graph(cfg.V, np.load(f"/dev/shm/{shm}_indptr.npy", mmap_mode="r"),
+                             np.load(f"/dev/shm/{shm}_indices.npy", mmap_mode="r"))
+            train = synth.train_set(cfg.V, workloads.SEED, cfg.train_pct)
+            inp = workloads.Inputs(cfg, gr, table, None, 0, 0, train,
+                                   synth.epoch_batches(train, cfg.B, 0, workloads.SEED))
+    gen_s = time.time() - t_setup
+    log(f"inputs {cfg.name}: V={cfg.V} E={inp.graph.E} dim={cfg.dim} gen {gen_s:.1f}s")
+
+    t1 = time.time()
+    g = H.helios_graph_load(inp.graph.indptr, inp.graph.indices, device=local)
+    full_batches = [b for b in inp.batches if len(b) == cfg.B]
+    # presample: one epoch with presample keys, split over ranks, hotness all-reduced (NCCL)
+    hot = torch.zeros(cfg.V, dtype=torch.int64, device="cuda")
+    mine = [b for b in range(len(inp.batches)) if b % world == rank]
+    pkeys = workloads.presample_keys(len(inp.batches))
+    for b in mine:
+        H.helios_presample(g, torch.as_tensor(inp.batches[b]).cuda(), cfg.B, cfg.fanouts, [pkeys[b]], hot)
+    H.helios_graph_sync(g)
+    if world > 1:
+        dist.all_reduce(hot)
+    presample_s = time.time() - t1
+    Hr, S = workloads.tier_rows(cfg, world)
+    S = max(0, min(S, cfg.V - world * Hr)) if cfg.host_frac + cfg.hbm_frac >= 1.0 else S
+    if cfg.hbm_frac + cfg.host_frac >= 1.0:
+        S = max(0, cfg.V - world * Hr)
+    t2 = time.time()
+    c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
+                             flags=H.HOST_ALIAS)
+    if world > 1:
+        blob = H.helios_cache_export(c)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, blob)
+        H.helios_cache_attach_peers(c, blobs)
+        dist.barrier()
+    build_s = time.time() - t2
+    log(f"graph load + presample {presample_s:.1f}s, cache build {build_s:.1f}s (H={Hr}/GPU, S={S})")
+
+    # ---- timed loop ----
+    blocks = H.Blocks.allocate(cfg.B, cfg.fanouts, g.V, g.E)
+    feats = torch.empty((blocks.nodes.numel(), cfg.R), dtype=torch.uint8, device="cuda")
+    stats = H.new_stats()
+    keys = workloads.batch_keys(0, len(inp.batches))
+    my_batches = [b for b in range(len(full_batches)) if b % world == rank]
+    need = args.warmup + args.steps
+    seq = [my_batches[i % len(my_batches)] for i in range(need)]
+    dev_seeds = [torch.as_tensor(inp.batches[b]).cuda() for b in sorted(set(seq))]
+    seed_of = {b: t for b, t in zip(sorted(set(seq)), dev_seeds)}
+    stream = torch.cuda.current_stream()
+    L = len(cfg.fanouts)
+
+    def step(b, ev=None):
+        H.helios_sample(g, seed_of[b], cfg.fanouts, keys[b], blocks, stream)
+        if ev is not None:
+            ev[0].record(stream)
+        H.helios_gather(c, blocks.nodes, blocks.level_counts[L:L + 1], feats, stats, stream)
+        if ev is not None:
+            ev[1].record(stream)
+
+    for i in range(args.warmup):
+        step(seq[i])
+    H.helios_sync(c)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stat_acc = torch.zeros(4, dtype=torch.int64, device="cuda")
+    nl_acc = torch.zeros(1, dtype=torch.int64, device="cuda")
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for i in range(args.steps):
+            e0, e1, e2 = evs[i]
+            e0.record(stream)
+            step(seq[args.warmup + i], (e1, e2))
+            stat_acc += stats
+            nl_acc += blocks.level_counts[L]
+        end.record(stream)
+        torch.cuda.synchronize()
+    H.helios_sync(c)
+    total_ms = start.elapsed_time(end)
+    sample_ms = [evs[i][0].elapsed_time(evs[i][1]) for i in range(args.steps)]
+    gather_ms = [evs[i][1].elapsed_time(evs[i][2]) for i in range(args.steps)]
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    max_ms = float(t.item())
+    st = stat_acc.cpu().tolist()
+    n_rows = int(nl_acc.item())
+
+    # ---- e2e: through the public API with host buffers (pinned seeds in, counts out) ----
+    pin_seeds = {b: torch.as_tensor(inp.batches[b]).pin_memory() for b in sorted(set(seq))}
+    out_host = torch.empty(L + 1 + 4, dtype=torch.int64).pin_memory()
+    dseeds = torch.empty(cfg.B, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_e2e = time.perf_counter()
+    for i in range(args.steps):
+        b = seq[args.warmup + i]
+        dseeds.copy_(pin_seeds[b], non_blocking=True)
+        H.helios_batch_prepare(g, c, dseeds, cfg.fanouts, keys[b], blocks, feats, stats, stream)
+        out_host[: L + 1].copy_(blocks.level_counts, non_blocking=True)
+        out_host[L + 1:].copy_(stats, non_blocking=True)
+        stream.synchronize()
+    e2e_s = time.perf_counter() - t_e2e
+    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_t.item())
+
+    # ---- parity at full size: GPU batches vs the oracle, bit for bit (rank 0) ----
+    parity = None
+    cpu = None
+    if rank == 0 and not args.profile:
+        import oracle
+        checked, ok = 0, True
+        pb = sorted(set(seq))[: args.parity_batches]
+        for b in pb:
+            H.helios_batch_prepare(g, c, seed_of[b], cfg.fanouts, keys[b], blocks, feats, stats, stream)
+            H.helios_sync(c)
+            got = blocks.to_host()
+            ob = oracle.sample(inp.graph.indptr, inp.graph.indices, inp.batches[b], cfg.fanouts, keys[b])
+            ok &= np.array_equal(got["nodes"], ob.nodes)
+            for h in range(L):
+                ok &= np.array_equal(got["block_indptr"][h], ob.block_indptr[h])
+                ok &= np.array_equal(got["block_indices"][h], ob.block_indices[h])
+            ref = oracle.gather(ob.nodes, cfg.R, table=table)
+            ok &= np.array_equal(feats[: len(ob.nodes)].cpu().numpy(), ref)
+            checked += 1
+        parity = {"batches": checked, "bit_exact": bool(ok), "checks": "nodes, block CSR, feature bytes"}
+        if not args.no_cpu_baseline:
+            r = run_oracle_baseline(inp, keys, args.cpu_budget)
+            cpu = {"value": round(r["value"], 4), "unit": "batches/s", "cores": 1, "kind": "oracle",
+                   "sample": f"{r['batches']} batches of {cfg.name} (first of epoch 0), single-threaded C++ oracle "
+                             f"sample+gather from the canonical host table, {r['seconds']:.1f}s",
+                   "feature_gbs": round(r["gbs"], 3)}
+
+    # ---- roofline of the dominant kernel (lookup+gather, K3/K4) ----
+    pk = measured_peaks()
+    bw_hbm = float(pk.get("hbm_gbs", HBM_PEAK_FALLBACK))
+    bw_pcie = pcie_h2d_peak(torch) if rank == 0 else 0.0
+    bw_nvl = 770.0  # measured peer copy per direction (B200_PROFILING.md); 1 GPU runs have no peer rows
+    R = cfg.R
+    steps = args.steps
+    n_local, n_peer, n_host, n_file = (x / steps for x in st)
+    nL = n_rows / steps
+    hbm_bytes = R * n_local + R * nL + 16 * nL         # tier read + output write + nodes/dir reads
+    pcie_bytes = R * (n_host + n_file)
+    nvl_bytes = R * n_peer
+    g_ms = statistics.mean(gather_ms)
+    t_roof_ms = (hbm_bytes / bw_hbm + pcie_bytes / max(bw_pcie, 1e-9) + nvl_bytes / bw_nvl) / 1e6
+    alg_bytes = hbm_bytes + pcie_bytes + nvl_bytes
+    achieved = alg_bytes / (g_ms * 1e6)
+    peak_eff = alg_bytes / (t_roof_ms * 1e6)
+    dominant = max((("hbm", hbm_bytes / bw_hbm), ("pcie", pcie_bytes / max(bw_pcie, 1e-9)), ("nvlink", nvl_bytes / bw_nvl)),
+                   key=lambda x: x[1])[0]
+    value = world * steps / (max_ms / 1e3)
+    e2e_val = world * steps / e2e_s
+    launches_per_step = 1 + 5 * L + 1
+    out = {
+        "metric": "sampled+gathered mini-batches/sec (feature GB/s and tier-roofline fraction alongside)",
+        "value": round(value, 3), "unit": "batches/s", "n_gpus": world, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": round(max_ms / steps, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int64 ids / fp32 feature bytes (u8 copy)",
+        "data": "synthetic (seeded R-MAT-marginal power-law graph, synth_feature rows; no datasets)",
+        "config": {"workload": cfg.name, "desc": cfg.note, "V": cfg.V, "E": int(inp.graph.E), "dim": cfg.dim,
+                   "batch_per_rank": cfg.B, "fanouts": cfg.fanouts, "hbm_rows_per_gpu": Hr, "host_rows": S,
+                   "scale": s, "parallelism": f"dp{world} (seeds split per rank, HBM tier sharded)",
+                   "l2": "inputs larger than L2 (CSR %.1f GB, feature table %.1f GB); no flush" % (
+                       (inp.graph.E * 4 + cfg.V * 8) / 1e9, cfg.V * R / 1e9)},
+        "feature_gbs": round(world * n_rows / steps * R * steps / (max_ms / 1e3) / 1e9, 2),
+        "stage_ms": {"sample": round(statistics.mean(sample_ms), 4), "gather": round(g_ms, 4)},
+        "rows_per_batch": {"n_L": round(nL, 1), "hbm_local": round(n_local, 1), "hbm_peer": round(n_peer, 1),
+                           "host": round(n_host, 1), "file": round(n_file, 1)},
+        "roofline": {"bound": dominant, "kernel": "k_lookup_gather (K3+K4)", "achieved": round(achieved, 2),
+                     "peak": round(peak_eff, 2), "unit": "GB/s", "frac": round(t_roof_ms / g_ms, 4),
+                     "traffic": None,
+                     "peaks_used": {"hbm_gbs": bw_hbm, "hbm_src": "MEASURED_PEAKS.json" if pk else "fallback",
+                                    "pcie_gbs": round(bw_pcie, 2), "pcie_src": "pinned H2D copy measured in this run",
+                                    "nvlink_gbs": bw_nvl},
+                     "bytes_per_launch": {"hbm": round(hbm_bytes), "pcie": round(pcie_bytes), "nvlink": round(nvl_bytes)},
+                     "t_roof_ms": round(t_roof_ms, 4)},
+        "e2e": {"value": round(e2e_val, 3), "unit": "batches/s", "h2d_bytes_per_step": cfg.B * 8,
+                "d2h_bytes_per_step": (L + 1 + 4) * 8},
+        "gpu_launches": launches_per_step * steps,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "parity": parity,
+        "setup_s": {"inputs": round(gen_s, 1), "load_presample": round(presample_s, 1), "cache_build": round(build_s, 1)},
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    c.free()
+    g.free()
+    if world > 1:
+        dist.barrier()
+        if rank == 0:
+            for suf in ("_feat", "_indptr.npy", "_indices.npy"):
+                try:
+                    os.unlink(f"/dev/shm/{shm}{suf}")
+                except OSError:
+                    pass
+        dist.destroy_process_group()
+
+
+def reference_arm(args, cfg, rank, world):
+    """--impl reference: the oracle (the only reference this paper has) on the host cores."""
+    if rank != 0:
+        return
+    import oracle
+    t0 = time.time()
+    inp = workloads.make_inputs(cfg, table=True)
+    gen_s = time.time() - t0
+    keys = workloads.batch_keys(0, len(inp.batches))
+    full = [b for b in inp.batches if len(b) == cfg.B]
+    L = len(cfg.fanouts)
+    for i in range(args.warmup):
+        ob = oracle.sample(inp.graph.indptr, inp.graph.indices, full[i % len(full)], cfg.fanouts, keys[i % len(full)])
+        oracle.gather(ob.nodes, cfg.R, table=inp.table)
+    t1 = time.perf_counter()
+    rows = 0
+    for i in range(args.steps):
+        b = (args.warmup + i) % len(full)
+        ob = oracle.sample(inp.graph.indptr, inp.graph.indices, full[b], cfg.fanouts, keys[b])
+        oracle.gather(ob.nodes, cfg.R, table=inp.table)
+        rows += len(ob.nodes)
+    dt = time.perf_counter() - t1
+    v = args.steps / dt
+    print(json.dumps({
+        "impl": "reference", "metric": "sampled+gathered mini-batches/sec (feature GB/s and tier-roofline fraction alongside)",
+        "value": round(v, 4), "unit": "batches/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3 / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64 ids / fp32 feature bytes (u8 copy)", "data": "synthetic",
+        "config": {"workload": cfg.name, "desc": cfg.note, "V": cfg.V, "E": int(inp.graph.E), "dim": cfg.dim,
+                   "batch_per_rank": cfg.B, "fanouts": cfg.fanouts},
+        "feature_gbs": round(rows * cfg.R / dt / 1e9, 3),
+        "cpu_baseline": {"value": round(v, 4), "unit": "batches/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} full batches of {cfg.name}, single-threaded C++ oracle"},
+        "e2e": {"value": round(v, 4), "unit": "batches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": {"inputs": round(gen_s, 1)},
+    }), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,217 @@
+/* helios.h — C ABI v1 of libhelios.so: the B200 mini-batch preparation hot path of Helios
+ * (arXiv 2310.00837): multi-hop uniform neighbour sampling over a CSR graph, dedup/relabel into
+ * per-hop block CSRs, and feature extraction through a GPU-managed heterogeneous cache
+ * (HBM tier, pinned-host tier read zero-copy, file tier served by GPU-initiated IO rings).
+ *
+ * Citations are PAPER.md line (= LaTeX paragraph) numbers with their section; "reading N" refers to
+ * the numbered readings of the paper in DESIGN.md §Readings.
+ *
+ * Conventions for every entry point:
+ *   - Plain pointers and sizes only.  "device" = CUDA device memory of the handle's device,
+ *     "host" = ordinary host memory.  `stream` is a cudaStream_t passed as void* (NULL = legacy
+ *     default stream).
+ *   - Ownership: inputs of *_load / *_build are copied (or, where stated, registered and borrowed);
+ *     every output buffer is caller-owned and sized with helios_sample_bounds(); the library
+ *     writes only within the capacities it is given.
+ *   - Stream semantics: helios_sample / helios_gather / helios_batch_prepare / helios_presample
+ *     only ENQUEUE work on `stream` (internal side streams are joined back with events);
+ *     helios_graph_load / helios_cache_build / export / attach / *_sync / *_free block.
+ *   - Errors: synchronous argument checks return immediately with a status; device-detected
+ *     problems (seed out of range, duplicate seed, IO error, ring watchdog) are LATCHED in the
+ *     handle and returned by the next helios_graph_sync / helios_sync — that batch's outputs are
+ *     then undefined.  helios_last_error() gives a thread-local detail string.  No exception
+ *     crosses the ABI; the library never calls exit().
+ *   - Handles are not thread-safe: one handle per (process, device); calls on one handle must be
+ *     issued from one host thread, and sample calls on one graph handle must be stream-ordered
+ *     (they share the graph's sampling workspace).
+ *   - IDs: int64 at the ABI (reading 11); V < 2^31 and CSR indices are int32.
+ */
+#ifndef HELIOS_H_
+#define HELIOS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HELIOS_ABI_VERSION 1
+#define HELIOS_MAX_HOPS 8
+#define HELIOS_MAX_RANKS 64
+
+typedef enum {
+  HELIOS_OK = 0,
+  HELIOS_E_INVALID = 1,  /* malformed argument (bad CSR, row_bytes % 16, duplicate seed, ...) */
+  HELIOS_E_RANGE = 2,    /* an id >= V */
+  HELIOS_E_CAPACITY = 3, /* a caller buffer is smaller than helios_sample_bounds() requires */
+  HELIOS_E_NOMEM = 4,    /* device / pinned allocation failed */
+  HELIOS_E_CUDA = 5,     /* a CUDA runtime call failed (detail in helios_last_error) */
+  HELIOS_E_IO = 6,       /* feature-file read failed or was short */
+  HELIOS_E_TIMEOUT = 7,  /* IO ring watchdog fired (no completion within the bound) */
+  HELIOS_E_STATE = 8     /* handle unusable after an earlier latched failure / wrong call order */
+} helios_status;
+
+typedef struct helios_graph helios_graph; /* opaque: device CSR + sampling workspace + latched error */
+typedef struct helios_cache helios_cache; /* opaque: directory, tiers, IO rings, IO worker threads */
+
+int helios_abi_version(void);
+/* Thread-local detail of the last failing call on this thread ("" if none). */
+const char* helios_last_error(void);
+
+/* ---- Graph ---------------------------------------------------------------------------------
+ * helios_graph_load: validates and uploads the CSR topology (the paper keeps "the entire topology
+ * data" resident, §3.2.1; we keep it in HBM by default).
+ *   device   CUDA device ordinal the handle lives on (made current for the call).
+ *   V, E     vertex / edge counts; 1 <= V < 2^31, 0 <= E.
+ *   indptr   host int64[V+1]: indptr[0] = 0, non-decreasing, indptr[V] = E  (else E_INVALID).
+ *   indices  host int32[E]: neighbour ids, each in [0, V)  (else E_RANGE).  Copied.
+ *   flags    reserved, pass 0.
+ *   out      receives the handle (free with helios_graph_free).
+ * Blocking.  Validation runs on the GPU after the copy. */
+helios_status helios_graph_load(int device, int64_t V, int64_t E, const int64_t* indptr, const int32_t* indices,
+                                uint32_t flags, helios_graph** out);
+void helios_graph_free(helios_graph* g);
+helios_status helios_graph_info(const helios_graph* g, int64_t* V, int64_t* E, int* device);
+/* Device pointers of the resident CSR (for tests / zero-copy consumers); borrowed, valid until free. */
+helios_status helios_graph_device_csr(const helios_graph* g, const int64_t** indptr, const int32_t** indices);
+
+/* ---- Sampling (K1 sample_hop + K2 dedup_relabel) ------------------------------------------
+ * Worst-case output sizes for a batch of n_seeds seeds with the given fanouts (f_h = -1: all
+ * neighbours):  n_0 = n_seeds,  e_h <= min(n_h * f_h, E),  n_{h+1} <= min(V, n_h + e_h).
+ *   max_level_nodes [L+1] host out: bound on n_h;  max_edges [L] host out: bound on e_h.
+ *   *max_nodes = max_level_nodes[L]. */
+helios_status helios_sample_bounds(int64_t n_seeds, const int32_t* fanouts, int32_t L, int64_t V, int64_t E,
+                                   int64_t* max_nodes, int64_t* max_level_nodes, int64_t* max_edges);
+
+/* Output of one sampled mini-batch ("batch generation", §3.3).  All
+ * pointers are caller-owned DEVICE buffers; caps are element counts.
+ *   nodes            int64[nodes_cap]: N_L — N_0 = seeds, then every newly reached id in
+ *                    first-occurrence order over (hop, row, slot) (readings 5-6); N_h is a prefix.
+ *   level_counts     int64[L+1]: n_0..n_L (device scalars written by the kernels).
+ *   edge_counts      int64[L]: e_0..e_{L-1}.
+ *   block_indptr[h]  int32[indptr_cap[h]] (>= n_h + 1): row i of hop h = frontier node N_h[i].
+ *   block_indices[h] int32[edges_cap[h]]: local ids (rows of N_{h+1}) of the sampled neighbours,
+ *                    slot order j = 0..k-1 within each row. */
+typedef struct {
+  int64_t* nodes;
+  int64_t nodes_cap;
+  int64_t* level_counts;
+  int64_t* edge_counts;
+  int32_t* block_indptr[HELIOS_MAX_HOPS];
+  int64_t indptr_cap[HELIOS_MAX_HOPS];
+  int32_t* block_indices[HELIOS_MAX_HOPS];
+  int64_t edges_cap[HELIOS_MAX_HOPS];
+} helios_blocks;
+
+/* helios_sample: L-hop uniform neighbour sampling without replacement ("2-hop random neighbor
+ * sampling", PAPER.md:292 §4.1; GPU sampling operator PAPER.md:215 §3.2.2, :239 §3.3).
+ * For hop h and every row i < n_h (frontier = all of N_h, reading 5), v = N_h[i], d = deg(v),
+ * k = min(d, f_h): all neighbours in CSR order if k == d, else Floyd's k-subset (reading 3) with
+ * draws t_j = mulhi32(Philox4x32-10(ctr={j>>2, h, lo32 v, hi32 v}, key={lo32 key, hi32 key})[j&3],
+ * d-k+j+1) (reading 2).  Then dedup/relabel into N_{h+1} (reading 6).
+ *   g        graph handle.
+ *   seeds    device int64[n_seeds], distinct, each < V (violations latched: E_INVALID / E_RANGE).
+ *   fanouts  host int32[L], each >= 1 or -1.  L in [0, HELIOS_MAX_HOPS].
+ *   key      64-bit batch key (keys are inputs; bench/test keys come from synth.batch_key).
+ *   out      caller buffers with caps >= helios_sample_bounds() (else E_CAPACITY, nothing enqueued).
+ * Enqueue-only on `stream`.  The graph's sampling workspace is allocated on first use for the
+ * largest bounds seen (that first call synchronises the device). */
+helios_status helios_sample(helios_graph* g, const int64_t* seeds, int64_t n_seeds, const int32_t* fanouts, int32_t L,
+                            uint64_t key, const helios_blocks* out, void* stream);
+
+/* Waits for `stream`, then returns and clears the graph's latched device error (HELIOS_OK if none). */
+helios_status helios_graph_sync(helios_graph* g, void* stream);
+
+/* helios_presample: one pass of pre-sampling that "collects all vertices' hotness" (PAPER.md:212
+ * §3.2.2 Cache Initialization; reading 8).  Seeds are split into consecutive batches of `batch`
+ * (last one may be short); batch b is sampled with keys[b]; hotness[v] += 1 for every v in that
+ * batch's N_L.
+ *   seeds     device int64[n_seeds];  keys host uint64[ceil(n_seeds / batch)].
+ *   hotness   device uint64[V], ACCUMULATED (zero it first; all-reduce across ranks if the
+ *             presample pass is split over ranks — the Python layer does that over NCCL).
+ * Enqueue-only. */
+helios_status helios_presample(helios_graph* g, const int64_t* seeds, int64_t n_seeds, int32_t batch,
+                               const int32_t* fanouts, int32_t L, const uint64_t* keys, uint64_t* hotness, void* stream);
+
+/* ---- Heterogeneous cache (§3.2) ------------------------------------------
+ * Directory word per vertex (int64): bits 63..62 tier (0 HBM, 1 HOST, 2 FILE),
+ * bits 61..56 owner rank (HBM tier), bits 55..0 slot (HBM/HOST) or file row (FILE).
+ * Placement (reading 9): order = vertices sorted by hotness desc, id asc; hot rank r:
+ *   r <  G*H        -> HBM(owner = r mod G, slot = r div G)      G = world_size, H = hbm_rows
+ *   r <  G*H + S    -> HOST(slot = (flags & HOST_ALIAS) ? v : r - G*H)            S = host_rows
+ *   otherwise       -> FILE(row = v): bytes [header + v*stride, +row_bytes) of feature_path. */
+#define HELIOS_CACHE_HOST_ALIAS 0x1u     /* host tier IS host_table (slot = v); no second copy   */
+#define HELIOS_CACHE_TABLE_MAPPED 0x2u   /* host_table is already cudaHostRegister'ed + mapped   */
+#define HELIOS_CACHE_NO_DIRECT_IO 0x4u   /* open feature_path without O_DIRECT                    */
+#define HELIOS_CACHE_IO_FAULT_AT 0x100u  /* test builds: IO workers fail the io_fault_at-th read  */
+
+typedef struct {
+  int32_t row_bytes;          /* R = dim * 4 for fp32 features; multiple of 16 (else E_INVALID) */
+  int32_t world_size, rank;   /* HBM tier sharded round-robin by hot rank over world_size GPUs  */
+  int64_t hbm_rows;           /* H: HBM-tier rows held by EACH rank                              */
+  int64_t host_rows;          /* S: pinned-host-tier rows (one shared tier)                      */
+  const uint64_t* hotness;    /* device uint64[V] (helios_presample output, already all-reduced) */
+  const void* host_table;     /* host: canonical rows, row v at host_table + v*R (V*R bytes), or NULL;
+                                 borrowed (registered + mapped unless TABLE_MAPPED); must outlive the cache */
+  const char* feature_path;   /* canonical feature file or NULL (required iff G*H + S < V and no
+                                 host_table covers the FILE rows... FILE-tier rows are ALWAYS read from it) */
+  int64_t header_bytes;       /* file: byte offset of row 0                                      */
+  int64_t file_stride;        /* file: bytes between rows (>= R; 512-multiple for O_DIRECT)      */
+  int32_t io_rings;           /* number of SQ/CQ ring pairs = host IO worker threads (>= 1)      */
+  int32_t ring_depth;         /* entries per ring, power of two                                  */
+  int32_t io_ctas;            /* CTA budget of each IO kernel (submit / complete); paper: 32 */
+  int32_t io_fault_at;        /* with HELIOS_CACHE_IO_FAULT_AT: 1-based read index that fails   */
+  uint32_t flags;
+} helios_cache_desc;
+
+/* Builds the directory and fills the tiers (blocking).  The HBM tier is filled from host_table
+ * when given, else from feature_path; a packed host tier likewise.  Starts the IO workers when
+ * any vertex is FILE-tier.  The graph handle must outlive the cache. */
+helios_status helios_cache_build(helios_graph* g, const helios_cache_desc* desc, helios_cache** out);
+void helios_cache_free(helios_cache* c);
+
+typedef struct {
+  const int64_t* dir;         /* device int64[V] directory                                      */
+  const void* hbm_tier;       /* device [hbm_rows, R] this rank's shard                         */
+  const void* host_tier;      /* host pointer of the host tier (alias of host_table or packed)   */
+  int64_t V, hbm_rows, host_rows, file_rows;
+  int32_t row_bytes, world_size, rank, peers_attached;
+  int32_t io_rings, ring_depth, direct_io;
+  int64_t io_reads;           /* file reads completed by the IO workers since build */
+} helios_cache_info;
+helios_status helios_cache_query(const helios_cache* c, helios_cache_info* out);
+
+/* Multi-GPU: export this rank's HBM shard (CUDA IPC handle + sizes) into `blob`
+ * (*bytes in: capacity, out: size; call with blob = NULL to get the size), all-gather the blobs
+ * (Python layer, NCCL), then attach: blobs = world_size consecutive blobs of `blob_bytes` each, in
+ * rank order.  After attach, HBM rows owned by peers are read directly over NVLink. */
+helios_status helios_cache_export(helios_cache* c, void* blob, size_t* bytes);
+helios_status helios_cache_attach_peers(helios_cache* c, const void* blobs, size_t blob_bytes);
+
+/* ---- Feature extraction (K3 lookup + K4 gather + K5/K6 IO rings) -------------------------
+ * out[i, :] = row(nodes[i]) for i < *n_nodes, byte for byte.
+ *   nodes     device int64[max_nodes];  n_nodes device int64 scalar (e.g. level_counts + L).
+ *   out       device [max_nodes, row_bytes];  stats device helios_gather_stats or NULL (overwritten).
+ * Enqueue-only; FILE-tier rows go through the rings (thread-level submission, PAPER.md:167-172
+ * §3.1.1; asynchronous completion, §3.1.2) on internal streams joined back. */
+typedef struct {
+  int64_t rows_hbm_local, rows_hbm_peer, rows_host, rows_file;
+} helios_gather_stats;
+helios_status helios_gather(helios_cache* c, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, void* out,
+                            helios_gather_stats* stats, void* stream);
+
+/* One whole mini-batch: helios_sample followed by helios_gather of N_L into `features`
+ * (device [out->nodes_cap, row_bytes]).  Enqueue-only. */
+helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64_t* seeds, int64_t n_seeds,
+                                   const int32_t* fanouts, int32_t L, uint64_t key, const helios_blocks* out,
+                                   void* features, helios_gather_stats* stats, void* stream);
+
+/* Waits for `stream` and the cache's IO streams; returns and clears latched errors of the cache
+ * and its graph (E_IO, E_TIMEOUT, E_INVALID, E_RANGE). */
+helios_status helios_sync(helios_cache* c, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HELIOS_H_ */

@@ -1,0 +1,361 @@
+// abi.cu — extern "C" entry points of libhelios.so (declared and documented in include/helios.h).
+#include <algorithm>
+#include <cstdarg>
+#include <cstring>
+#include <new>
+
+#include "internal.cuh"
+
+namespace helios {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& s) { g_last_error = s; }
+
+helios_status fail(helios_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, helios_cache* c);
+helios_status cache_ensure_miss_cap(helios_cache* c, int64_t max_nodes);
+void cache_free_impl(helios_cache* c);
+
+static helios_status read_latched(int* d_err, helios_status* out) {
+  int h = 0;
+  HCUDA(cudaMemcpy(&h, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h) HCUDA(cudaMemset(d_err, 0, sizeof(int)));
+  *out = (helios_status)h;
+  return HELIOS_OK;
+}
+
+}  // namespace helios
+
+using namespace helios;
+
+#define GUARD_BEGIN try {
+#define GUARD_END                                                   \
+  }                                                                 \
+  catch (const std::bad_alloc&) {                                   \
+    return fail(HELIOS_E_NOMEM, "host allocation failed");          \
+  }                                                                 \
+  catch (...) {                                                     \
+    return fail(HELIOS_E_STATE, "unexpected C++ exception");        \
+  }
+
+extern "C" {
+
+int helios_abi_version(void) { return HELIOS_ABI_VERSION; }
+
+const char* helios_last_error(void) { return helios::g_last_error.c_str(); }
+
+helios_status helios_graph_load(int device, int64_t V, int64_t E, const int64_t* indptr, const int32_t* indices,
+                                uint32_t flags, helios_graph** out) {
+  GUARD_BEGIN
+  (void)flags;
+  HCHECK(out, HELIOS_E_INVALID, "out is NULL");
+  *out = nullptr;
+  HCHECK(V >= 1 && V < (1ll << 31), HELIOS_E_INVALID, "V=%lld out of [1, 2^31)", (long long)V);
+  HCHECK(E >= 0 && indptr && (E == 0 || indices), HELIOS_E_INVALID, "bad E / null arrays");
+  HCHECK(indptr[0] == 0 && indptr[V] == E, HELIOS_E_INVALID, "indptr[0]=%lld indptr[V]=%lld E=%lld",
+         (long long)indptr[0], (long long)indptr[V], (long long)E);
+  int ndev = 0;
+  HCUDA(cudaGetDeviceCount(&ndev));
+  HCHECK(device >= 0 && device < ndev, HELIOS_E_INVALID, "device %d of %d", device, ndev);
+  DeviceGuard dg(device);
+  helios_graph* g = new helios_graph();
+  g->device = device;
+  g->V = V;
+  g->E = E;
+  cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, device);
+  auto cleanup = [&](helios_status st) {
+    if (g->indptr) cudaFree(g->indptr);
+    if (g->indices) cudaFree(g->indices);
+    if (g->d_err) cudaFree(g->d_err);
+    delete g;
+    return st;
+  };
+  if (cudaMalloc(&g->indptr, (V + 1) * 8) != cudaSuccess || cudaMalloc(&g->indices, std::max<int64_t>(E, 1) * 4) != cudaSuccess ||
+      cudaMalloc(&g->d_err, sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    return cleanup(fail(HELIOS_E_NOMEM, "device allocation of the CSR (%lld B) failed", (long long)(V * 8 + E * 4)));
+  }
+  if (cudaMemcpy(g->indptr, indptr, (V + 1) * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+      (E > 0 && cudaMemcpy(g->indices, indices, E * 4, cudaMemcpyHostToDevice) != cudaSuccess) ||
+      cudaMemset(g->d_err, 0, sizeof(int)) != cudaSuccess)
+    return cleanup(fail(HELIOS_E_CUDA, "CSR upload failed: %s", cudaGetErrorString(cudaGetLastError())));
+  helios_status st = validate_csr_device(g->indptr, g->indices, V, E, g->d_err, 0);
+  if (st != HELIOS_OK) return cleanup(st);
+  helios_status lat = HELIOS_OK;
+  if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(fail(HELIOS_E_CUDA, "validate: %s", cudaGetErrorString(cudaGetLastError())));
+  st = read_latched(g->d_err, &lat);
+  if (st != HELIOS_OK) return cleanup(st);
+  if (lat != HELIOS_OK)
+    return cleanup(fail(lat, lat == HELIOS_E_RANGE ? "CSR index >= V" : "CSR indptr not monotone / inconsistent"));
+  *out = g;
+  return HELIOS_OK;
+  GUARD_END
+}
+
+void helios_graph_free(helios_graph* g) {
+  if (!g) return;
+  DeviceGuard dg(g->device);
+  cudaDeviceSynchronize();
+  cudaFree(g->indptr);
+  cudaFree(g->indices);
+  cudaFree(g->d_err);
+  if (g->ws.reset_base) cudaFree(g->ws.reset_base);
+  if (g->ws.slot_of) cudaFree(g->ws.slot_of);
+  if (g->pre_mem) cudaFree(g->pre_mem);
+  delete g;
+}
+
+helios_status helios_graph_info(const helios_graph* g, int64_t* V, int64_t* E, int* device) {
+  HCHECK(g, HELIOS_E_INVALID, "null graph");
+  if (V) *V = g->V;
+  if (E) *E = g->E;
+  if (device) *device = g->device;
+  return HELIOS_OK;
+}
+
+helios_status helios_graph_device_csr(const helios_graph* g, const int64_t** indptr, const int32_t** indices) {
+  HCHECK(g, HELIOS_E_INVALID, "null graph");
+  if (indptr) *indptr = g->indptr;
+  if (indices) *indices = g->indices;
+  return HELIOS_OK;
+}
+
+helios_status helios_sample_bounds(int64_t n_seeds, const int32_t* fanouts, int32_t L, int64_t V, int64_t E,
+                                   int64_t* max_nodes, int64_t* max_level_nodes, int64_t* max_edges) {
+  GUARD_BEGIN
+  return sample_bounds(n_seeds, fanouts, L, V, E, max_nodes, max_level_nodes, max_edges);
+  GUARD_END
+}
+
+helios_status helios_sample(helios_graph* g, const int64_t* seeds, int64_t n_seeds, const int32_t* fanouts, int32_t L,
+                            uint64_t key, const helios_blocks* out, void* stream) {
+  GUARD_BEGIN
+  HCHECK(g, HELIOS_E_INVALID, "null graph");
+  DeviceGuard dg(g->device);
+  return sample_enqueue(g, seeds, n_seeds, fanouts, L, key, out, (cudaStream_t)stream);
+  GUARD_END
+}
+
+helios_status helios_graph_sync(helios_graph* g, void* stream) {
+  GUARD_BEGIN
+  HCHECK(g, HELIOS_E_INVALID, "null graph");
+  DeviceGuard dg(g->device);
+  HCUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  helios_status lat = HELIOS_OK;
+  helios_status st = read_latched(g->d_err, &lat);
+  if (st != HELIOS_OK) return st;
+  if (lat != HELIOS_OK) return fail(lat, "latched device error %d (seed out of range / duplicate seed)", (int)lat);
+  return HELIOS_OK;
+  GUARD_END
+}
+
+helios_status helios_presample(helios_graph* g, const int64_t* seeds, int64_t n_seeds, int32_t batch,
+                               const int32_t* fanouts, int32_t L, const uint64_t* keys, uint64_t* hotness, void* stream) {
+  GUARD_BEGIN
+  HCHECK(g && hotness && keys && batch > 0 && (n_seeds == 0 || seeds), HELIOS_E_INVALID, "bad presample arguments");
+  DeviceGuard dg(g->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t maxn, lvl[HELIOS_MAX_HOPS + 1], edg[HELIOS_MAX_HOPS];
+  helios_status s = sample_bounds(batch, fanouts, L, g->V, g->E, &maxn, lvl, edg);
+  if (s != HELIOS_OK) return s;
+  bool same = (g->pre_mem && g->pre_cap_B >= batch && g->pre_L == L);
+  for (int h = 0; same && h < L; h++) same = (g->pre_fan[h] == fanouts[h]);
+  if (!same) {
+    HCUDA(cudaDeviceSynchronize());
+    if (g->pre_mem) cudaFree(g->pre_mem);
+    g->pre_mem = nullptr;
+    size_t bytes = maxn * 8 + (L + 1) * 8 + HELIOS_MAX_HOPS * 8;
+    for (int h = 0; h < L; h++) bytes += (lvl[h] + 1) * 4 + edg[h] * 4 + 64;
+    HCUDA(cudaMalloc(&g->pre_mem, bytes));
+    char* p = (char*)g->pre_mem;
+    helios_blocks& b = g->pre_blocks;
+    b = helios_blocks{};
+    b.nodes = (int64_t*)p;
+    b.nodes_cap = maxn;
+    p += maxn * 8;
+    b.level_counts = (int64_t*)p;
+    p += (L + 1) * 8;
+    b.edge_counts = (int64_t*)p;
+    p += HELIOS_MAX_HOPS * 8;
+    for (int h = 0; h < L; h++) {
+      b.block_indptr[h] = (int32_t*)p;
+      b.indptr_cap[h] = lvl[h] + 1;
+      p += ((lvl[h] + 1) * 4 + 31) / 32 * 32;
+      b.block_indices[h] = (int32_t*)p;
+      b.edges_cap[h] = edg[h];
+      p += (edg[h] * 4 + 31) / 32 * 32;
+    }
+    g->pre_cap_B = batch;
+    g->pre_L = L;
+    for (int h = 0; h < L; h++) g->pre_fan[h] = fanouts[h];
+  }
+  for (int64_t b = 0, i = 0; i < n_seeds; b++, i += batch) {
+    int64_t nb = std::min<int64_t>(batch, n_seeds - i);
+    s = sample_enqueue(g, seeds + i, nb, fanouts, L, keys[b], &g->pre_blocks, st);
+    if (s != HELIOS_OK) return s;
+    s = hot_count_enqueue(g->pre_blocks.nodes, g->pre_blocks.level_counts + L, maxn, hotness, g->sms, st);
+    if (s != HELIOS_OK) return s;
+  }
+  return HELIOS_OK;
+  GUARD_END
+}
+
+helios_status helios_cache_build(helios_graph* g, const helios_cache_desc* d, helios_cache** out) {
+  GUARD_BEGIN
+  HCHECK(g && d && out, HELIOS_E_INVALID, "null argument");
+  *out = nullptr;
+  HCHECK(d->row_bytes > 0 && d->row_bytes % 16 == 0, HELIOS_E_INVALID, "row_bytes %d not a positive multiple of 16",
+         d->row_bytes);
+  HCHECK(d->world_size >= 1 && d->world_size <= HELIOS_MAX_RANKS && d->rank >= 0 && d->rank < d->world_size,
+         HELIOS_E_INVALID, "rank %d / world_size %d", d->rank, d->world_size);
+  HCHECK(d->hbm_rows >= 0 && d->host_rows >= 0, HELIOS_E_INVALID, "negative tier size");
+  HCHECK(d->hotness, HELIOS_E_INVALID, "hotness is NULL");
+  DeviceGuard dg(g->device);
+  helios_cache* c = new helios_cache();
+  helios_status st = cache_build_impl(g, d, c);
+  if (st != HELIOS_OK) {
+    std::string keep = helios_last_error();
+    cache_free_impl(c);
+    delete c;
+    set_error(keep);
+    return st;
+  }
+  *out = c;
+  return HELIOS_OK;
+  GUARD_END
+}
+
+void helios_cache_free(helios_cache* c) {
+  if (!c) return;
+  DeviceGuard dg(c->device);
+  cache_free_impl(c);
+  delete c;
+}
+
+helios_status helios_cache_query(const helios_cache* c, helios_cache_info* o) {
+  HCHECK(c && o, HELIOS_E_INVALID, "null argument");
+  o->dir = c->dir;
+  o->hbm_tier = c->hbm;
+  o->host_tier = c->host_tier;
+  o->V = c->V;
+  o->hbm_rows = c->H;
+  o->host_rows = c->S;
+  o->file_rows = c->file_rows;
+  o->row_bytes = c->R;
+  o->world_size = c->G;
+  o->rank = c->rank;
+  o->peers_attached = c->peers_attached;
+  o->io_rings = c->io.rings;
+  o->ring_depth = c->io.depth;
+  o->direct_io = c->io.direct ? 1 : 0;
+  o->io_reads = c->io.reads.load();
+  return HELIOS_OK;
+}
+
+struct ExportBlob {
+  uint32_t magic;
+  int32_t rank, world, R;
+  int64_t H;
+  cudaIpcMemHandle_t handle;
+};
+
+helios_status helios_cache_export(helios_cache* c, void* blob, size_t* bytes) {
+  GUARD_BEGIN
+  HCHECK(c && bytes, HELIOS_E_INVALID, "null argument");
+  if (!blob) {
+    *bytes = sizeof(ExportBlob);
+    return HELIOS_OK;
+  }
+  HCHECK(*bytes >= sizeof(ExportBlob), HELIOS_E_CAPACITY, "blob capacity %zu < %zu", *bytes, sizeof(ExportBlob));
+  DeviceGuard dg(c->device);
+  ExportBlob b{};
+  b.magic = 0x48454C31u;
+  b.rank = c->rank;
+  b.world = c->G;
+  b.R = c->R;
+  b.H = c->H;
+  HCUDA(cudaIpcGetMemHandle(&b.handle, c->hbm));
+  memcpy(blob, &b, sizeof(b));
+  *bytes = sizeof(b);
+  return HELIOS_OK;
+  GUARD_END
+}
+
+helios_status helios_cache_attach_peers(helios_cache* c, const void* blobs, size_t blob_bytes) {
+  GUARD_BEGIN
+  HCHECK(c && blobs && blob_bytes >= sizeof(ExportBlob), HELIOS_E_INVALID, "bad attach arguments");
+  DeviceGuard dg(c->device);
+  for (int r = 0; r < c->G; r++) {
+    ExportBlob b;
+    memcpy(&b, (const char*)blobs + (size_t)r * blob_bytes, sizeof(b));
+    HCHECK(b.magic == 0x48454C31u && b.rank == r && b.world == c->G && b.R == c->R && b.H == c->H, HELIOS_E_INVALID,
+           "blob %d inconsistent (rank %d world %d R %d H %lld)", r, b.rank, b.world, b.R, (long long)b.H);
+    if (r == c->rank) continue;
+    if (c->peer_ptrs[r]) continue;
+    void* p = nullptr;
+    HCUDA(cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess));
+    c->peer_ptrs[r] = (char*)p;
+  }
+  HCUDA(cudaMemcpy(c->d_peers, c->peer_ptrs, HELIOS_MAX_RANKS * sizeof(char*), cudaMemcpyHostToDevice));
+  c->peers_attached = 1;
+  return HELIOS_OK;
+  GUARD_END
+}
+
+helios_status helios_gather(helios_cache* c, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, void* out,
+                            helios_gather_stats* stats, void* stream) {
+  GUARD_BEGIN
+  HCHECK(c, HELIOS_E_INVALID, "null cache");
+  DeviceGuard dg(c->device);
+  helios_status st = cache_ensure_miss_cap(c, max_nodes);
+  if (st != HELIOS_OK) return st;
+  return gather_enqueue(c, nodes, n_nodes, max_nodes, out, stats, (cudaStream_t)stream);
+  GUARD_END
+}
+
+helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64_t* seeds, int64_t n_seeds,
+                                   const int32_t* fanouts, int32_t L, uint64_t key, const helios_blocks* out,
+                                   void* features, helios_gather_stats* stats, void* stream) {
+  GUARD_BEGIN
+  HCHECK(g && c && out, HELIOS_E_INVALID, "null argument");
+  HCHECK(c->g == g, HELIOS_E_INVALID, "cache was built on another graph");
+  DeviceGuard dg(g->device);
+  helios_status st = sample_enqueue(g, seeds, n_seeds, fanouts, L, key, out, (cudaStream_t)stream);
+  if (st != HELIOS_OK) return st;
+  st = cache_ensure_miss_cap(c, out->nodes_cap);
+  if (st != HELIOS_OK) return st;
+  return gather_enqueue(c, out->nodes, out->level_counts + L, out->nodes_cap, features, stats, (cudaStream_t)stream);
+  GUARD_END
+}
+
+helios_status helios_sync(helios_cache* c, void* stream) {
+  GUARD_BEGIN
+  HCHECK(c, HELIOS_E_INVALID, "null cache");
+  DeviceGuard dg(c->device);
+  HCUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  if (c->s_submit) HCUDA(cudaStreamSynchronize(c->s_submit));
+  if (c->s_complete) HCUDA(cudaStreamSynchronize(c->s_complete));
+  helios_status a = HELIOS_OK, b = HELIOS_OK;
+  helios_status st = read_latched(c->d_err, &a);
+  if (st != HELIOS_OK) return st;
+  st = read_latched(c->g->d_err, &b);
+  if (st != HELIOS_OK) return st;
+  int host = c->io.host_err.exchange(0);
+  if (a != HELIOS_OK) return fail(a, "latched cache error %d (IO failure or ring watchdog)", (int)a);
+  if (host != 0) return fail((helios_status)host, "IO worker reported error %d", host);
+  if (b != HELIOS_OK) return fail(b, "latched sampling error %d (seed out of range / duplicate seed)", (int)b);
+  return HELIOS_OK;
+  GUARD_END
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+// device.cuh — device-side primitives: Philox4x32-10, hash probing, decoupled look-back tile scan.
+#pragma once
+
+#include <cub/block/block_scan.cuh>
+
+#include "internal.cuh"
+
+namespace helios {
+
+// Philox4x32-10 (Salmon et al., SC'11), reading 2: counter {j>>2, h, lo32 v, hi32 v}, key = batch key.
+__device__ __forceinline__ uint32_t philox_word(uint64_t key, uint32_t h, uint64_t v, uint32_t j) {
+  uint32_t c0 = j >> 2, c1 = h, c2 = (uint32_t)v, c3 = (uint32_t)(v >> 32);
+  uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  uint32_t w = j & 3;
+  return w == 0 ? c0 : (w == 1 ? c1 : (w == 2 ? c2 : c3));
+}
+
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x85EBCA6Bu;
+  x ^= x >> 13;
+  x *= 0xC2B2AE35u;
+  x ^= x >> 16;
+  return x;
+}
+
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
+// Open-addressing (linear probing) insert-or-find of key u; returns the slot, *fresh = created here.
+__device__ __forceinline__ uint32_t table_insert(uint32_t* keys, uint32_t mask, uint32_t u, bool* fresh) {
+  uint32_t s = hash32(u) & mask;
+  for (;;) {
+    uint32_t k = ld_volatile_u32(keys + s);
+    if (k == u) {
+      *fresh = false;
+      return s;
+    }
+    if (k == kEmpty) {
+      uint32_t prev = atomicCAS(keys + s, kEmpty, u);
+      if (prev == kEmpty) {
+        *fresh = true;
+        return s;
+      }
+      if (prev == u) {
+        *fresh = false;
+        return s;
+      }
+    }
+    s = (s + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ void latch(int* err, int code) {
+  if (code) atomicCAS(err, 0, code);
+}
+
+constexpr unsigned long long kStatusInvalid = ~0ull;
+constexpr unsigned long long kStatusIncl = 1ull << 62;
+
+// Tile ticket: counter starts at all-ones, so the first ticket is 0.  Call from every thread.
+__device__ __forceinline__ unsigned tile_ticket(const ScanState& s, unsigned* sm) {
+  if (threadIdx.x == 0) *sm = atomicAdd(s.counter, 1u) + 1u;
+  __syncthreads();
+  return *sm;
+}
+
+// Decoupled look-back (Merrill & Garland 2016): publish this tile's aggregate, walk back to the
+// nearest inclusive prefix, publish our inclusive prefix; returns the exclusive prefix of the tile.
+__device__ __forceinline__ long long tile_lookback(const ScanState& s, unsigned tile, long long agg, long long* sm) {
+  if (threadIdx.x == 0) {
+    long long prefix = 0;
+    if (tile == 0) {
+      atomicExch(&s.status[0], kStatusIncl | (unsigned long long)agg);
+    } else {
+      atomicExch(&s.status[tile], (unsigned long long)agg);
+      long long acc = 0;
+      int j = (int)tile - 1;
+      for (;;) {
+        unsigned long long w = ld_volatile_u64(&s.status[j]);
+        if (w == kStatusInvalid) continue;
+        if (w & kStatusIncl) {
+          acc += (long long)(w & ~kStatusIncl);
+          break;
+        }
+        acc += (long long)w;
+        j--;
+      }
+      prefix = acc;
+      atomicExch(&s.status[tile], kStatusIncl | (unsigned long long)(acc + agg));
+    }
+    *sm = prefix;
+  }
+  __syncthreads();
+  return *sm;
+}
+
+}  // namespace helios

@@ -1,0 +1,365 @@
+// gather.cu — K3 cache_lookup fused with K4 gather_rows, and the K5/K6 IO rings.
+//
+// k_lookup_gather<VPL,U>: one warp per row, U rows in flight per warp, VPL 16-byte vectors per lane
+//   per row.  dir[v] resolves the row to its tier ("GPU threads directly access the
+//   cached data in CPU memory by UVA ... or in GPU memory"): HBM (local shard or a peer shard read
+//   over NVLink), HOST (pinned, mapped, read zero-copy over PCIe), or FILE (appended to the miss
+//   list for the IO rings).  Per-tier row counts are warp-reduced into helios_gather_stats.
+// k_io_submit: thread-level parallel IO command submission (§3.1.1) — every lane
+//   owns one request, requests are striped over several SQ rings, the descriptor carries the file
+//   offset (the "SSD logic block") and the staging slot (the "temporary IO buffer").
+// k_io_complete: asynchronous completion handling (§3.1.2) — each warp claims a
+//   request, polls its CQ entry (acquire, system scope), then the whole warp moves the row from the
+//   staging slot into the output feature buffer and frees the slot.
+#include <algorithm>
+
+#include "device.cuh"
+
+namespace helios {
+
+struct GatherArgs {
+  const int64_t* nodes;
+  const int64_t* n_nodes;
+  const int64_t* dir;
+  char* out;
+  int32_t R;
+  int32_t rank;
+  const char* hbm;          // this rank's shard
+  char* const* peers;       // device [G]
+  const char* host_dev;     // device alias of the host tier
+  int64_t* miss_out;
+  int64_t* miss_row;
+  unsigned long long* miss_count;
+  helios_gather_stats* stats;
+};
+
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+template <int VPL, int U>
+__global__ void __launch_bounds__(256) k_lookup_gather(GatherArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n = *a.n_nodes;
+  const int nvec = a.R >> 4;
+  long long c_local = 0, c_peer = 0, c_host = 0, c_file = 0;
+  for (int64_t base = warp * U; base < n; base += nwarps * U) {
+    // lane u < U resolves row base+u
+    const char* src = nullptr;
+    int tier = -1;
+    if (lane < U && base + lane < n) {
+      const int64_t i = base + lane;
+      const int64_t v = a.nodes[i];
+      const uint64_t w = (uint64_t)a.dir[v];
+      tier = (int)(w >> 62);
+      const int owner = (int)((w >> 56) & 63);
+      const int64_t slot = (int64_t)(w & ((1ull << 56) - 1));
+      if (tier == 0) {
+        if (owner == a.rank) {
+          src = a.hbm + slot * a.R;
+          c_local++;
+        } else {
+          src = a.peers[owner] + slot * a.R;
+          c_peer++;
+        }
+      } else if (tier == 1) {
+        src = a.host_dev + slot * a.R;
+        c_host++;
+      } else {
+        c_file++;
+        const unsigned long long m = atomicAdd(a.miss_count, 1ull);
+        a.miss_out[m] = i;
+        a.miss_row[m] = slot;
+      }
+    }
+    for (int c0 = 0; c0 < nvec; c0 += 32 * VPL) {
+      int4 r[U][VPL];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int4* s = (const int4*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)src, u);
+        const int t = __shfl_sync(0xFFFFFFFFu, tier, u);
+        if (t == 0 || t == 1) {
+#pragma unroll
+          for (int k = 0; k < VPL; k++) {
+            const int idx = c0 + lane + 32 * k;
+            if (idx < nvec) r[u][k] = ld_stream(s + idx);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int t = __shfl_sync(0xFFFFFFFFu, tier, u);
+        if (t == 0 || t == 1) {
+          int4* d = (int4*)(a.out + (base + u) * (int64_t)a.R);
+#pragma unroll
+          for (int k = 0; k < VPL; k++) {
+            const int idx = c0 + lane + 32 * k;
+            if (idx < nvec) d[idx] = r[u][k];
+          }
+        }
+      }
+    }
+  }
+  if (a.stats) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      c_local += __shfl_xor_sync(0xFFFFFFFFu, c_local, o);
+      c_peer += __shfl_xor_sync(0xFFFFFFFFu, c_peer, o);
+      c_host += __shfl_xor_sync(0xFFFFFFFFu, c_host, o);
+      c_file += __shfl_xor_sync(0xFFFFFFFFu, c_file, o);
+    }
+    if (lane == 0) {
+      if (c_local) atomicAdd((unsigned long long*)&a.stats->rows_hbm_local, (unsigned long long)c_local);
+      if (c_peer) atomicAdd((unsigned long long*)&a.stats->rows_hbm_peer, (unsigned long long)c_peer);
+      if (c_host) atomicAdd((unsigned long long*)&a.stats->rows_host, (unsigned long long)c_host);
+      if (c_file) atomicAdd((unsigned long long*)&a.stats->rows_file, (unsigned long long)c_file);
+    }
+  }
+}
+
+// Plain row copy by id (setup: HBM-tier fill from a mapped host table).
+__global__ void k_rows_by_id(const char* __restrict__ src, int32_t R, const int32_t* __restrict__ ids, int64_t n,
+                             char* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int nvec = R >> 4;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    const int4* s = (const int4*)(src + (int64_t)ids[i] * R);
+    int4* d = (int4*)(dst + i * (int64_t)R);
+    for (int k = lane; k < nvec; k += 32) d[k] = ld_stream(s + k);
+  }
+}
+
+helios_status gather_rows_by_id(const char* src_dev, int32_t R, const int32_t* ids, int64_t n, char* dst, int sms,
+                                cudaStream_t st) {
+  if (n <= 0) return HELIOS_OK;
+  k_rows_by_id<<<sms * 8, 256, 0, st>>>(src_dev, R, ids, n, dst);
+  HCUDA(cudaGetLastError());
+  return HELIOS_OK;
+}
+
+// ---- IO rings --------------------------------------------------------------------------------
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_gpu_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int4 ld_volatile_v4(const int4* p) {
+  int4 r;
+  asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+
+constexpr uint64_t kWatchdogNs = 30ull * 1000000000ull;
+
+struct IoArgs {
+  const int64_t* miss_out;
+  const int64_t* miss_row;
+  unsigned long long* ctl;   // [0] misses, [1] submit ticket, [2] complete ticket
+  SqEntry* sq;               // device alias of pinned SQ
+  CqEntry* cq;               // device alias of pinned CQ
+  const char* staging;       // device alias of pinned staging
+  uint32_t* free_seq;
+  const uint32_t* base_seq;
+  int rings, depth;
+  int64_t slot_bytes, header, stride;
+  int32_t len, R;
+  char* out;
+  int* err;
+};
+
+__global__ void __launch_bounds__(256) k_io_submit(IoArgs a) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long M = a.ctl[0];
+  const uint64_t t0 = globaltimer();
+  for (;;) {
+    unsigned long long tk = 0;
+    if (lane == 0) tk = atomicAdd(&a.ctl[1], 32ull);
+    tk = __shfl_sync(0xFFFFFFFFu, tk, 0);
+    if (tk >= M) break;
+    const unsigned long long m = tk + lane;
+    if (m < M) {
+      const int r = (int)(m % a.rings);
+      const uint32_t p = (uint32_t)(m / a.rings);
+      const uint32_t seq = a.base_seq[r] + p + 1u;
+      const uint32_t slot = (seq - 1u) & (uint32_t)(a.depth - 1);
+      const int64_t idx = (int64_t)r * a.depth + slot;
+      bool ok = true;
+      // slot reusable once its previous occupant (seq - depth) was consumed by io_complete
+      while ((int32_t)(seq - (uint32_t)a.depth - ld_acquire_gpu_u32(a.free_seq + idx)) > 0) {
+        if (globaltimer() - t0 > kWatchdogNs) {
+          latch(a.err, HELIOS_E_TIMEOUT);
+          ok = false;
+          break;
+        }
+        __nanosleep(256);
+      }
+      if (ok) {
+        SqEntry* e = a.sq + idx;
+        e->file_off = (uint64_t)(a.header + a.miss_row[m] * a.stride);
+        e->len = (uint32_t)a.len;
+        e->slot = (uint32_t)idx;
+        e->out_row = (uint64_t)a.miss_out[m];
+        __threadfence_system();
+        st_release_sys_u32(&e->seq, seq);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_io_complete(IoArgs a) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long M = a.ctl[0];
+  const int nvec = a.R >> 4;
+  const uint64_t t0 = globaltimer();
+  for (;;) {
+    unsigned long long m = 0;
+    if (lane == 0) m = atomicAdd(&a.ctl[2], 1ull);
+    m = __shfl_sync(0xFFFFFFFFu, m, 0);
+    if (m >= M) break;
+    const int r = (int)(m % a.rings);
+    const uint32_t p = (uint32_t)(m / a.rings);
+    const uint32_t seq = a.base_seq[r] + p + 1u;
+    const uint32_t slot = (seq - 1u) & (uint32_t)(a.depth - 1);
+    const int64_t idx = (int64_t)r * a.depth + slot;
+    bool ok = true;
+    while (ld_acquire_sys_u32(&a.cq[idx].seq) != seq) {  // every lane polls (one coalesced request)
+      if (globaltimer() - t0 > kWatchdogNs) {
+        ok = false;
+        break;
+      }
+      __nanosleep(128);
+    }
+    ok = __all_sync(0xFFFFFFFFu, ok);
+    if (!ok) {
+      if (lane == 0) latch(a.err, HELIOS_E_TIMEOUT);
+      break;
+    }
+    const int st = *(volatile const int32_t*)&a.cq[idx].status;
+    if (st != 0) {
+      if (lane == 0) latch(a.err, HELIOS_E_IO);
+    } else {
+      const int4* s = (const int4*)(a.staging + idx * a.slot_bytes);
+      int4* d = (int4*)(a.out + a.miss_out[m] * (int64_t)a.R);
+      for (int k = lane; k < nvec; k += 32) d[k] = ld_volatile_v4(s + k);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      st_release_gpu_u32(a.free_seq + idx, seq);
+    }
+  }
+}
+
+__global__ void k_io_finish(unsigned long long* ctl, uint32_t* base_seq, int rings) {
+  const unsigned long long M = ctl[0];
+  for (int r = threadIdx.x; r < rings; r += blockDim.x)
+    base_seq[r] += (uint32_t)(M / rings + ((unsigned long long)r < M % rings ? 1 : 0));
+}
+
+// The IO kernels wait on each other while running concurrently, so they must not be lazily
+// loaded (CUDA 12 lazy loading may wait for the running kernel before loading the other one).
+helios_status io_preload_kernels() {
+  cudaFuncAttributes fa;
+  HCUDA(cudaFuncGetAttributes(&fa, k_io_submit));
+  HCUDA(cudaFuncGetAttributes(&fa, k_io_complete));
+  HCUDA(cudaFuncGetAttributes(&fa, k_io_finish));
+  return HELIOS_OK;
+}
+
+template <int VPL, int U>
+static void launch_gather(const GatherArgs& a, int sms, cudaStream_t st) {
+  k_lookup_gather<VPL, U><<<sms * 8, 256, 0, st>>>(a);
+}
+
+helios_status gather_enqueue(helios_cache* c, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, void* out,
+                             helios_gather_stats* stats, cudaStream_t st) {
+  HCHECK(nodes && n_nodes && (out || max_nodes == 0), HELIOS_E_INVALID, "null gather argument");
+  HCHECK(c->G == 1 || c->peers_attached, HELIOS_E_STATE, "world_size %d but peers not attached", c->G);
+  HCHECK(!c->has_file || max_nodes <= c->io.miss_cap, HELIOS_E_CAPACITY, "max_nodes %lld > miss list cap %lld",
+         (long long)max_nodes, (long long)c->io.miss_cap);
+  if (stats) HCUDA(cudaMemsetAsync(stats, 0, sizeof(helios_gather_stats), st));
+  GatherArgs a;
+  a.nodes = nodes;
+  a.n_nodes = n_nodes;
+  a.dir = c->dir;
+  a.out = (char*)out;
+  a.R = c->R;
+  a.rank = c->rank;
+  a.hbm = c->hbm;
+  a.peers = c->d_peers;
+  a.host_dev = c->d_host_tier;
+  a.miss_out = c->io.d_miss_out;
+  a.miss_row = c->io.d_miss_row;
+  a.miss_count = c->io.d_ctl;
+  a.stats = stats;
+  if (c->has_file) HCUDA(cudaMemsetAsync(c->io.d_ctl, 0, 4 * sizeof(unsigned long long), st));
+  const int nvec = c->R / 16;
+  if (nvec <= 32) launch_gather<1, 4>(a, c->sms, st);
+  else if (nvec <= 64) launch_gather<2, 2>(a, c->sms, st);
+  else if (nvec <= 128) launch_gather<4, 1>(a, c->sms, st);
+  else launch_gather<8, 1>(a, c->sms, st);
+  HCUDA(cudaGetLastError());
+  if (c->has_file) {
+    IoArgs io;
+    io.miss_out = c->io.d_miss_out;
+    io.miss_row = c->io.d_miss_row;
+    io.ctl = c->io.d_ctl;
+    io.sq = c->io.d_sq;
+    io.cq = c->io.d_cq;
+    io.staging = c->io.d_staging;
+    io.free_seq = c->io.d_free_seq;
+    io.base_seq = c->io.d_base_seq;
+    io.rings = c->io.rings;
+    io.depth = c->io.depth;
+    io.slot_bytes = c->io.slot_bytes;
+    io.header = c->header;
+    io.stride = c->stride;
+    io.len = (int32_t)c->stride;
+    io.R = c->R;
+    io.out = (char*)out;
+    io.err = c->d_err;
+    HCUDA(cudaEventRecord(c->ev_lookup, st));
+    HCUDA(cudaStreamWaitEvent(c->s_submit, c->ev_lookup, 0));
+    HCUDA(cudaStreamWaitEvent(c->s_complete, c->ev_lookup, 0));
+    k_io_complete<<<c->io_ctas, 256, 0, c->s_complete>>>(io);
+    k_io_submit<<<c->io_ctas, 256, 0, c->s_submit>>>(io);
+    HCUDA(cudaGetLastError());
+    HCUDA(cudaEventRecord(c->ev_submit, c->s_submit));
+    HCUDA(cudaEventRecord(c->ev_complete, c->s_complete));
+    HCUDA(cudaStreamWaitEvent(st, c->ev_submit, 0));
+    HCUDA(cudaStreamWaitEvent(st, c->ev_complete, 0));
+    k_io_finish<<<1, 64, 0, st>>>(c->io.d_ctl, c->io.d_base_seq, c->io.rings);
+    HCUDA(cudaGetLastError());
+  }
+  return HELIOS_OK;
+}
+
+}  // namespace helios

@@ -1,0 +1,190 @@
+// internal.cuh — shared internals of libhelios.so (device helpers, handle structs, error plumbing).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/helios.h"
+
+namespace helios {
+
+// ---- error plumbing --------------------------------------------------------------------------
+void set_error(const std::string& s);
+helios_status fail(helios_status st, const char* fmt, ...);
+
+#define HCUDA(call)                                                                           \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return ::helios::fail(HELIOS_E_CUDA, "%s:%d %s -> %s", __FILE__, __LINE__, #call,       \
+                            cudaGetErrorString(e_));                                          \
+  } while (0)
+
+#define HCHECK(cond, st, ...)                                  \
+  do {                                                         \
+    if (!(cond)) return ::helios::fail((st), __VA_ARGS__);     \
+  } while (0)
+
+// Scoped "make device current" for entry points.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // empty hash key / unassigned local id / no minpos
+constexpr int kScanBlock = 256;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanBlock * kScanItems;
+
+// Per-scan decoupled look-back state (reset to all-ones bytes before use).
+struct ScanState {
+  unsigned long long* status;  // [tiles]: all-ones = invalid; bit 62 set = inclusive; else aggregate
+  unsigned int* counter;       // tile ticket (all-ones -> first ticket is 0)
+};
+
+// Sampling workspace (per graph handle).
+struct SampleWS {
+  int64_t cap_nodes = 0, cap_edges = 0, cap_tiles_rows = 0, cap_tiles_edges = 0;
+  int L = 0;
+  uint32_t table_size = 0;   // power of two
+  // reset region (one cudaMemsetAsync(0xFF) per batch): keys | minpos | local | scan status | counters
+  char* reset_base = nullptr;
+  size_t reset_bytes = 0;
+  uint32_t* keys = nullptr;
+  uint32_t* minpos = nullptr;
+  uint32_t* local = nullptr;
+  ScanState row_scan[HELIOS_MAX_HOPS];
+  ScanState edge_scan[HELIOS_MAX_HOPS];
+  uint32_t* slot_of = nullptr;  // [cap_edges]
+};
+
+struct helios_graph_impl;
+
+}  // namespace helios
+
+struct helios_graph {
+  int device = 0;
+  int sms = 148;
+  int64_t V = 0, E = 0;
+  int64_t* indptr = nullptr;   // device [V+1]
+  int32_t* indices = nullptr;  // device [E]
+  int* d_err = nullptr;        // device latched error (0 = none)
+  helios::SampleWS ws;
+  // presample scratch (lazily allocated)
+  helios_blocks pre_blocks{};
+  int64_t pre_cap_B = 0;
+  int pre_L = -1;
+  int32_t pre_fan[HELIOS_MAX_HOPS] = {};
+  void* pre_mem = nullptr;
+};
+
+namespace helios {
+
+// IO ring entry (SQ): 32 bytes, `seq` published last with release semantics (system scope).
+struct alignas(32) SqEntry {
+  uint64_t file_off;
+  uint32_t len;
+  uint32_t slot;
+  uint64_t out_row;
+  uint32_t seq;
+  uint32_t rsvd;
+};
+struct alignas(8) CqEntry {
+  uint32_t seq;     // == SqEntry.seq once the read landed in staging
+  int32_t status;   // 0 ok, else HELIOS_E_IO
+};
+
+struct IoRings {
+  int rings = 0, depth = 0;
+  int64_t slot_bytes = 0;       // staging stride per slot (4096-aligned)
+  SqEntry* sq = nullptr;        // pinned mapped [rings*depth]
+  CqEntry* cq = nullptr;        // pinned mapped [rings*depth]
+  char* staging = nullptr;      // pinned mapped [rings*depth*slot_bytes] (4096-aligned)
+  SqEntry* d_sq = nullptr;      // device aliases of the above
+  CqEntry* d_cq = nullptr;
+  char* d_staging = nullptr;
+  // device-side ring state
+  uint32_t* d_free_seq = nullptr;   // [rings*depth] last sequence consumed by io_complete per slot
+  uint32_t* d_base_seq = nullptr;   // [rings] sequences issued before the current batch
+  // miss list (device)
+  int64_t miss_cap = 0;
+  int64_t* d_miss_out = nullptr;    // output row of each miss
+  int64_t* d_miss_row = nullptr;    // file row of each miss
+  unsigned long long* d_ctl = nullptr;  // [0] miss count, [1] submit ticket, [2] complete ticket
+  // host workers
+  std::vector<std::thread> workers;
+  std::atomic<bool> stop{false};
+  std::atomic<int> host_err{0};
+  std::atomic<int64_t> reads{0};
+  int fd = -1;
+  bool direct = false;
+  int64_t fault_at = 0;  // 1-based global read index to fail (tests), 0 = off
+  std::atomic<int64_t> read_counter{0};
+};
+
+}  // namespace helios
+
+struct helios_cache {
+  helios_graph* g = nullptr;
+  int device = 0;
+  int sms = 148;
+  int64_t V = 0;
+  int32_t R = 0;
+  int32_t G = 1, rank = 0;
+  int64_t H = 0, S = 0, file_rows = 0;
+  uint32_t flags = 0;
+  int64_t* dir = nullptr;         // device [V]
+  char* hbm = nullptr;            // device [H, R]
+  char* host_tier = nullptr;      // host pointer
+  char* d_host_tier = nullptr;    // device-mapped alias
+  bool host_owned = false;        // packed host tier allocated by us
+  bool host_registered = false;   // we registered host_table
+  const void* host_table = nullptr;
+  char** d_peers = nullptr;       // device [G] HBM shard base per rank (self included)
+  char* peer_ptrs[HELIOS_MAX_RANKS] = {};
+  int peers_attached = 0;
+  int* d_err = nullptr;           // device latched error
+  std::string path;
+  int64_t header = 0, stride = 0;
+  int io_ctas = 32;
+  helios::IoRings io;
+  bool has_file = false;
+  cudaStream_t s_submit = nullptr, s_complete = nullptr;
+  cudaEvent_t ev_lookup = nullptr, ev_submit = nullptr, ev_complete = nullptr;
+};
+
+namespace helios {
+
+// Launch helpers implemented in the .cu files.
+helios_status sample_enqueue(helios_graph* g, const int64_t* seeds, int64_t n_seeds, const int32_t* fanouts, int32_t L,
+                             uint64_t key, const helios_blocks* out, cudaStream_t st);
+helios_status sample_bounds(int64_t n_seeds, const int32_t* fanouts, int32_t L, int64_t V, int64_t E,
+                            int64_t* max_nodes, int64_t* level, int64_t* edges);
+helios_status hot_count_enqueue(const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, uint64_t* hot,
+                                int sms, cudaStream_t st);
+helios_status gather_enqueue(helios_cache* c, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, void* out,
+                             helios_gather_stats* stats, cudaStream_t st);
+helios_status validate_csr_device(const int64_t* indptr, const int32_t* indices, int64_t V, int64_t E, int* d_flag,
+                                  cudaStream_t st);
+helios_status cache_sort_and_dir(helios_cache* c, const uint64_t* hot, int32_t* d_order /*[V]*/);
+helios_status gather_rows_by_id(const char* src_dev, int32_t R, const int32_t* ids, int64_t n, char* dst, int sms,
+                                cudaStream_t st);
+helios_status io_start(helios_cache* c, const helios_cache_desc* d);
+helios_status io_preload_kernels();
+void io_stop(helios_cache* c);
+
+}  // namespace helios

@@ -1,0 +1,381 @@
+// sample.cu — K1 sample_hop and K2 dedup_relabel, the neighbour-sampling
+// operator of PAPER.md:215 (§3.2.2) / :239 (§3.3), "2-hop random neighbor sampling" PAPER.md:292.
+//
+// Per hop h (all launches enqueue-only, sizes bounded on the host, actual counts device-resident):
+//   k_row_count_scan   k_i = min(deg(N_h[i]), f_h) and block_indptr = exclusive scan (single-pass
+//                      decoupled look-back), e_h = total.
+//   k_sample_fill<G>   one G-lane group per row: copy the whole adjacency when k == d, else Floyd's
+//                      k-subset with Philox draws resolved by group ballots; writes GLOBAL ids into
+//                      block_indices[h] (relabelled in place below).
+//   k_dedup_insert     open-addressing insert of every sampled id; atomicMin keeps the first edge
+//                      position of ids new at this hop.
+//   k_dedup_assign     flag = "this edge is the first occurrence of a new id"; single-pass scan of
+//                      the flags numbers new ids n_h, n_h+1, ... in first-occurrence order and
+//                      appends them to N_{h+1}.
+//   k_relabel          block_indices[h][e] = local id of the sampled global id.
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "device.cuh"
+
+namespace helios {
+
+__global__ void k_validate_csr(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int64_t V,
+                               int64_t E, int* flag) {
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = tid; v < V; v += nt)
+    if (indptr[v + 1] < indptr[v]) atomicCAS(flag, 0, HELIOS_E_INVALID);
+  for (int64_t e = tid; e < E; e += nt) {
+    int32_t u = indices[e];
+    if (u < 0 || (int64_t)u >= V) atomicCAS(flag, 0, HELIOS_E_RANGE);
+  }
+  if (tid == 0 && (indptr[0] != 0 || indptr[V] != E)) atomicCAS(flag, 0, HELIOS_E_INVALID);
+}
+
+helios_status validate_csr_device(const int64_t* indptr, const int32_t* indices, int64_t V, int64_t E, int* d_flag,
+                                  cudaStream_t st) {
+  int dev, sms;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_validate_csr<<<sms * 8, 256, 0, st>>>(indptr, indices, V, E, d_flag);
+  HCUDA(cudaGetLastError());
+  return HELIOS_OK;
+}
+
+__global__ void k_insert_seeds(const int64_t* __restrict__ seeds, int64_t B, int64_t V, uint32_t* keys, uint32_t* local,
+                               uint32_t mask, int64_t* __restrict__ nodes, int64_t* level_counts, int* err) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i == 0) level_counts[0] = B;
+  if (i >= B) return;
+  int64_t u = seeds[i];
+  nodes[i] = u;
+  if (u < 0 || u >= V) {
+    latch(err, HELIOS_E_RANGE);
+    return;
+  }
+  bool fresh;
+  uint32_t s = table_insert(keys, mask, (uint32_t)u, &fresh);
+  if (!fresh) {
+    latch(err, HELIOS_E_INVALID);  // duplicate seed (reading 7)
+    return;
+  }
+  local[s] = (uint32_t)i;
+}
+
+// k_i = min(deg, f) and the exclusive scan of k into block_indptr[h].
+__global__ void __launch_bounds__(kScanBlock) k_row_count_scan(const int64_t* __restrict__ nodes,
+                                                               const int64_t* __restrict__ level_counts, int h,
+                                                               const int64_t* __restrict__ indptr, int64_t V, int32_t f,
+                                                               int32_t* __restrict__ bp, int64_t* edge_counts,
+                                                               ScanState ss) {
+  using BS = cub::BlockScan<long long, kScanBlock>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ unsigned s_tile;
+  __shared__ long long s_prefix;
+  const unsigned tile = tile_ticket(ss, &s_tile);
+  const int64_t n = level_counts[h];
+  const int64_t base = (int64_t)tile * kScanTile;
+  if (tile > 0 && base >= n) return;
+  long long k[kScanItems];
+  long long sum = 0;
+#pragma unroll
+  for (int q = 0; q < kScanItems; q++) {
+    int64_t i = base + threadIdx.x * kScanItems + q;
+    k[q] = 0;
+    if (i < n) {
+      int64_t v = nodes[i];
+      if ((uint64_t)v < (uint64_t)V) {
+        int64_t d = indptr[v + 1] - indptr[v];
+        k[q] = (f < 0) ? d : min(d, (int64_t)f);
+      }
+    }
+    sum += k[q];
+  }
+  long long excl, agg;
+  BS(tmp).ExclusiveSum(sum, excl, agg);
+  long long prefix = tile_lookback(ss, tile, agg, &s_prefix);
+  long long run = prefix + excl;
+#pragma unroll
+  for (int q = 0; q < kScanItems; q++) {
+    int64_t i = base + threadIdx.x * kScanItems + q;
+    if (i < n) bp[i] = (int32_t)run;
+    run += k[q];
+  }
+  if (threadIdx.x == 0 && ((n == 0 && tile == 0) || (base < n && n <= base + kScanTile))) {
+    bp[n] = (int32_t)(prefix + agg);
+    edge_counts[h] = prefix + agg;
+  }
+}
+
+// One G-lane group per frontier row.  G = power of two >= min(f, 32) (>= 4).
+template <int G>
+__global__ void __launch_bounds__(256) k_sample_fill(const int64_t* __restrict__ nodes, const int64_t* __restrict__ level_counts,
+                                                     int h, const int64_t* __restrict__ indptr,
+                                                     const int32_t* __restrict__ indices, int64_t V, int32_t f,
+                                                     uint64_t key, const int32_t* __restrict__ bp, int32_t* out) {
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const unsigned gmask = (G == 32) ? 0xFFFFFFFFu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  const int64_t n = level_counts[h];
+  const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+  for (int64_t i = grp; i < n; i += ngrp) {
+    const int64_t v = nodes[i];
+    int64_t base = 0, d = 0;
+    if ((uint64_t)v < (uint64_t)V) {
+      base = indptr[v];
+      d = indptr[v + 1] - base;
+    }
+    const int64_t off = bp[i];
+    const int64_t k = (f < 0) ? d : min(d, (int64_t)f);
+    if (k == d) {  // every neighbour, CSR order, no RNG consumed
+      for (int64_t p = gl; p < d; p += G) out[off + p] = indices[base + p];
+    } else if (k <= G) {  // Floyd: lane j owns draw j; sequential resolution by group ballots
+      uint32_t t = 0, m = 0;
+      if (gl < k) {
+        m = (uint32_t)(d - k + gl + 1);
+        t = __umulhi(philox_word(key, (uint32_t)h, (uint64_t)v, (uint32_t)gl), m);
+      }
+      uint32_t P = 0;
+      for (int j = 0; j < (int)k; j++) {
+        const uint32_t tj = __shfl_sync(gmask, t, j, G);
+        const unsigned hit = __ballot_sync(gmask, gl < j && P == tj);
+        if (gl == j) P = hit ? (m - 1) : tj;
+      }
+      if (gl < k) out[off + gl] = indices[base + P];
+    } else {  // k > G (fanout > 32): leader runs Floyd serially using the output row as the set
+      if (gl == 0) {
+        for (int64_t j = 0; j < k; j++) {
+          const uint32_t m = (uint32_t)(d - k + j + 1);
+          const uint32_t tj = __umulhi(philox_word(key, (uint32_t)h, (uint64_t)v, (uint32_t)j), m);
+          bool seen = false;
+          for (int64_t q = 0; q < j; q++)
+            if ((uint32_t)out[off + q] == tj) {
+              seen = true;
+              break;
+            }
+          out[off + j] = (int32_t)(seen ? m - 1 : tj);
+        }
+      }
+      __syncwarp(gmask);
+      for (int64_t j = gl; j < k; j += G) out[off + j] = indices[base + out[off + j]];
+      __syncwarp(gmask);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_dedup_insert(const int32_t* __restrict__ ids, const int64_t* __restrict__ edge_counts,
+                                                      int h, uint32_t* keys, uint32_t* minpos,
+                                                      const uint32_t* local, uint32_t mask,
+                                                      uint32_t* __restrict__ slot_of) {
+  const int64_t eh = edge_counts[h];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < eh; e += (int64_t)gridDim.x * blockDim.x) {
+    bool fresh;
+    const uint32_t s = table_insert(keys, mask, (uint32_t)ids[e], &fresh);
+    slot_of[e] = s;
+    if (fresh || ld_volatile_u32(local + s) == kEmpty) atomicMin(minpos + s, (uint32_t)e);
+  }
+}
+
+__global__ void __launch_bounds__(kScanBlock) k_dedup_assign(const int32_t* __restrict__ ids,
+                                                             const int64_t* __restrict__ edge_counts, int h,
+                                                             const uint32_t* __restrict__ slot_of,
+                                                             const uint32_t* __restrict__ minpos, uint32_t* local,
+                                                             int64_t* __restrict__ nodes, int64_t* level_counts,
+                                                             ScanState ss) {
+  using BS = cub::BlockScan<int, kScanBlock>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ unsigned s_tile;
+  __shared__ long long s_prefix;
+  const unsigned tile = tile_ticket(ss, &s_tile);
+  const int64_t eh = edge_counts[h];
+  const int64_t nh = level_counts[h];
+  const int64_t base = (int64_t)tile * kScanTile;
+  if (tile > 0 && base >= eh) return;
+  int flag[kScanItems];
+  uint32_t slot[kScanItems];
+  int sum = 0;
+#pragma unroll
+  for (int q = 0; q < kScanItems; q++) {
+    const int64_t e = base + threadIdx.x * kScanItems + q;
+    flag[q] = 0;
+    slot[q] = 0;
+    if (e < eh) {
+      slot[q] = slot_of[e];
+      flag[q] = (ld_volatile_u32(local + slot[q]) == kEmpty && minpos[slot[q]] == (uint32_t)e) ? 1 : 0;
+    }
+    sum += flag[q];
+  }
+  int excl, agg;
+  BS(tmp).ExclusiveSum(sum, excl, agg);
+  const long long prefix = tile_lookback(ss, tile, agg, &s_prefix);
+  long long run = prefix + excl;
+#pragma unroll
+  for (int q = 0; q < kScanItems; q++) {
+    if (flag[q]) {
+      const int64_t e = base + threadIdx.x * kScanItems + q;
+      const int64_t id = nh + run;
+      nodes[id] = ids[e];
+      local[slot[q]] = (uint32_t)id;
+      run++;
+    }
+  }
+  if (threadIdx.x == 0 && ((eh == 0 && tile == 0) || (base < eh && eh <= base + kScanTile)))
+    level_counts[h + 1] = nh + prefix + agg;
+}
+
+__global__ void __launch_bounds__(256) k_relabel(int32_t* ids, const int64_t* __restrict__ edge_counts, int h,
+                                                 const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ local) {
+  const int64_t eh = edge_counts[h];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < eh; e += (int64_t)gridDim.x * blockDim.x)
+    ids[e] = (int32_t)local[slot_of[e]];
+}
+
+__global__ void k_hot_count(const int64_t* __restrict__ nodes, const int64_t* __restrict__ n_nodes, uint64_t* hot) {
+  const int64_t n = *n_nodes;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd((unsigned long long*)&hot[nodes[i]], 1ull);
+}
+
+helios_status hot_count_enqueue(const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, uint64_t* hot, int sms,
+                                cudaStream_t st) {
+  int grid = (int)std::min<int64_t>((max_nodes + 255) / 256, (int64_t)sms * 8);
+  k_hot_count<<<std::max(grid, 1), 256, 0, st>>>(nodes, n_nodes, hot);
+  HCUDA(cudaGetLastError());
+  return HELIOS_OK;
+}
+
+// ---- host side --------------------------------------------------------------------------------
+
+helios_status sample_bounds(int64_t n_seeds, const int32_t* fanouts, int32_t L, int64_t V, int64_t E, int64_t* max_nodes,
+                            int64_t* level, int64_t* edges) {
+  HCHECK(L >= 0 && L <= HELIOS_MAX_HOPS, HELIOS_E_INVALID, "L=%d out of [0,%d]", L, HELIOS_MAX_HOPS);
+  HCHECK(n_seeds >= 0, HELIOS_E_INVALID, "n_seeds < 0");
+  int64_t n = n_seeds;
+  if (level) level[0] = n;
+  for (int h = 0; h < L; h++) {
+    HCHECK(fanouts && (fanouts[h] >= 1 || fanouts[h] == -1), HELIOS_E_INVALID, "fanout[%d]=%d (need >=1 or -1)", h,
+           fanouts ? fanouts[h] : 0);
+    int64_t e = (fanouts[h] < 0) ? E : std::min<int64_t>(n * (int64_t)fanouts[h], E);
+    if (edges) edges[h] = e;
+    n = std::min<int64_t>(V, n + e);
+    if (level) level[h + 1] = n;
+  }
+  if (max_nodes) *max_nodes = n;
+  return HELIOS_OK;
+}
+
+static uint32_t pow2_at_least(int64_t x) {
+  uint64_t p = 1024;
+  while ((int64_t)p < x) p <<= 1;
+  return (uint32_t)p;
+}
+
+static helios_status ensure_ws(helios_graph* g, const int64_t* lvl, const int64_t* edg, int L, int64_t max_nodes) {
+  SampleWS& w = g->ws;
+  int64_t max_e = 1, tiles_r = 1, tiles_e = 1;
+  for (int h = 0; h < L; h++) {
+    max_e = std::max(max_e, edg[h]);
+    tiles_r = std::max(tiles_r, (lvl[h] + kScanTile - 1) / kScanTile);
+    tiles_e = std::max(tiles_e, (edg[h] + kScanTile - 1) / kScanTile);
+  }
+  uint32_t T = pow2_at_least(2 * std::min<int64_t>(g->V, std::max<int64_t>(max_nodes, 1)));
+  if (w.reset_base && T <= w.table_size && max_e <= w.cap_edges && tiles_r <= w.cap_tiles_rows &&
+      tiles_e <= w.cap_tiles_edges)
+    return HELIOS_OK;
+  HCUDA(cudaDeviceSynchronize());
+  if (w.reset_base) cudaFree(w.reset_base);
+  if (w.slot_of) cudaFree(w.slot_of);
+  w = SampleWS{};
+  // grow generously so later batches with a few more rows do not reallocate
+  T = std::max(T, w.table_size);
+  size_t table_bytes = (size_t)T * 4;
+  size_t status_bytes = (size_t)(tiles_r + tiles_e) * HELIOS_MAX_HOPS * 8;
+  size_t counter_bytes = (size_t)2 * HELIOS_MAX_HOPS * 4;
+  w.reset_bytes = 3 * table_bytes + status_bytes + counter_bytes;
+  HCUDA(cudaMalloc(&w.reset_base, w.reset_bytes));
+  HCUDA(cudaMalloc(&w.slot_of, (size_t)max_e * 4));
+  w.table_size = T;
+  w.cap_edges = max_e;
+  w.cap_tiles_rows = tiles_r;
+  w.cap_tiles_edges = tiles_e;
+  char* p = w.reset_base;
+  w.keys = (uint32_t*)p;
+  p += table_bytes;
+  w.minpos = (uint32_t*)p;
+  p += table_bytes;
+  w.local = (uint32_t*)p;
+  p += table_bytes;
+  for (int h = 0; h < HELIOS_MAX_HOPS; h++) {
+    w.row_scan[h].status = (unsigned long long*)p;
+    p += tiles_r * 8;
+    w.edge_scan[h].status = (unsigned long long*)p;
+    p += tiles_e * 8;
+  }
+  for (int h = 0; h < HELIOS_MAX_HOPS; h++) {
+    w.row_scan[h].counter = (unsigned*)p;
+    p += 4;
+    w.edge_scan[h].counter = (unsigned*)p;
+    p += 4;
+  }
+  return HELIOS_OK;
+}
+
+template <int G>
+static void launch_fill(const helios_graph* g, const helios_blocks* out, int h, int64_t rows, int32_t f, uint64_t key,
+                        cudaStream_t st) {
+  int64_t threads = std::max<int64_t>(rows, 1) * G;
+  int grid = (int)std::min<int64_t>((threads + 255) / 256, (int64_t)g->sms * 16);
+  k_sample_fill<G><<<grid, 256, 0, st>>>(out->nodes, out->level_counts, h, g->indptr, g->indices, g->V, f, key,
+                                         out->block_indptr[h], out->block_indices[h]);
+}
+
+helios_status sample_enqueue(helios_graph* g, const int64_t* seeds, int64_t B, const int32_t* fanouts, int32_t L,
+                             uint64_t key, const helios_blocks* out, cudaStream_t st) {
+  int64_t maxn, lvl[HELIOS_MAX_HOPS + 1], edg[HELIOS_MAX_HOPS];
+  helios_status s = sample_bounds(B, fanouts, L, g->V, g->E, &maxn, lvl, edg);
+  if (s != HELIOS_OK) return s;
+  HCHECK(out && out->nodes && out->level_counts && (L == 0 || out->edge_counts), HELIOS_E_INVALID, "null output");
+  HCHECK(out->nodes_cap >= maxn, HELIOS_E_CAPACITY, "nodes_cap %lld < bound %lld", (long long)out->nodes_cap,
+         (long long)maxn);
+  for (int h = 0; h < L; h++) {
+    HCHECK(out->block_indptr[h] && out->block_indices[h], HELIOS_E_INVALID, "null block buffer for hop %d", h);
+    HCHECK(out->indptr_cap[h] >= lvl[h] + 1, HELIOS_E_CAPACITY, "indptr_cap[%d] %lld < %lld", h,
+           (long long)out->indptr_cap[h], (long long)lvl[h] + 1);
+    HCHECK(out->edges_cap[h] >= edg[h], HELIOS_E_CAPACITY, "edges_cap[%d] %lld < %lld", h, (long long)out->edges_cap[h],
+           (long long)edg[h]);
+    HCHECK(edg[h] < (1ll << 31), HELIOS_E_CAPACITY, "hop %d edge bound %lld exceeds int32 block indices", h,
+           (long long)edg[h]);
+  }
+  HCHECK(B == 0 || seeds, HELIOS_E_INVALID, "null seeds");
+  s = ensure_ws(g, lvl, edg, L, maxn);
+  if (s != HELIOS_OK) return s;
+  SampleWS& w = g->ws;
+  const uint32_t mask = w.table_size - 1;
+  HCUDA(cudaMemsetAsync(w.reset_base, 0xFF, w.reset_bytes, st));
+  k_insert_seeds<<<(int)std::max<int64_t>(1, (B + 255) / 256), 256, 0, st>>>(seeds, B, g->V, w.keys, w.local, mask,
+                                                                               out->nodes, out->level_counts, g->d_err);
+  for (int h = 0; h < L; h++) {
+    const int32_t f = fanouts[h];
+    int rt = (int)std::max<int64_t>(1, (lvl[h] + kScanTile - 1) / kScanTile);
+    k_row_count_scan<<<rt, kScanBlock, 0, st>>>(out->nodes, out->level_counts, h, g->indptr, g->V, f,
+                                                out->block_indptr[h], out->edge_counts, w.row_scan[h]);
+    if (f < 0 || f > 16) launch_fill<32>(g, out, h, lvl[h], f, key, st);
+    else if (f > 8) launch_fill<16>(g, out, h, lvl[h], f, key, st);
+    else if (f > 4) launch_fill<8>(g, out, h, lvl[h], f, key, st);
+    else launch_fill<4>(g, out, h, lvl[h], f, key, st);
+    int ge = (int)std::min<int64_t>(std::max<int64_t>(1, (edg[h] + 255) / 256), (int64_t)g->sms * 16);
+    k_dedup_insert<<<ge, 256, 0, st>>>(out->block_indices[h], out->edge_counts, h, w.keys, w.minpos, w.local, mask,
+                                       w.slot_of);
+    int et = (int)std::max<int64_t>(1, (edg[h] + kScanTile - 1) / kScanTile);
+    k_dedup_assign<<<et, kScanBlock, 0, st>>>(out->block_indices[h], out->edge_counts, h, w.slot_of, w.minpos, w.local,
+                                              out->nodes, out->level_counts, w.edge_scan[h]);
+    k_relabel<<<ge, 256, 0, st>>>(out->block_indices[h], out->edge_counts, h, w.slot_of, w.local);
+  }
+  HCUDA(cudaGetLastError());
+  return HELIOS_OK;
+}
+
+}  // namespace helios

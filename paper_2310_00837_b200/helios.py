@@ -1,0 +1,309 @@
+"""Thin ctypes binding of libhelios.so (C ABI v1, include/helios.h) — argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module only turns torch tensors
+into device pointers, torch streams into cudaStream_t handles, and statuses into exceptions.  There
+is no CPU fallback: importing this module fails loudly when libhelios.so is missing.
+Function names are the ABI's.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "libhelios.so")
+if not os.path.exists(SO_PATH):
+    raise ImportError(f"{SO_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(nvcc, sm_100a). There is no CPU fallback.")
+_lib = ctypes.CDLL(SO_PATH)
+
+MAX_HOPS = 8
+MAX_RANKS = 64
+STATUS = ["OK", "E_INVALID", "E_RANGE", "E_CAPACITY", "E_NOMEM", "E_CUDA", "E_IO", "E_TIMEOUT", "E_STATE"]
+HOST_ALIAS, TABLE_MAPPED, NO_DIRECT_IO, IO_FAULT_AT = 0x1, 0x2, 0x4, 0x100
+
+i64, i32, u32, u64, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p
+
+
+class helios_blocks(ctypes.Structure):
+    _fields_ = [("nodes", vp), ("nodes_cap", i64), ("level_counts", vp), ("edge_counts", vp),
+                ("block_indptr", vp * MAX_HOPS), ("indptr_cap", i64 * MAX_HOPS),
+                ("block_indices", vp * MAX_HOPS), ("edges_cap", i64 * MAX_HOPS)]
+
+
+class helios_cache_desc(ctypes.Structure):
+    _fields_ = [("row_bytes", i32), ("world_size", i32), ("rank", i32), ("hbm_rows", i64), ("host_rows", i64),
+                ("hotness", vp), ("host_table", vp), ("feature_path", ctypes.c_char_p), ("header_bytes", i64),
+                ("file_stride", i64), ("io_rings", i32), ("ring_depth", i32), ("io_ctas", i32),
+                ("io_fault_at", i32), ("flags", u32)]
+
+
+class helios_cache_info(ctypes.Structure):
+    _fields_ = [("dir", vp), ("hbm_tier", vp), ("host_tier", vp), ("V", i64), ("hbm_rows", i64), ("host_rows", i64),
+                ("file_rows", i64), ("row_bytes", i32), ("world_size", i32), ("rank", i32), ("peers_attached", i32),
+                ("io_rings", i32), ("ring_depth", i32), ("direct_io", i32), ("io_reads", i64)]
+
+
+_sig = {
+    "helios_abi_version": (ctypes.c_int, []),
+    "helios_last_error": (ctypes.c_char_p, []),
+    "helios_graph_load": (ctypes.c_int, [ctypes.c_int, i64, i64, vp, vp, u32, ctypes.POINTER(vp)]),
+    "helios_graph_free": (None, [vp]),
+    "helios_graph_info": (ctypes.c_int, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_int)]),
+    "helios_graph_device_csr": (ctypes.c_int, [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]),
+    "helios_sample_bounds": (ctypes.c_int, [i64, vp, i32, i64, i64, ctypes.POINTER(i64), vp, vp]),
+    "helios_sample": (ctypes.c_int, [vp, vp, i64, vp, i32, u64, ctypes.POINTER(helios_blocks), vp]),
+    "helios_graph_sync": (ctypes.c_int, [vp, vp]),
+    "helios_presample": (ctypes.c_int, [vp, vp, i64, i32, vp, i32, vp, vp, vp]),
+    "helios_cache_build": (ctypes.c_int, [vp, ctypes.POINTER(helios_cache_desc), ctypes.POINTER(vp)]),
+    "helios_cache_free": (None, [vp]),
+    "helios_cache_query": (ctypes.c_int, [vp, ctypes.POINTER(helios_cache_info)]),
+    "helios_cache_export": (ctypes.c_int, [vp, vp, ctypes.POINTER(ctypes.c_size_t)]),
+    "helios_cache_attach_peers": (ctypes.c_int, [vp, vp, ctypes.c_size_t]),
+    "helios_gather": (ctypes.c_int, [vp, vp, vp, i64, vp, vp, vp]),
+    "helios_batch_prepare": (ctypes.c_int, [vp, vp, vp, i64, vp, i32, u64, ctypes.POINTER(helios_blocks), vp, vp, vp]),
+    "helios_sync": (ctypes.c_int, [vp, vp]),
+}
+for _n, (_r, _a) in _sig.items():
+    _f = getattr(_lib, _n)
+    _f.restype = _r
+    _f.argtypes = _a
+
+ABI_SYMBOLS = tuple(_sig)
+
+
+class HeliosError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        self.name = STATUS[status] if 0 <= status < len(STATUS) else str(status)
+        detail = (_lib.helios_last_error() or b"").decode(errors="replace")
+        super().__init__(f"{where}: HELIOS_{self.name}: {detail}")
+
+
+def _check(st: int, where: str) -> None:
+    if st != 0:
+        raise HeliosError(st, where)
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return t.data_ptr()
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return int(t)
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def helios_abi_version() -> int:
+    return _lib.helios_abi_version()
+
+
+# ---- graph ---------------------------------------------------------------------------------------
+
+class Graph:
+    def __init__(self, handle: int, V: int, E: int, device: int):
+        self.handle, self.V, self.E, self.device = handle, V, E, device
+
+    def free(self):
+        if self.handle:
+            _lib.helios_graph_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def helios_graph_load(indptr: np.ndarray, indices: np.ndarray, device: int = 0) -> Graph:
+    indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+    indices = np.ascontiguousarray(indices, dtype=np.int32)
+    V, E = len(indptr) - 1, len(indices)
+    h = vp()
+    _check(_lib.helios_graph_load(device, V, E, _ptr(indptr), _ptr(indices) if E else None, 0, ctypes.byref(h)),
+           "helios_graph_load")
+    return Graph(h.value, V, E, device)
+
+
+def helios_graph_device_csr(g: Graph) -> tuple[int, int]:
+    a, b = vp(), vp()
+    _check(_lib.helios_graph_device_csr(g.handle, ctypes.byref(a), ctypes.byref(b)), "helios_graph_device_csr")
+    return a.value, b.value
+
+
+def helios_sample_bounds(n_seeds: int, fanouts, V: int, E: int) -> tuple[int, list[int], list[int]]:
+    fan = np.ascontiguousarray(fanouts, dtype=np.int32)
+    L = len(fan)
+    lvl = np.zeros(L + 1, dtype=np.int64)
+    edg = np.zeros(max(L, 1), dtype=np.int64)
+    mx = i64()
+    _check(_lib.helios_sample_bounds(n_seeds, _ptr(fan), L, V, E, ctypes.byref(mx), _ptr(lvl), _ptr(edg)),
+           "helios_sample_bounds")
+    return mx.value, lvl.tolist(), edg[:L].tolist()
+
+
+@dataclass
+class Blocks:
+    """Caller-owned device output buffers of one mini-batch, sized by helios_sample_bounds."""
+    nodes: torch.Tensor
+    level_counts: torch.Tensor
+    edge_counts: torch.Tensor
+    block_indptr: list
+    block_indices: list
+    fanouts: list
+
+    @staticmethod
+    def allocate(n_seeds: int, fanouts, V: int, E: int, device=0) -> "Blocks":
+        mx, lvl, edg = helios_sample_bounds(n_seeds, fanouts, V, E)
+        dev = torch.device("cuda", device) if isinstance(device, int) else device
+        return Blocks(nodes=torch.empty(max(mx, 1), dtype=torch.int64, device=dev),
+                      level_counts=torch.zeros(len(fanouts) + 1, dtype=torch.int64, device=dev),
+                      edge_counts=torch.zeros(MAX_HOPS, dtype=torch.int64, device=dev),
+                      block_indptr=[torch.empty(lvl[h] + 1, dtype=torch.int32, device=dev) for h in range(len(fanouts))],
+                      block_indices=[torch.empty(max(edg[h], 1), dtype=torch.int32, device=dev)
+                                     for h in range(len(fanouts))],
+                      fanouts=list(fanouts))
+
+    def struct(self) -> helios_blocks:
+        s = helios_blocks()
+        s.nodes = self.nodes.data_ptr()
+        s.nodes_cap = self.nodes.numel()
+        s.level_counts = self.level_counts.data_ptr()
+        s.edge_counts = self.edge_counts.data_ptr()
+        for h in range(len(self.fanouts)):
+            s.block_indptr[h] = self.block_indptr[h].data_ptr()
+            s.indptr_cap[h] = self.block_indptr[h].numel()
+            s.block_indices[h] = self.block_indices[h].data_ptr()
+            s.edges_cap[h] = self.block_indices[h].numel()
+        return s
+
+    def to_host(self) -> dict:
+        """Copies the batch back (synchronises): nodes, level_counts, edge_counts, per-hop CSR."""
+        L = len(self.fanouts)
+        lc = self.level_counts.cpu().numpy()
+        ec = self.edge_counts[:L].cpu().numpy()
+        return {"nodes": self.nodes[: lc[L]].cpu().numpy(), "level_counts": lc, "edge_counts": ec,
+                "block_indptr": [self.block_indptr[h][: lc[h] + 1].cpu().numpy() for h in range(L)],
+                "block_indices": [self.block_indices[h][: ec[h]].cpu().numpy() for h in range(L)]}
+
+
+def helios_sample(g: Graph, seeds: torch.Tensor, fanouts, key: int, out: Blocks, stream=None) -> None:
+    fan = np.ascontiguousarray(fanouts, dtype=np.int32)
+    s = out.struct()
+    _check(_lib.helios_sample(g.handle, _ptr(seeds), seeds.numel(), _ptr(fan), len(fan), key & (2**64 - 1),
+                              ctypes.byref(s), _stream(stream)), "helios_sample")
+
+
+def helios_graph_sync(g: Graph, stream=None) -> None:
+    _check(_lib.helios_graph_sync(g.handle, _stream(stream)), "helios_graph_sync")
+
+
+def helios_presample(g: Graph, seeds: torch.Tensor, batch: int, fanouts, keys, hotness: torch.Tensor,
+                     stream=None) -> None:
+    fan = np.ascontiguousarray(fanouts, dtype=np.int32)
+    ks = np.ascontiguousarray([k & (2**64 - 1) for k in keys], dtype=np.uint64)
+    _check(_lib.helios_presample(g.handle, _ptr(seeds), seeds.numel(), batch, _ptr(fan), len(fan), _ptr(ks),
+                                 _ptr(hotness), _stream(stream)), "helios_presample")
+
+
+# ---- cache ---------------------------------------------------------------------------------------
+
+class Cache:
+    def __init__(self, handle: int, graph: Graph, keepalive):
+        self.handle, self.graph, self._keep = handle, graph, keepalive
+
+    def info(self) -> helios_cache_info:
+        inf = helios_cache_info()
+        _check(_lib.helios_cache_query(self.handle, ctypes.byref(inf)), "helios_cache_query")
+        return inf
+
+    def free(self):
+        if self.handle:
+            _lib.helios_cache_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def helios_cache_build(g: Graph, hotness: torch.Tensor, row_bytes: int, hbm_rows: int, host_rows: int,
+                       host_table: np.ndarray | None = None, feature_path: str | None = None, header_bytes: int = 0,
+                       file_stride: int = 0, world_size: int = 1, rank: int = 0, io_rings: int = 4,
+                       ring_depth: int = 256, io_ctas: int = 32, flags: int = 0, io_fault_at: int = 0) -> Cache:
+    d = helios_cache_desc()
+    d.row_bytes, d.world_size, d.rank = row_bytes, world_size, rank
+    d.hbm_rows, d.host_rows = hbm_rows, host_rows
+    d.hotness = hotness.data_ptr()
+    d.host_table = _ptr(host_table)
+    path = feature_path.encode() if feature_path else None
+    d.feature_path = path
+    d.header_bytes, d.file_stride = header_bytes, file_stride
+    d.io_rings, d.ring_depth, d.io_ctas, d.io_fault_at, d.flags = io_rings, ring_depth, io_ctas, io_fault_at, flags
+    h = vp()
+    _check(_lib.helios_cache_build(g.handle, ctypes.byref(d), ctypes.byref(h)), "helios_cache_build")
+    return Cache(h.value, g, (host_table, path))
+
+
+def helios_cache_export(c: Cache) -> bytes:
+    n = ctypes.c_size_t(0)
+    _check(_lib.helios_cache_export(c.handle, None, ctypes.byref(n)), "helios_cache_export")
+    buf = ctypes.create_string_buffer(n.value)
+    _check(_lib.helios_cache_export(c.handle, buf, ctypes.byref(n)), "helios_cache_export")
+    return buf.raw[: n.value]
+
+
+def helios_cache_attach_peers(c: Cache, blobs: list[bytes]) -> None:
+    size = len(blobs[0])
+    assert all(len(b) == size for b in blobs)
+    buf = ctypes.create_string_buffer(b"".join(blobs), size * len(blobs))
+    _check(_lib.helios_cache_attach_peers(c.handle, buf, size), "helios_cache_attach_peers")
+
+
+def helios_gather(c: Cache, nodes: torch.Tensor, n_nodes: torch.Tensor, out: torch.Tensor,
+                  stats: torch.Tensor | None = None, stream=None) -> None:
+    _check(_lib.helios_gather(c.handle, _ptr(nodes), _ptr(n_nodes), nodes.numel(), _ptr(out), _ptr(stats),
+                              _stream(stream)), "helios_gather")
+
+
+def helios_batch_prepare(g: Graph, c: Cache, seeds: torch.Tensor, fanouts, key: int, out: Blocks,
+                         features: torch.Tensor, stats: torch.Tensor | None = None, stream=None) -> None:
+    fan = np.ascontiguousarray(fanouts, dtype=np.int32)
+    s = out.struct()
+    _check(_lib.helios_batch_prepare(g.handle, c.handle, _ptr(seeds), seeds.numel(), _ptr(fan), len(fan),
+                                     key & (2**64 - 1), ctypes.byref(s), _ptr(features), _ptr(stats),
+                                     _stream(stream)), "helios_batch_prepare")
+
+
+def helios_sync(c: Cache, stream=None) -> None:
+    _check(_lib.helios_sync(c.handle, _stream(stream)), "helios_sync")
+
+
+def new_stats(device=0) -> torch.Tensor:
+    """Device helios_gather_stats: int64[4] = rows_hbm_local, rows_hbm_peer, rows_host, rows_file."""
+    return torch.zeros(4, dtype=torch.int64, device=torch.device("cuda", device) if isinstance(device, int) else device)
+
+
+class _CudaArray:
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (int(ptr), False), "version": 3}
+
+
+def device_view(ptr: int, n: int, dtype=torch.int64) -> torch.Tensor:
+    """Zero-copy torch view of a library-owned device array (e.g. helios_cache_info.dir)."""
+    typestr = {torch.int64: "<i8", torch.int32: "<i4", torch.uint8: "|u1", torch.float32: "<f4"}[dtype]
+    return torch.as_tensor(_CudaArray(ptr, n, typestr), device="cuda")

@@ -1,0 +1,150 @@
+"""GPU parity of helios_cache_build / helios_gather / helios_batch_prepare against the oracle.
+
+* Directory: bit-exact vs oracle.cache_dir for several (world_size, rank, H, S, alias) cases.
+* Gather: output bytes == oracle.gather (canonical rows) for every row, all three tiers (HBM,
+  pinned host zero-copy, file through the GPU-initiated IO rings), row sizes 400/512/4096 B;
+  per-tier row counts == oracle.lookup_counts.
+* batch_prepare over the C1 epoch (every batch) == oracle sample + gather.
+* IO rings: ring_depth 2 (wrap-around + back-pressure), fault injection -> latched E_IO.
+"""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+import workloads  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_2310_00837_b200 import helios
+    return helios
+
+
+@pytest.fixture(scope="module")
+def c1(tmp_path_factory):
+    return workloads.make_inputs(workloads.CONFIGS["C1"], table=True, file=True,
+                                 workdir=str(tmp_path_factory.mktemp("c1")))
+
+
+@pytest.fixture(scope="module")
+def c1_hot(H, c1):
+    g = H.helios_graph_load(c1.graph.indptr, c1.graph.indices)
+    keys = workloads.presample_keys(len(c1.batches))
+    hot = torch.zeros(c1.cfg.V, dtype=torch.int64, device="cuda")
+    H.helios_presample(g, torch.as_tensor(np.concatenate(c1.batches)).cuda(), c1.cfg.B, c1.cfg.fanouts, keys, hot)
+    H.helios_graph_sync(g)
+    return g, hot
+
+
+@pytest.mark.parametrize("G,rank,Hr,S,alias", [(1, 0, 1000, 4000, False), (1, 0, 1000, 4000, True), (3, 2, 700, 500, False),
+                                               (4, 1, 0, 9000, True), (1, 0, 20000, 0, False)])
+def test_directory_parity(H, c1, c1_hot, G, rank, Hr, S, alias):
+    g, hot = c1_hot
+    c = H.helios_cache_build(g, hot, c1.cfg.R, Hr, S, host_table=c1.table, feature_path=c1.feature_path,
+                             header_bytes=c1.header, file_stride=c1.stride, world_size=G, rank=rank,
+                             flags=H.HOST_ALIAS if alias else 0)
+    inf = c.info()
+    dgpu = H.device_view(inf.dir, c1.cfg.V, torch.int64).cpu().numpy()
+    dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), G, Hr, S, host_slot_is_id=alias)
+    assert np.array_equal(dgpu, dref)
+    c.free()
+
+
+def gather_and_check(H, c, inp, nodes_np, stats_ref):
+    R = inp.cfg.R
+    nodes = torch.as_tensor(nodes_np).cuda()
+    n = torch.tensor([len(nodes_np)], dtype=torch.int64, device="cuda")
+    out = torch.full((max(1, len(nodes_np)), R), 0xAB, dtype=torch.uint8, device="cuda")
+    stats = H.new_stats()
+    H.helios_gather(c, nodes, n, out, stats)
+    H.helios_sync(c)
+    ref = oracle.gather(nodes_np, R, table=inp.table)
+    assert np.array_equal(out[: len(nodes_np)].cpu().numpy(), ref)
+    assert stats.cpu().numpy().tolist() == stats_ref.tolist()
+
+
+@pytest.mark.parametrize("alias", [False, True])
+def test_gather_three_tiers_c1(H, c1, c1_hot, alias):
+    g, hot = c1_hot
+    cfg = c1.cfg
+    Hr, S = workloads.tier_rows(cfg)
+    c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=c1.table, feature_path=c1.feature_path,
+                             header_bytes=c1.header, file_stride=c1.stride, flags=H.HOST_ALIAS if alias else 0)
+    assert c.info().file_rows == cfg.V - Hr - S
+    dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S, host_slot_is_id=alias)
+    rng = np.random.default_rng(0)
+    for n in (1, 31, 1000, 4097, cfg.V):
+        nodes = rng.permutation(cfg.V)[:n]
+        gather_and_check(H, c, c1, nodes, oracle.lookup_counts(dref, nodes))
+    c.free()
+
+
+@pytest.mark.parametrize("dim", [100, 1024])
+def test_gather_row_sizes(H, tmp_path, dim):
+    V = 6000
+    gr = synth.graph(V, 50_000, seed=5)
+    table = synth.features(V, dim)
+    path = str(tmp_path / "f.bin")
+    stride = synth.write_feature_file(path, V, dim, header_bytes=4096)
+    g = H.helios_graph_load(gr.indptr, gr.indices)
+    hot = torch.as_tensor(np.random.default_rng(dim).integers(0, 50, V)).cuda()
+    c = H.helios_cache_build(g, hot, 4 * dim, 1000, 2000, host_table=None, feature_path=path, header_bytes=4096,
+                             file_stride=stride, ring_depth=16, io_rings=3)
+    dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, 1000, 2000)
+    nodes = np.random.default_rng(1).permutation(V)[:3001]
+    inp = workloads.Inputs(workloads.Config("x", V, 0, dim, 0, [], 0, 0), gr, table, path, 4096, stride, None, [])
+    gather_and_check(H, c, inp, nodes, oracle.lookup_counts(dref, nodes))
+    c.free()
+
+
+def test_io_ring_wraparound_and_fault(H, c1, c1_hot):
+    g, hot = c1_hot
+    cfg = c1.cfg
+    c = H.helios_cache_build(g, hot, cfg.R, 0, 0, host_table=None, feature_path=c1.feature_path,
+                             header_bytes=c1.header, file_stride=c1.stride, ring_depth=2, io_rings=2, io_ctas=2)
+    nodes = np.random.default_rng(9).permutation(cfg.V)[:3000]
+    gather_and_check(H, c, c1, nodes, np.array([0, 0, 0, 3000]))
+    gather_and_check(H, c, c1, nodes[::-1].copy(), np.array([0, 0, 0, 3000]))   # sequences continue across batches
+    c.free()
+    c = H.helios_cache_build(g, hot, cfg.R, 0, 0, host_table=None, feature_path=c1.feature_path,
+                             header_bytes=c1.header, file_stride=c1.stride, ring_depth=8, io_rings=2,
+                             flags=H.IO_FAULT_AT, io_fault_at=17)
+    out = torch.empty((3000, cfg.R), dtype=torch.uint8, device="cuda")
+    H.helios_gather(c, torch.as_tensor(nodes).cuda(), torch.tensor([3000], device="cuda"), out)
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_sync(c)
+    assert e.value.name == "E_IO"
+    c.free()
+
+
+def test_batch_prepare_c1_epoch(H, c1, c1_hot):
+    g, hot = c1_hot
+    cfg = c1.cfg
+    Hr, S = workloads.tier_rows(cfg)
+    c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=c1.table, feature_path=c1.feature_path,
+                             header_bytes=c1.header, file_stride=c1.stride, flags=H.HOST_ALIAS)
+    dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S, host_slot_is_id=True)
+    blocks = H.Blocks.allocate(cfg.B, cfg.fanouts, g.V, g.E)
+    feats = torch.empty((blocks.nodes.numel(), cfg.R), dtype=torch.uint8, device="cuda")
+    stats = H.new_stats()
+    keys = workloads.batch_keys(0, len(c1.batches))
+    for seeds, key in zip(c1.batches, keys):
+        H.helios_batch_prepare(g, c, torch.as_tensor(seeds).cuda(), cfg.fanouts, key, blocks, feats, stats)
+        H.helios_sync(c)
+        got = blocks.to_host()
+        orc = oracle.sample(c1.graph.indptr, c1.graph.indices, seeds, cfg.fanouts, key)
+        assert np.array_equal(got["nodes"], orc.nodes)
+        for h in range(len(cfg.fanouts)):
+            assert np.array_equal(got["block_indptr"][h], orc.block_indptr[h])
+            assert np.array_equal(got["block_indices"][h], orc.block_indices[h])
+        n = len(orc.nodes)
+        ref = oracle.gather(orc.nodes, cfg.R, table=c1.table)
+        assert np.array_equal(feats[:n].cpu().numpy(), ref)
+        assert stats.cpu().numpy().tolist() == oracle.lookup_counts(dref, orc.nodes).tolist()
+    c.free()

@@ -1,0 +1,129 @@
+"""GPU parity of helios_sample / helios_presample (K1 sample_hop + K2 dedup_relabel) against the
+CPU oracle, bit-exact: nodes (N_L), level counts, per-hop block CSR.
+
+Sizes: the C1 config over a whole epoch; a medium power-law graph spanning many scan tiles with
+ragged tails; fanout -1 (BFS), fanout > 32 (serial Floyd path), hub rows; edge cases (0/1 seeds,
+isolated seeds) and the latched errors (duplicate seed, seed >= V) and E_CAPACITY.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+import workloads  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_2310_00837_b200 import helios
+    assert torch.cuda.is_available()
+    return helios
+
+
+def run_gpu(H, g, seeds, fanouts, key):
+    blocks = H.Blocks.allocate(len(seeds), fanouts, g.V, g.E)
+    s = torch.as_tensor(np.asarray(seeds, dtype=np.int64)).cuda()
+    H.helios_sample(g, s, fanouts, key, blocks)
+    H.helios_graph_sync(g)
+    return blocks.to_host()
+
+
+def assert_same(gpu, orc, L):
+    assert np.array_equal(gpu["level_counts"], orc.level_counts)
+    assert np.array_equal(gpu["edge_counts"], orc.edge_counts)
+    assert np.array_equal(gpu["nodes"], orc.nodes)
+    for h in range(L):
+        assert np.array_equal(gpu["block_indptr"][h], orc.block_indptr[h]), f"hop {h} indptr"
+        assert np.array_equal(gpu["block_indices"][h], orc.block_indices[h]), f"hop {h} indices"
+
+
+@pytest.fixture(scope="module")
+def c1():
+    return workloads.make_inputs(workloads.CONFIGS["C1"], table=False)
+
+
+@pytest.fixture(scope="module")
+def medium():
+    return synth.graph(300_000, 6_000_000, seed=21)
+
+
+def test_c1_full_epoch(H, c1):
+    cfg = c1.cfg
+    g = H.helios_graph_load(c1.graph.indptr, c1.graph.indices)
+    keys = workloads.batch_keys(0, len(c1.batches))
+    for b, (seeds, key) in enumerate(zip(c1.batches, keys)):
+        gpu = run_gpu(H, g, seeds, cfg.fanouts, key)
+        orc = oracle.sample(c1.graph.indptr, c1.graph.indices, seeds, cfg.fanouts, key)
+        assert_same(gpu, orc, len(cfg.fanouts))
+
+
+@pytest.mark.parametrize("B,fanouts", [(1024, [15, 10, 5]), (1000, [25, 10]), (333, [3, 3, 3, 3]), (77, [40]),
+                                       (5, [-1, -1]), (1, [15, 10, 5])])
+def test_medium_graph(H, medium, B, fanouts):
+    g = H.helios_graph_load(medium.indptr, medium.indices)
+    rng = np.random.default_rng(B)
+    seeds = rng.choice(medium.V, B, replace=False)
+    for key in (1, 0xDEADBEEFCAFEF00D):
+        gpu = run_gpu(H, g, seeds, fanouts, key)
+        orc = oracle.sample(medium.indptr, medium.indices, seeds, fanouts, key)
+        assert_same(gpu, orc, len(fanouts))
+
+
+def test_hub_and_isolated(H):
+    d = 200_000
+    adj_len = np.zeros(d + 2, dtype=np.int64)
+    adj_len[0] = d
+    indptr = np.concatenate([[0], np.cumsum(adj_len)])
+    indices = np.arange(1, d + 1, dtype=np.int32)
+    g = H.helios_graph_load(indptr, indices)
+    for fan in ([15], [15, 2], [33], [-1]):
+        for seeds in ([0], [0, d + 1], [d + 1], [5, 0]):
+            gpu = run_gpu(H, g, seeds, fan, 12345)
+            orc = oracle.sample(indptr, indices, seeds, fan, 12345)
+            assert_same(gpu, orc, len(fan))
+
+
+def test_zero_seeds(H, c1):
+    g = H.helios_graph_load(c1.graph.indptr, c1.graph.indices)
+    gpu = run_gpu(H, g, [], [10, 5], 1)
+    assert gpu["level_counts"].tolist() == [0, 0, 0] and len(gpu["nodes"]) == 0
+
+
+def test_latched_errors(H, c1):
+    g = H.helios_graph_load(c1.graph.indptr, c1.graph.indices)
+    with pytest.raises(H.HeliosError) as e:
+        run_gpu(H, g, [1, 2, 1], [5], 1)
+    assert e.value.name == "E_INVALID"
+    with pytest.raises(H.HeliosError) as e:
+        run_gpu(H, g, [1, c1.cfg.V + 3], [5], 1)
+    assert e.value.name == "E_RANGE"
+    run_gpu(H, g, [1, 2, 3], [5], 1)  # handle usable again after the latched error is read
+    blocks = H.Blocks.allocate(10, [5], g.V, g.E)
+    s = torch.arange(20, device="cuda", dtype=torch.int64)
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_sample(g, s, [5], 1, blocks)
+    assert e.value.name == "E_CAPACITY"
+
+
+def test_graph_load_validation(H):
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_graph_load(np.array([0, 2, 1, 3]), np.array([0, 1, 2], dtype=np.int32))
+    assert e.value.name == "E_INVALID"
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_graph_load(np.array([0, 1, 2]), np.array([0, 7], dtype=np.int32))
+    assert e.value.name == "E_RANGE"
+
+
+def test_presample_hotness(H, c1):
+    cfg = c1.cfg
+    g = H.helios_graph_load(c1.graph.indptr, c1.graph.indices)
+    seeds = np.concatenate(c1.batches)
+    keys = workloads.presample_keys(len(c1.batches))
+    hot = torch.zeros(cfg.V, dtype=torch.int64, device="cuda")
+    H.helios_presample(g, torch.as_tensor(seeds).cuda(), cfg.B, cfg.fanouts, keys, hot)
+    H.helios_graph_sync(g)
+    ref = oracle.presample(c1.graph.indptr, c1.graph.indices, c1.batches, keys, cfg.fanouts)
+    assert np.array_equal(hot.cpu().numpy().astype(np.uint64), ref)
