@@ -178,6 +178,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--parity-batches", type=int, default=2)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no baseline, no parity")
+    ap.add_argument("--depth", type=int, default=2, help="batches in flight (plan slots)")
+    ap.add_argument("--no-graph", action="store_true", help="launch kernels directly instead of CUDA graphs")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -250,83 +252,98 @@ def main():
     build_s = time.time() - t2
     log(f"graph load + presample {presample_s:.1f}s, cache build {build_s:.1f}s (H={Hr}/GPU, S={S})")
 
-    # ---- timed loop ----
-    blocks = H.Blocks.allocate(cfg.B, cfg.fanouts, g.V, g.E)
-    feats = torch.empty((blocks.nodes.numel(), cfg.R), dtype=torch.uint8, device="cuda")
-    stats = H.new_stats()
+    # ---- timed loop: the execution plan (CUDA graphs, `depth` batches in flight) ----
+    L = len(cfg.fanouts)
     keys = workloads.batch_keys(0, len(inp.batches))
     my_batches = [b for b in range(len(full_batches)) if b % world == rank]
     need = args.warmup + args.steps
     seq = [my_batches[i % len(my_batches)] for i in range(need)]
-    dev_seeds = [torch.as_tensor(inp.batches[b]).cuda() for b in sorted(set(seq))]
-    seed_of = {b: t for b, t in zip(sorted(set(seq)), dev_seeds)}
+    seed_of = {b: torch.as_tensor(inp.batches[b]).cuda() for b in sorted(set(seq))}
     stream = torch.cuda.current_stream()
-    L = len(cfg.fanouts)
-
-    def step(b, ev=None):
-        H.helios_sample(g, seed_of[b], cfg.fanouts, keys[b], blocks, stream)
-        if ev is not None:
-            ev[0].record(stream)
-        H.helios_gather(c, blocks.nodes, blocks.level_counts[L:L + 1], feats, stats, stream)
-        if ev is not None:
-            ev[1].record(stream)
+    depth = args.depth
+    plan = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=depth, flags=H.PLAN_NO_GRAPH if args.no_graph else 0)
 
     for i in range(args.warmup):
-        step(seq[i])
+        H.helios_plan_submit(plan, i % depth, seed_of[seq[i]], keys[seq[i]], stream)
+    for k in range(depth):
+        H.helios_plan_wait(plan, k, stream)
     H.helios_sync(c)
     torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    stat_acc = torch.zeros(4, dtype=torch.int64, device="cuda")
-    nl_acc = torch.zeros(1, dtype=torch.int64, device="cuda")
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push("timed")
     with ClockSampler(local) as clk:
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         start.record(stream)
         for i in range(args.steps):
-            e0, e1, e2 = evs[i]
-            e0.record(stream)
-            step(seq[args.warmup + i], (e1, e2))
-            stat_acc += stats
-            nl_acc += blocks.level_counts[L]
+            b = seq[args.warmup + i]
+            H.helios_plan_submit(plan, i % depth, seed_of[b], keys[b], stream)
+        for k in range(depth):
+            H.helios_plan_wait(plan, k, stream)
         end.record(stream)
         torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     H.helios_sync(c)
     total_ms = start.elapsed_time(end)
-    sample_ms = [evs[i][0].elapsed_time(evs[i][1]) for i in range(args.steps)]
-    gather_ms = [evs[i][1].elapsed_time(evs[i][2]) for i in range(args.steps)]
+    sample_ms, gather_ms = [], []
+    for k in range(depth):
+        n_k = len(range(k, args.steps, depth))
+        for back in range(min(n_k, 255)):
+            a, b_ = H.helios_plan_timing(plan, k, back)
+            sample_ms.append(a)
+            gather_ms.append(b_)
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
     max_ms = float(t.item())
-    st = stat_acc.cpu().tolist()
-    n_rows = int(nl_acc.item())
+    if args.profile:
+        print(json.dumps({"profile_run": True, "ms_per_step": max_ms / args.steps}), flush=True)
+        return
+    # per-batch row counts of the timed batches (deterministic; re-run untimed through slot 0)
+    st = [0, 0, 0, 0]
+    n_rows = 0
+    blk0, _, stats0 = plan.outputs[0]
+    for i in range(args.steps):
+        b = seq[args.warmup + i]
+        H.helios_plan_submit(plan, 0, seed_of[b], keys[b], stream)
+        H.helios_plan_wait(plan, 0, stream)
+        stream.synchronize()
+        st = [x + int(y) for x, y in zip(st, stats0.cpu().tolist())]
+        n_rows += int(blk0.level_counts[L].item())
+    H.helios_sync(c)
 
     # ---- e2e: through the public API with host buffers (pinned seeds in, counts out) ----
-    pin_seeds = {b: torch.as_tensor(inp.batches[b]).pin_memory() for b in sorted(set(seq))}
-    out_host = torch.empty(L + 1 + 4, dtype=torch.int64).pin_memory()
-    dseeds = torch.empty(cfg.B, dtype=torch.int64, device="cuda")
+    host_seeds = {b: np.ascontiguousarray(inp.batches[b]) for b in sorted(set(seq))}
+    out_host = torch.empty(depth, L + 1 + 4, dtype=torch.int64).pin_memory()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+
+    def consume(k):
+        blk, _, sts = plan.outputs[k]
+        H.helios_plan_wait(plan, k, stream)
+        out_host[k, : L + 1].copy_(blk.level_counts, non_blocking=True)
+        out_host[k, L + 1:].copy_(sts, non_blocking=True)
+
     t_e2e = time.perf_counter()
     for i in range(args.steps):
         b = seq[args.warmup + i]
-        dseeds.copy_(pin_seeds[b], non_blocking=True)
-        H.helios_batch_prepare(g, c, dseeds, cfg.fanouts, keys[b], blocks, feats, stats, stream)
-        out_host[: L + 1].copy_(blocks.level_counts, non_blocking=True)
-        out_host[L + 1:].copy_(stats, non_blocking=True)
-        stream.synchronize()
+        H.helios_plan_submit(plan, i % depth, host_seeds[b], keys[b], stream)
+        if i >= depth - 1:
+            consume((i - depth + 1) % depth)
+            stream.synchronize()
+    for i in range(max(0, args.steps - depth + 1), args.steps):
+        consume(i % depth)
+    stream.synchronize()
     e2e_s = time.perf_counter() - t_e2e
+    H.helios_sync(c)
     e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_s = float(e2e_t.item())
-
     # ---- parity at full size: GPU batches vs the oracle, bit for bit (rank 0) ----
     parity = None
     cpu = None
@@ -334,9 +351,12 @@ def main():
         import oracle
         checked, ok = 0, True
         pb = sorted(set(seq))[: args.parity_batches]
-        for b in pb:
-            H.helios_batch_prepare(g, c, seed_of[b], cfg.fanouts, keys[b], blocks, feats, stats, stream)
+        for j, b in enumerate(pb):   # the timed launch configuration: plan slots + CUDA graphs
+            k = j % depth
+            H.helios_plan_submit(plan, k, seed_of[b], keys[b], stream)
+            H.helios_plan_wait(plan, k, stream)
             H.helios_sync(c)
+            blocks, feats, _ = plan.outputs[k]
             got = blocks.to_host()
             ob = oracle.sample(inp.graph.indptr, inp.graph.indices, inp.batches[b], cfg.fanouts, keys[b])
             ok &= np.array_equal(got["nodes"], ob.nodes)
@@ -375,7 +395,7 @@ def main():
                    key=lambda x: x[1])[0]
     value = world * steps / (max_ms / 1e3)
     e2e_val = world * steps / e2e_s
-    launches_per_step = 1 + 5 * L + 1
+    launches_per_step = 2 + 3 * L + 1 + (3 if c.info().file_rows > 0 else 0)
     out = {
         "metric": "sampled+gathered mini-batches/sec (feature GB/s and tier-roofline fraction alongside)",
         "value": round(value, 3), "unit": "batches/s", "n_gpus": world, "steps": steps, "warmup": args.warmup,
@@ -388,7 +408,8 @@ def main():
                    "l2": "inputs larger than L2 (CSR %.1f GB, feature table %.1f GB); no flush" % (
                        (inp.graph.E * 4 + cfg.V * 8) / 1e9, cfg.V * R / 1e9)},
         "feature_gbs": round(world * n_rows / steps * R * steps / (max_ms / 1e3) / 1e9, 2),
-        "stage_ms": {"sample": round(statistics.mean(sample_ms), 4), "gather": round(g_ms, 4)},
+        "stage_ms": {"sample": round(statistics.mean(sample_ms), 4), "gather": round(g_ms, 4),
+                     "note": f"per batch, device events around the two graph segments, {depth} batches in flight"},
         "rows_per_batch": {"n_L": round(nL, 1), "hbm_local": round(n_local, 1), "hbm_peer": round(n_peer, 1),
                            "host": round(n_host, 1), "file": round(n_file, 1)},
         "roofline": {"bound": dominant, "kernel": "k_lookup_gather (K3+K4)", "achieved": round(achieved, 2),
@@ -409,6 +430,7 @@ def main():
     }
     if rank == 0:
         print(json.dumps(out), flush=True)
+    plan.free()
     c.free()
     g.free()
     if world > 1:

@@ -207,6 +207,50 @@ helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64
                                    const int32_t* fanouts, int32_t L, uint64_t key, const helios_blocks* out,
                                    void* features, helios_gather_stats* stats, void* stream);
 
+/* ---- Execution plan: CUDA-graph replay + in-flight batch slots ------------------------------
+ * The paper's runtime "decomposes GNN model execution into a sequence of GPU-initiated operators"
+ * and builds an intra- and inter-mini-batch pipeline plan (§3.3).  A plan owns
+ * `depth` slots; each slot has its own sampling workspace, output buffers, stream and a CUDA graph
+ * of the whole batch (sampling kernels + lookup/gather), captured once at creation and replayed per
+ * batch (key and n_seeds are read from device memory).  Batches submitted to different slots run
+ * concurrently (sampling of batch i+1 overlaps the gather of batch i); FILE-tier IO of successive
+ * batches is serialised on the cache's IO streams.
+ *   desc.max_seeds   B: capacity of every slot (n_seeds <= B per submit).
+ *   desc.L, fanouts  hops and fanouts (as helios_sample).
+ *   desc.depth       number of slots, 1..8.
+ *   desc.flags       HELIOS_PLAN_NO_GRAPH: launch the kernels directly on every submit.
+ *   c                cache, or NULL for a sampling-only plan (no features / stats).
+ * Blocking create/free. */
+#define HELIOS_PLAN_NO_GRAPH 0x1u
+#define HELIOS_SUBMIT_SEEDS_HOST 0x1u  /* seeds pointer is host memory (copied to the slot, H2D) */
+typedef struct helios_plan helios_plan;
+typedef struct {
+  int64_t max_seeds;
+  int32_t L;
+  int32_t fanouts[HELIOS_MAX_HOPS];
+  int32_t depth;
+  uint32_t flags;
+} helios_plan_desc;
+helios_status helios_plan_create(helios_graph* g, helios_cache* c, const helios_plan_desc* desc, helios_plan** out);
+void helios_plan_free(helios_plan* p);
+/* Plan-owned DEVICE outputs of `slot` (valid until helios_plan_free): the slot's blocks, its
+ * feature buffer [blocks->nodes_cap, row_bytes] (NULL without cache) and its gather stats. */
+helios_status helios_plan_outputs(helios_plan* p, int32_t slot, helios_blocks* blocks, void** features,
+                                  helios_gather_stats** stats);
+/* Enqueue one batch into `slot`: ordered after all work already enqueued on `stream` (so the
+ * caller may produce the seeds there and must have enqueued its consumption of the slot's previous
+ * outputs there) and after the slot's previous batch.  seeds: device int64[n_seeds] (or host with
+ * HELIOS_SUBMIT_SEEDS_HOST; copied before return is NOT guaranteed for device seeds — keep them
+ * alive until the batch completes).  n_seeds <= desc.max_seeds (else E_CAPACITY). */
+helios_status helios_plan_submit(helios_plan* p, int32_t slot, const int64_t* seeds, int64_t n_seeds, uint64_t key,
+                                 uint32_t flags, void* stream);
+/* Makes `stream` wait for the last batch submitted to `slot`. */
+helios_status helios_plan_wait(helios_plan* p, int32_t slot, void* stream);
+/* Device time (ms) of the sampling and gather phases of a batch of `slot`: back = 0 is the slot's
+ * last submitted batch, back = k the k-th before it (k < 256; CUDA events recorded around the two
+ * graph segments).  Blocks until that batch is done; E_RANGE if it is no longer recorded. */
+helios_status helios_plan_timing(helios_plan* p, int32_t slot, int32_t back, float* sample_ms, float* gather_ms);
+
 /* Waits for `stream` and the cache's IO streams; returns and clears latched errors of the cache
  * and its graph (E_IO, E_TIMEOUT, E_INVALID, E_RANGE). */
 helios_status helios_sync(helios_cache* c, void* stream);

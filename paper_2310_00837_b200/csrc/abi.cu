@@ -23,8 +23,28 @@ helios_status fail(helios_status st, const char* fmt, ...) {
 }
 
 helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, helios_cache* c);
-helios_status cache_ensure_miss_cap(helios_cache* c, int64_t max_nodes);
 void cache_free_impl(helios_cache* c);
+void plan_free_impl(helios_plan* p);
+helios_status plan_create_impl(helios_plan* p);
+helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seeds, int64_t n, uint64_t key, uint32_t flags,
+                               cudaStream_t caller);
+helios_status plan_wait_impl(helios_plan* p, int32_t slot, cudaStream_t st);
+helios_status plan_timing_impl(helios_plan* p, int32_t slot, int32_t back, float* sample_ms, float* gather_ms);
+helios_status plan_outputs_impl(helios_plan* p, int32_t slot, helios_blocks* blocks, void** features,
+                                helios_gather_stats** stats);
+
+// helios_sample on the graph's default sampling context.
+static helios_status sample_default(helios_graph* g, const int64_t* seeds, int64_t B, const int32_t* fanouts, int32_t L,
+                                    uint64_t key, const helios_blocks* out, cudaStream_t st) {
+  helios_status s = sample_check_out(g, B, fanouts, L, out);
+  if (s != HELIOS_OK) return s;
+  HCHECK(B == 0 || seeds, HELIOS_E_INVALID, "null seeds");
+  s = ws_ensure(g, g->ws, B, fanouts, L);
+  if (s != HELIOS_OK) return s;
+  s = ws_upload_params(g->ws, key, B, st);
+  if (s != HELIOS_OK) return s;
+  return sample_launch(g, g->ws, seeds, B, fanouts, L, out, st);
+}
 
 static helios_status read_latched(int* d_err, helios_status* out) {
   int h = 0;
@@ -109,8 +129,7 @@ void helios_graph_free(helios_graph* g) {
   cudaFree(g->indptr);
   cudaFree(g->indices);
   cudaFree(g->d_err);
-  if (g->ws.reset_base) cudaFree(g->ws.reset_base);
-  if (g->ws.slot_of) cudaFree(g->ws.slot_of);
+  ws_free(g->ws);
   if (g->pre_mem) cudaFree(g->pre_mem);
   delete g;
 }
@@ -142,7 +161,7 @@ helios_status helios_sample(helios_graph* g, const int64_t* seeds, int64_t n_see
   GUARD_BEGIN
   HCHECK(g, HELIOS_E_INVALID, "null graph");
   DeviceGuard dg(g->device);
-  return sample_enqueue(g, seeds, n_seeds, fanouts, L, key, out, (cudaStream_t)stream);
+  return sample_default(g, seeds, n_seeds, fanouts, L, key, out, (cudaStream_t)stream);
   GUARD_END
 }
 
@@ -201,7 +220,7 @@ helios_status helios_presample(helios_graph* g, const int64_t* seeds, int64_t n_
   }
   for (int64_t b = 0, i = 0; i < n_seeds; b++, i += batch) {
     int64_t nb = std::min<int64_t>(batch, n_seeds - i);
-    s = sample_enqueue(g, seeds + i, nb, fanouts, L, keys[b], &g->pre_blocks, st);
+    s = sample_default(g, seeds + i, nb, fanouts, L, keys[b], &g->pre_blocks, st);
     if (s != HELIOS_OK) return s;
     s = hot_count_enqueue(g->pre_blocks.nodes, g->pre_blocks.level_counts + L, maxn, hotness, g->sms, st);
     if (s != HELIOS_OK) return s;
@@ -317,9 +336,11 @@ helios_status helios_gather(helios_cache* c, const int64_t* nodes, const int64_t
   GUARD_BEGIN
   HCHECK(c, HELIOS_E_INVALID, "null cache");
   DeviceGuard dg(c->device);
-  helios_status st = cache_ensure_miss_cap(c, max_nodes);
+  helios_status st = gws_ensure(c, c->gws, max_nodes);
   if (st != HELIOS_OK) return st;
-  return gather_enqueue(c, nodes, n_nodes, max_nodes, out, stats, (cudaStream_t)stream);
+  st = gather_launch(c, c->gws, nodes, n_nodes, max_nodes, out, stats, (cudaStream_t)stream);
+  if (st != HELIOS_OK) return st;
+  return io_launch(c, c->gws, out, (cudaStream_t)stream);
   GUARD_END
 }
 
@@ -330,11 +351,80 @@ helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64
   HCHECK(g && c && out, HELIOS_E_INVALID, "null argument");
   HCHECK(c->g == g, HELIOS_E_INVALID, "cache was built on another graph");
   DeviceGuard dg(g->device);
-  helios_status st = sample_enqueue(g, seeds, n_seeds, fanouts, L, key, out, (cudaStream_t)stream);
-  if (st != HELIOS_OK) return st;
-  st = cache_ensure_miss_cap(c, out->nodes_cap);
-  if (st != HELIOS_OK) return st;
-  return gather_enqueue(c, out->nodes, out->level_counts + L, out->nodes_cap, features, stats, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  helios_status s = sample_default(g, seeds, n_seeds, fanouts, L, key, out, st);
+  if (s != HELIOS_OK) return s;
+  s = gws_ensure(c, c->gws, out->nodes_cap);
+  if (s != HELIOS_OK) return s;
+  s = gather_launch(c, c->gws, out->nodes, out->level_counts + L, out->nodes_cap, features, stats, st);
+  if (s != HELIOS_OK) return s;
+  return io_launch(c, c->gws, features, st);
+  GUARD_END
+}
+
+helios_status helios_plan_create(helios_graph* g, helios_cache* c, const helios_plan_desc* d, helios_plan** out) {
+  GUARD_BEGIN
+  HCHECK(g && d && out, HELIOS_E_INVALID, "null argument");
+  *out = nullptr;
+  HCHECK(!c || c->g == g, HELIOS_E_INVALID, "cache was built on another graph");
+  HCHECK(d->depth >= 1 && d->depth <= 8, HELIOS_E_INVALID, "plan depth %d not in [1,8]", d->depth);
+  HCHECK(d->max_seeds >= 0, HELIOS_E_INVALID, "max_seeds < 0");
+  DeviceGuard dg(g->device);
+  helios_plan* p = new helios_plan();
+  p->g = g;
+  p->c = c;
+  p->d = *d;
+  p->graphs = !(d->flags & HELIOS_PLAN_NO_GRAPH);
+  helios_status st = plan_create_impl(p);
+  if (st != HELIOS_OK) {
+    std::string keep = helios_last_error();
+    plan_free_impl(p);
+    delete p;
+    set_error(keep);
+    return st;
+  }
+  *out = p;
+  return HELIOS_OK;
+  GUARD_END
+}
+
+void helios_plan_free(helios_plan* p) {
+  if (!p) return;
+  DeviceGuard dg(p->g->device);
+  plan_free_impl(p);
+  delete p;
+}
+
+helios_status helios_plan_outputs(helios_plan* p, int32_t slot, helios_blocks* blocks, void** features,
+                                  helios_gather_stats** stats) {
+  GUARD_BEGIN
+  HCHECK(p, HELIOS_E_INVALID, "null plan");
+  return plan_outputs_impl(p, slot, blocks, features, stats);
+  GUARD_END
+}
+
+helios_status helios_plan_submit(helios_plan* p, int32_t slot, const int64_t* seeds, int64_t n_seeds, uint64_t key,
+                                 uint32_t flags, void* stream) {
+  GUARD_BEGIN
+  HCHECK(p, HELIOS_E_INVALID, "null plan");
+  DeviceGuard dg(p->g->device);
+  return plan_submit_impl(p, slot, seeds, n_seeds, key, flags, (cudaStream_t)stream);
+  GUARD_END
+}
+
+helios_status helios_plan_wait(helios_plan* p, int32_t slot, void* stream) {
+  GUARD_BEGIN
+  HCHECK(p, HELIOS_E_INVALID, "null plan");
+  DeviceGuard dg(p->g->device);
+  return plan_wait_impl(p, slot, (cudaStream_t)stream);
+  GUARD_END
+}
+
+helios_status helios_plan_timing(helios_plan* p, int32_t slot, int32_t back, float* sample_ms, float* gather_ms) {
+  GUARD_BEGIN
+  HCHECK(p, HELIOS_E_INVALID, "null plan");
+  DeviceGuard dg(p->g->device);
+  return plan_timing_impl(p, slot, back, sample_ms, gather_ms);
   GUARD_END
 }
 

@@ -144,8 +144,6 @@ helios_status io_start(helios_cache* c, const helios_cache_desc* d) {
   HCUDA(cudaMemset(io.d_free_seq, 0, n * 4));
   HCUDA(cudaMalloc(&io.d_base_seq, io.rings * 4));
   HCUDA(cudaMemset(io.d_base_seq, 0, io.rings * 4));
-  HCUDA(cudaMalloc(&io.d_ctl, 4 * sizeof(unsigned long long)));
-  HCUDA(cudaMemset(io.d_ctl, 0, 4 * sizeof(unsigned long long)));
   // O_DIRECT probe: one aligned read; fall back to buffered IO if the filesystem refuses it
   if (io.direct) {
     ssize_t got = pread(io.fd, io.staging, io.slot_bytes < 4096 ? 4096 : 4096, 0);
@@ -175,15 +173,10 @@ void io_stop(helios_cache* c) {
   if (io.staging) cudaFreeHost(io.staging);
   if (io.d_free_seq) cudaFree(io.d_free_seq);
   if (io.d_base_seq) cudaFree(io.d_base_seq);
-  if (io.d_ctl) cudaFree(io.d_ctl);
-  if (io.d_miss_out) cudaFree(io.d_miss_out);
-  if (io.d_miss_row) cudaFree(io.d_miss_row);
   io.sq = nullptr;
   io.cq = nullptr;
   io.staging = nullptr;
   io.d_free_seq = io.d_base_seq = nullptr;
-  io.d_ctl = nullptr;
-  io.d_miss_out = io.d_miss_row = nullptr;
 }
 
 // ---- file reads for setup (tier fill) ------------------------------------------------------
@@ -351,6 +344,7 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
   HCUDA(cudaEventCreateWithFlags(&c->ev_lookup, cudaEventDisableTiming));
   HCUDA(cudaEventCreateWithFlags(&c->ev_submit, cudaEventDisableTiming));
   HCUDA(cudaEventCreateWithFlags(&c->ev_complete, cudaEventDisableTiming));
+  HCUDA(cudaEventCreateWithFlags(&c->ev_io_done, cudaEventDisableTiming));
   if (c->has_file) {
     st = io_start(c, d);
     if (st != HELIOS_OK) return st;
@@ -358,20 +352,10 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
   return HELIOS_OK;
 }
 
-helios_status cache_ensure_miss_cap(helios_cache* c, int64_t max_nodes) {
-  if (!c->has_file || max_nodes <= c->io.miss_cap) return HELIOS_OK;
-  HCUDA(cudaDeviceSynchronize());
-  if (c->io.d_miss_out) cudaFree(c->io.d_miss_out);
-  if (c->io.d_miss_row) cudaFree(c->io.d_miss_row);
-  HCUDA(cudaMalloc(&c->io.d_miss_out, max_nodes * 8));
-  HCUDA(cudaMalloc(&c->io.d_miss_row, max_nodes * 8));
-  c->io.miss_cap = max_nodes;
-  return HELIOS_OK;
-}
-
 void cache_free_impl(helios_cache* c) {
   cudaDeviceSynchronize();
   io_stop(c);
+  gws_free(c->gws);
   for (int r = 0; r < HELIOS_MAX_RANKS; r++)
     if (r != c->rank && c->peer_ptrs[r]) cudaIpcCloseMemHandle(c->peer_ptrs[r]);
   if (c->host_registered) cudaHostUnregister((void*)c->host_table);
@@ -385,6 +369,7 @@ void cache_free_impl(helios_cache* c) {
   if (c->ev_lookup) cudaEventDestroy(c->ev_lookup);
   if (c->ev_submit) cudaEventDestroy(c->ev_submit);
   if (c->ev_complete) cudaEventDestroy(c->ev_complete);
+  if (c->ev_io_done) cudaEventDestroy(c->ev_io_done);
 }
 
 }  // namespace helios

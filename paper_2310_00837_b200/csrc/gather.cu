@@ -299,13 +299,33 @@ static void launch_gather(const GatherArgs& a, int sms, cudaStream_t st) {
   k_lookup_gather<VPL, U><<<sms * 8, 256, 0, st>>>(a);
 }
 
-helios_status gather_enqueue(helios_cache* c, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, void* out,
-                             helios_gather_stats* stats, cudaStream_t st) {
+void gws_free(GatherWS& w) {
+  if (w.d_miss_out) cudaFree(w.d_miss_out);
+  if (w.d_miss_row) cudaFree(w.d_miss_row);
+  if (w.d_ctl) cudaFree(w.d_ctl);
+  w = GatherWS{};
+}
+
+helios_status gws_ensure(helios_cache* c, GatherWS& w, int64_t max_nodes) {
+  if (!c->has_file || (w.d_ctl && max_nodes <= w.miss_cap)) return HELIOS_OK;
+  HCUDA(cudaDeviceSynchronize());
+  gws_free(w);
+  HCUDA(cudaMalloc(&w.d_miss_out, std::max<int64_t>(max_nodes, 1) * 8));
+  HCUDA(cudaMalloc(&w.d_miss_row, std::max<int64_t>(max_nodes, 1) * 8));
+  HCUDA(cudaMalloc(&w.d_ctl, 4 * sizeof(unsigned long long)));
+  HCUDA(cudaMemset(w.d_ctl, 0, 4 * sizeof(unsigned long long)));
+  w.miss_cap = max_nodes;
+  return HELIOS_OK;
+}
+
+helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes,
+                            void* out, helios_gather_stats* stats, cudaStream_t st) {
   HCHECK(nodes && n_nodes && (out || max_nodes == 0), HELIOS_E_INVALID, "null gather argument");
   HCHECK(c->G == 1 || c->peers_attached, HELIOS_E_STATE, "world_size %d but peers not attached", c->G);
-  HCHECK(!c->has_file || max_nodes <= c->io.miss_cap, HELIOS_E_CAPACITY, "max_nodes %lld > miss list cap %lld",
-         (long long)max_nodes, (long long)c->io.miss_cap);
+  HCHECK(!c->has_file || (w.d_ctl && max_nodes <= w.miss_cap), HELIOS_E_CAPACITY,
+         "max_nodes %lld > miss list cap %lld", (long long)max_nodes, (long long)w.miss_cap);
   if (stats) HCUDA(cudaMemsetAsync(stats, 0, sizeof(helios_gather_stats), st));
+  if (c->has_file) HCUDA(cudaMemsetAsync(w.d_ctl, 0, 4 * sizeof(unsigned long long), st));
   GatherArgs a;
   a.nodes = nodes;
   a.n_nodes = n_nodes;
@@ -316,49 +336,60 @@ helios_status gather_enqueue(helios_cache* c, const int64_t* nodes, const int64_
   a.hbm = c->hbm;
   a.peers = c->d_peers;
   a.host_dev = c->d_host_tier;
-  a.miss_out = c->io.d_miss_out;
-  a.miss_row = c->io.d_miss_row;
-  a.miss_count = c->io.d_ctl;
+  a.miss_out = w.d_miss_out;
+  a.miss_row = w.d_miss_row;
+  a.miss_count = w.d_ctl;
   a.stats = stats;
-  if (c->has_file) HCUDA(cudaMemsetAsync(c->io.d_ctl, 0, 4 * sizeof(unsigned long long), st));
   const int nvec = c->R / 16;
   if (nvec <= 32) launch_gather<1, 4>(a, c->sms, st);
   else if (nvec <= 64) launch_gather<2, 2>(a, c->sms, st);
   else if (nvec <= 128) launch_gather<4, 1>(a, c->sms, st);
   else launch_gather<8, 1>(a, c->sms, st);
   HCUDA(cudaGetLastError());
-  if (c->has_file) {
-    IoArgs io;
-    io.miss_out = c->io.d_miss_out;
-    io.miss_row = c->io.d_miss_row;
-    io.ctl = c->io.d_ctl;
-    io.sq = c->io.d_sq;
-    io.cq = c->io.d_cq;
-    io.staging = c->io.d_staging;
-    io.free_seq = c->io.d_free_seq;
-    io.base_seq = c->io.d_base_seq;
-    io.rings = c->io.rings;
-    io.depth = c->io.depth;
-    io.slot_bytes = c->io.slot_bytes;
-    io.header = c->header;
-    io.stride = c->stride;
-    io.len = (int32_t)c->stride;
-    io.R = c->R;
-    io.out = (char*)out;
-    io.err = c->d_err;
-    HCUDA(cudaEventRecord(c->ev_lookup, st));
-    HCUDA(cudaStreamWaitEvent(c->s_submit, c->ev_lookup, 0));
-    HCUDA(cudaStreamWaitEvent(c->s_complete, c->ev_lookup, 0));
-    k_io_complete<<<c->io_ctas, 256, 0, c->s_complete>>>(io);
-    k_io_submit<<<c->io_ctas, 256, 0, c->s_submit>>>(io);
-    HCUDA(cudaGetLastError());
-    HCUDA(cudaEventRecord(c->ev_submit, c->s_submit));
-    HCUDA(cudaEventRecord(c->ev_complete, c->s_complete));
-    HCUDA(cudaStreamWaitEvent(st, c->ev_submit, 0));
-    HCUDA(cudaStreamWaitEvent(st, c->ev_complete, 0));
-    k_io_finish<<<1, 64, 0, st>>>(c->io.d_ctl, c->io.d_base_seq, c->io.rings);
-    HCUDA(cudaGetLastError());
+  return HELIOS_OK;
+}
+
+// K5 / K6 on the cache's IO streams for the misses recorded in w by the preceding gather_launch on
+// `st`.  IO batches are serialised across gather contexts through ev_io_done (ring sequence
+// numbers advance per batch in k_io_finish).
+helios_status io_launch(helios_cache* c, GatherWS& w, void* out, cudaStream_t st) {
+  if (!c->has_file) return HELIOS_OK;
+  IoArgs io;
+  io.miss_out = w.d_miss_out;
+  io.miss_row = w.d_miss_row;
+  io.ctl = w.d_ctl;
+  io.sq = c->io.d_sq;
+  io.cq = c->io.d_cq;
+  io.staging = c->io.d_staging;
+  io.free_seq = c->io.d_free_seq;
+  io.base_seq = c->io.d_base_seq;
+  io.rings = c->io.rings;
+  io.depth = c->io.depth;
+  io.slot_bytes = c->io.slot_bytes;
+  io.header = c->header;
+  io.stride = c->stride;
+  io.len = (int32_t)c->stride;
+  io.R = c->R;
+  io.out = (char*)out;
+  io.err = c->d_err;
+  HCUDA(cudaEventRecord(c->ev_lookup, st));
+  HCUDA(cudaStreamWaitEvent(c->s_submit, c->ev_lookup, 0));
+  HCUDA(cudaStreamWaitEvent(c->s_complete, c->ev_lookup, 0));
+  if (c->io_pending) {
+    HCUDA(cudaStreamWaitEvent(c->s_submit, c->ev_io_done, 0));
+    HCUDA(cudaStreamWaitEvent(c->s_complete, c->ev_io_done, 0));
   }
+  k_io_complete<<<c->io_ctas, 256, 0, c->s_complete>>>(io);
+  k_io_submit<<<c->io_ctas, 256, 0, c->s_submit>>>(io);
+  HCUDA(cudaGetLastError());
+  HCUDA(cudaEventRecord(c->ev_submit, c->s_submit));
+  HCUDA(cudaEventRecord(c->ev_complete, c->s_complete));
+  HCUDA(cudaStreamWaitEvent(st, c->ev_submit, 0));
+  HCUDA(cudaStreamWaitEvent(st, c->ev_complete, 0));
+  k_io_finish<<<1, 64, 0, st>>>(w.d_ctl, c->io.d_base_seq, c->io.rings);
+  HCUDA(cudaGetLastError());
+  HCUDA(cudaEventRecord(c->ev_io_done, st));
+  c->io_pending = true;
   return HELIOS_OK;
 }
 

@@ -56,10 +56,10 @@ struct ScanState {
   unsigned int* counter;       // tile ticket (all-ones -> first ticket is 0)
 };
 
-// Sampling workspace (per graph handle).
+// Sampling workspace: one per sampling context (the graph's default context, and one per plan
+// slot so that consecutive batches can be in flight concurrently).
 struct SampleWS {
-  int64_t cap_nodes = 0, cap_edges = 0, cap_tiles_rows = 0, cap_tiles_edges = 0;
-  int L = 0;
+  int64_t cap_edges = 0, cap_tiles_rows = 0, cap_tiles_edges = 0, cap_seeds = 0;
   uint32_t table_size = 0;   // power of two
   // reset region (one cudaMemsetAsync(0xFF) per batch): keys | minpos | local | scan status | counters
   char* reset_base = nullptr;
@@ -69,7 +69,20 @@ struct SampleWS {
   uint32_t* local = nullptr;
   ScanState row_scan[HELIOS_MAX_HOPS];
   ScanState edge_scan[HELIOS_MAX_HOPS];
-  uint32_t* slot_of = nullptr;  // [cap_edges]
+  uint32_t* slot_of = nullptr;  // [cap_edges] hash slot of each sampled edge of the current hop
+  // per-batch parameters, read by the kernels from device memory so that a captured CUDA graph
+  // can be replayed for every batch: [0] key, [1] n_seeds
+  int64_t* d_params = nullptr;
+  int64_t* h_params = nullptr;  // pinned staging for the parameter upload
+  cudaEvent_t params_ev = nullptr;
+};
+
+// Per-gather IO bookkeeping (miss list + tickets); one per gather context.
+struct GatherWS {
+  int64_t miss_cap = 0;
+  int64_t* d_miss_out = nullptr;    // output row of each FILE-tier miss
+  int64_t* d_miss_row = nullptr;    // file row of each miss
+  unsigned long long* d_ctl = nullptr;  // [0] miss count, [1] submit ticket, [2] complete ticket
 };
 
 struct helios_graph_impl;
@@ -120,11 +133,6 @@ struct IoRings {
   // device-side ring state
   uint32_t* d_free_seq = nullptr;   // [rings*depth] last sequence consumed by io_complete per slot
   uint32_t* d_base_seq = nullptr;   // [rings] sequences issued before the current batch
-  // miss list (device)
-  int64_t miss_cap = 0;
-  int64_t* d_miss_out = nullptr;    // output row of each miss
-  int64_t* d_miss_row = nullptr;    // file row of each miss
-  unsigned long long* d_ctl = nullptr;  // [0] miss count, [1] submit ticket, [2] complete ticket
   // host workers
   std::vector<std::thread> workers;
   std::atomic<bool> stop{false};
@@ -163,21 +171,67 @@ struct helios_cache {
   int io_ctas = 32;
   helios::IoRings io;
   bool has_file = false;
+  helios::GatherWS gws;            // default gather context (helios_gather / helios_batch_prepare)
   cudaStream_t s_submit = nullptr, s_complete = nullptr;
-  cudaEvent_t ev_lookup = nullptr, ev_submit = nullptr, ev_complete = nullptr;
+  cudaEvent_t ev_lookup = nullptr, ev_submit = nullptr, ev_complete = nullptr, ev_io_done = nullptr;
+  bool io_pending = false;         // ev_io_done recorded at least once
+};
+
+#include <vector>
+namespace helios {
+
+struct PlanSlot {
+  SampleWS ws;
+  GatherWS gws;
+  helios_blocks blocks{};
+  void* mem = nullptr;
+  char* feats = nullptr;
+  helios_gather_stats* stats = nullptr;
+  int64_t* d_seeds = nullptr;
+  int64_t* h_seeds = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaGraphExec_t g_sample = nullptr, g_gather = nullptr;
+  cudaEvent_t ev_caller = nullptr, ev_end = nullptr;
+  static constexpr int kRing = 256;
+  std::vector<cudaEvent_t> ring;  // kRing x {start, mid, end} timing events
+  int64_t count = 0;              // batches submitted to this slot
+  bool submitted = false;
+};
+
+}  // namespace helios
+
+struct helios_plan {
+  helios_graph* g = nullptr;
+  helios_cache* c = nullptr;
+  helios_plan_desc d{};
+  int64_t maxn = 0;
+  bool graphs = true;
+  std::vector<helios::PlanSlot> slots;
 };
 
 namespace helios {
 
 // Launch helpers implemented in the .cu files.
-helios_status sample_enqueue(helios_graph* g, const int64_t* seeds, int64_t n_seeds, const int32_t* fanouts, int32_t L,
-                             uint64_t key, const helios_blocks* out, cudaStream_t st);
 helios_status sample_bounds(int64_t n_seeds, const int32_t* fanouts, int32_t L, int64_t V, int64_t E,
                             int64_t* max_nodes, int64_t* level, int64_t* edges);
+helios_status sample_check_out(const helios_graph* g, int64_t B, const int32_t* fanouts, int32_t L,
+                               const helios_blocks* out);
+helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* fanouts, int32_t L);
+void ws_free(SampleWS& w);
+// Uploads (key, n_seeds) into w.d_params on `st` (not capturable; done before a graph replay).
+helios_status ws_upload_params(SampleWS& w, uint64_t key, int64_t B, cudaStream_t st);
+// Enqueues the sampling kernels; they read key / n_seeds from w.d_params.  B_max sizes the grids.
+helios_status sample_launch(helios_graph* g, SampleWS& w, const int64_t* seeds, int64_t B_max, const int32_t* fanouts,
+                            int32_t L, const helios_blocks* out, cudaStream_t st);
 helios_status hot_count_enqueue(const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, uint64_t* hot,
                                 int sms, cudaStream_t st);
-helios_status gather_enqueue(helios_cache* c, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, void* out,
-                             helios_gather_stats* stats, cudaStream_t st);
+helios_status gws_ensure(helios_cache* c, GatherWS& w, int64_t max_nodes);
+void gws_free(GatherWS& w);
+// Lookup + gather of the HBM / host tiers; FILE-tier rows are appended to w's miss list.
+helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes,
+                            void* out, helios_gather_stats* stats, cudaStream_t st);
+// IO rings for the misses of the last gather_launch on `st` (not capturable: cross-stream events).
+helios_status io_launch(helios_cache* c, GatherWS& w, void* out, cudaStream_t st);
 helios_status validate_csr_device(const int64_t* indptr, const int32_t* indices, int64_t V, int64_t E, int* d_flag,
                                   cudaStream_t st);
 helios_status cache_sort_and_dir(helios_cache* c, const uint64_t* hot, int32_t* d_order /*[V]*/);

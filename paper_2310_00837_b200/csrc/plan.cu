@@ -1,0 +1,199 @@
+// plan.cu — execution plan: per-slot workspaces + CUDA graphs of a whole mini-batch.
+//
+// The paper's runtime splits a training iteration into GPU-initiated operators, builds an intra-
+// and inter-mini-batch pipeline plan and launches the operators on asynchronous streams
+// (§3.3, Fig. pipeline_design).  Here a plan slot is one in-flight mini-batch:
+// its sampling operators (K1/K2) and lookup/gather operator (K3/K4) are captured once into two CUDA
+// graphs and replayed for every batch on the slot's stream; slots run concurrently, so the
+// sampling of batch i+1 overlaps the gather of batch i (the inter-mini-batch pipeline).  File-tier
+// IO operators (K5/K6) are launched per batch behind the graphs (they wait on cross-stream events).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace helios {
+
+void plan_free_impl(helios_plan* p) {
+  cudaDeviceSynchronize();
+  for (auto& s : p->slots) {
+    ws_free(s.ws);
+    gws_free(s.gws);
+    if (s.mem) cudaFree(s.mem);
+    if (s.feats) cudaFree(s.feats);
+    if (s.d_seeds) cudaFree(s.d_seeds);
+    if (s.h_seeds) cudaFreeHost(s.h_seeds);
+    if (s.g_sample) cudaGraphExecDestroy(s.g_sample);
+    if (s.g_gather) cudaGraphExecDestroy(s.g_gather);
+    for (cudaEvent_t e : {s.ev_caller, s.ev_end})
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : s.ring)
+      if (e) cudaEventDestroy(e);
+    if (s.stream) cudaStreamDestroy(s.stream);
+  }
+  p->slots.clear();
+}
+
+template <typename F>
+static helios_status capture(cudaStream_t st, cudaGraphExec_t* out, F&& body) {
+  HCUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  helios_status s = body();
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(st, &graph);
+  if (s != HELIOS_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return s;
+  }
+  if (e != cudaSuccess) return fail(HELIOS_E_CUDA, "stream capture failed: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(out, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(HELIOS_E_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e));
+  return HELIOS_OK;
+}
+
+helios_status plan_create_impl(helios_plan* p) {
+  helios_graph* g = p->g;
+  const helios_plan_desc& d = p->d;
+  int64_t lvl[HELIOS_MAX_HOPS + 1], edg[HELIOS_MAX_HOPS];
+  helios_status s = sample_bounds(d.max_seeds, d.fanouts, d.L, g->V, g->E, &p->maxn, lvl, edg);
+  if (s != HELIOS_OK) return s;
+  p->slots.resize(d.depth);
+  for (int k = 0; k < d.depth; k++) {
+    PlanSlot& sl = p->slots[k];
+    // output blocks: one allocation
+    size_t bytes = p->maxn * 8 + (d.L + 1) * 8 + HELIOS_MAX_HOPS * 8 + 256;
+    for (int h = 0; h < d.L; h++) bytes += ((lvl[h] + 1) * 4 + 255) / 256 * 256 + (edg[h] * 4 + 255) / 256 * 256;
+    HCUDA(cudaMalloc(&sl.mem, bytes));
+    char* q = (char*)sl.mem;
+    sl.blocks.nodes = (int64_t*)q;
+    sl.blocks.nodes_cap = std::max<int64_t>(p->maxn, 1);
+    q += (p->maxn * 8 + 255) / 256 * 256;
+    sl.blocks.level_counts = (int64_t*)q;
+    q += 128;
+    sl.blocks.edge_counts = (int64_t*)q;
+    q += 128;
+    for (int h = 0; h < d.L; h++) {
+      sl.blocks.block_indptr[h] = (int32_t*)q;
+      sl.blocks.indptr_cap[h] = lvl[h] + 1;
+      q += ((lvl[h] + 1) * 4 + 255) / 256 * 256;
+      sl.blocks.block_indices[h] = (int32_t*)q;
+      sl.blocks.edges_cap[h] = edg[h];
+      q += (edg[h] * 4 + 255) / 256 * 256;
+    }
+    HCUDA(cudaMemset(sl.blocks.level_counts, 0, 256));
+    HCUDA(cudaMalloc(&sl.d_seeds, std::max<int64_t>(d.max_seeds, 1) * 8));
+    HCUDA(cudaHostAlloc(&sl.h_seeds, std::max<int64_t>(d.max_seeds, 1) * 8, cudaHostAllocDefault));
+    if (p->c) {
+      HCUDA(cudaMalloc(&sl.feats, std::max<int64_t>(p->maxn, 1) * (int64_t)p->c->R));
+      HCUDA(cudaMalloc(&sl.stats, sizeof(helios_gather_stats)));
+      HCUDA(cudaMemset(sl.stats, 0, sizeof(helios_gather_stats)));
+      s = gws_ensure(p->c, sl.gws, sl.blocks.nodes_cap);
+      if (s != HELIOS_OK) return s;
+    }
+    s = ws_ensure(g, sl.ws, d.max_seeds, d.fanouts, d.L);
+    if (s != HELIOS_OK) return s;
+    HCUDA(cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking));
+    HCUDA(cudaEventCreateWithFlags(&sl.ev_caller, cudaEventDisableTiming));
+    HCUDA(cudaEventCreateWithFlags(&sl.ev_end, cudaEventDisableTiming));
+    sl.ring.assign(3 * PlanSlot::kRing, nullptr);
+    for (auto& e : sl.ring) HCUDA(cudaEventCreate(&e));
+    if (p->graphs) {
+      s = capture(sl.stream, &sl.g_sample, [&]() {
+        return sample_launch(g, sl.ws, sl.d_seeds, d.max_seeds, d.fanouts, d.L, &sl.blocks, sl.stream);
+      });
+      if (s != HELIOS_OK) return s;
+      if (p->c) {
+        s = capture(sl.stream, &sl.g_gather, [&]() {
+          return gather_launch(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + d.L, sl.blocks.nodes_cap,
+                               sl.feats, sl.stats, sl.stream);
+        });
+        if (s != HELIOS_OK) return s;
+      }
+    }
+  }
+  HCUDA(cudaDeviceSynchronize());
+  return HELIOS_OK;
+}
+
+helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seeds, int64_t n, uint64_t key, uint32_t flags,
+                               cudaStream_t caller) {
+  HCHECK(slot >= 0 && slot < (int32_t)p->slots.size(), HELIOS_E_INVALID, "slot %d of %zu", slot, p->slots.size());
+  HCHECK(n >= 0 && n <= p->d.max_seeds, HELIOS_E_CAPACITY, "n_seeds %lld > plan capacity %lld", (long long)n,
+         (long long)p->d.max_seeds);
+  HCHECK(n == 0 || seeds, HELIOS_E_INVALID, "null seeds");
+  PlanSlot& sl = p->slots[slot];
+  HCUDA(cudaEventRecord(sl.ev_caller, caller));
+  HCUDA(cudaStreamWaitEvent(sl.stream, sl.ev_caller, 0));
+  if (n > 0) {
+    if (flags & HELIOS_SUBMIT_SEEDS_HOST) {
+      HCUDA(cudaEventSynchronize(sl.ws.params_ev));  // previous H2D from h_seeds is done
+      memcpy(sl.h_seeds, seeds, n * 8);
+      HCUDA(cudaMemcpyAsync(sl.d_seeds, sl.h_seeds, n * 8, cudaMemcpyHostToDevice, sl.stream));
+    } else {
+      HCUDA(cudaMemcpyAsync(sl.d_seeds, seeds, n * 8, cudaMemcpyDeviceToDevice, sl.stream));
+    }
+  }
+  helios_status s = ws_upload_params(sl.ws, key, n, sl.stream);
+  if (s != HELIOS_OK) return s;
+  cudaEvent_t* ev = &sl.ring[3 * (sl.count % PlanSlot::kRing)];
+  HCUDA(cudaEventRecord(ev[0], sl.stream));
+  if (p->graphs) {
+    HCUDA(cudaGraphLaunch(sl.g_sample, sl.stream));
+  } else {
+    s = sample_launch(p->g, sl.ws, sl.d_seeds, p->d.max_seeds, p->d.fanouts, p->d.L, &sl.blocks, sl.stream);
+    if (s != HELIOS_OK) return s;
+  }
+  HCUDA(cudaEventRecord(ev[1], sl.stream));
+  if (p->c) {
+    if (p->graphs) {
+      HCUDA(cudaGraphLaunch(sl.g_gather, sl.stream));
+    } else {
+      s = gather_launch(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + p->d.L, sl.blocks.nodes_cap, sl.feats,
+                        sl.stats, sl.stream);
+      if (s != HELIOS_OK) return s;
+    }
+    s = io_launch(p->c, sl.gws, sl.feats, sl.stream);
+    if (s != HELIOS_OK) return s;
+  }
+  HCUDA(cudaEventRecord(ev[2], sl.stream));
+  HCUDA(cudaEventRecord(sl.ev_end, sl.stream));
+  sl.count++;
+  sl.submitted = true;
+  return HELIOS_OK;
+}
+
+helios_status plan_wait_impl(helios_plan* p, int32_t slot, cudaStream_t st) {
+  HCHECK(slot >= 0 && slot < (int32_t)p->slots.size(), HELIOS_E_INVALID, "slot %d of %zu", slot, p->slots.size());
+  PlanSlot& sl = p->slots[slot];
+  if (!sl.submitted) return HELIOS_OK;
+  HCUDA(cudaStreamWaitEvent(st, sl.ev_end, 0));
+  return HELIOS_OK;
+}
+
+helios_status plan_timing_impl(helios_plan* p, int32_t slot, int32_t back, float* sample_ms, float* gather_ms) {
+  HCHECK(slot >= 0 && slot < (int32_t)p->slots.size(), HELIOS_E_INVALID, "slot %d of %zu", slot, p->slots.size());
+  PlanSlot& sl = p->slots[slot];
+  HCHECK(back >= 0 && back < PlanSlot::kRing && back < sl.count, HELIOS_E_RANGE, "slot %d: batch -%d not recorded", slot,
+         back);
+  cudaEvent_t* ev = &sl.ring[3 * ((sl.count - 1 - back) % PlanSlot::kRing)];
+  HCUDA(cudaEventSynchronize(ev[2]));
+  float a = 0, b = 0;
+  HCUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+  HCUDA(cudaEventElapsedTime(&b, ev[1], ev[2]));
+  if (sample_ms) *sample_ms = a;
+  if (gather_ms) *gather_ms = b;
+  return HELIOS_OK;
+}
+
+helios_status plan_outputs_impl(helios_plan* p, int32_t slot, helios_blocks* blocks, void** features,
+                                helios_gather_stats** stats) {
+  HCHECK(slot >= 0 && slot < (int32_t)p->slots.size(), HELIOS_E_INVALID, "slot %d of %zu", slot, p->slots.size());
+  PlanSlot& sl = p->slots[slot];
+  if (blocks) *blocks = sl.blocks;
+  if (features) *features = sl.feats;
+  if (stats) *stats = sl.stats;
+  return HELIOS_OK;
+}
+
+}  // namespace helios

@@ -25,6 +25,8 @@ MAX_HOPS = 8
 MAX_RANKS = 64
 STATUS = ["OK", "E_INVALID", "E_RANGE", "E_CAPACITY", "E_NOMEM", "E_CUDA", "E_IO", "E_TIMEOUT", "E_STATE"]
 HOST_ALIAS, TABLE_MAPPED, NO_DIRECT_IO, IO_FAULT_AT = 0x1, 0x2, 0x4, 0x100
+PLAN_NO_GRAPH = 0x1
+SUBMIT_SEEDS_HOST = 0x1
 
 i64, i32, u32, u64, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p
 
@@ -40,6 +42,10 @@ class helios_cache_desc(ctypes.Structure):
                 ("hotness", vp), ("host_table", vp), ("feature_path", ctypes.c_char_p), ("header_bytes", i64),
                 ("file_stride", i64), ("io_rings", i32), ("ring_depth", i32), ("io_ctas", i32),
                 ("io_fault_at", i32), ("flags", u32)]
+
+
+class helios_plan_desc(ctypes.Structure):
+    _fields_ = [("max_seeds", i64), ("L", i32), ("fanouts", i32 * MAX_HOPS), ("depth", i32), ("flags", u32)]
 
 
 class helios_cache_info(ctypes.Structure):
@@ -67,6 +73,13 @@ _sig = {
     "helios_gather": (ctypes.c_int, [vp, vp, vp, i64, vp, vp, vp]),
     "helios_batch_prepare": (ctypes.c_int, [vp, vp, vp, i64, vp, i32, u64, ctypes.POINTER(helios_blocks), vp, vp, vp]),
     "helios_sync": (ctypes.c_int, [vp, vp]),
+    "helios_plan_create": (ctypes.c_int, [vp, vp, ctypes.POINTER(helios_plan_desc), ctypes.POINTER(vp)]),
+    "helios_plan_free": (None, [vp]),
+    "helios_plan_outputs": (ctypes.c_int, [vp, i32, ctypes.POINTER(helios_blocks), ctypes.POINTER(vp),
+                                           ctypes.POINTER(vp)]),
+    "helios_plan_submit": (ctypes.c_int, [vp, i32, vp, i64, u64, u32, vp]),
+    "helios_plan_wait": (ctypes.c_int, [vp, i32, vp]),
+    "helios_plan_timing": (ctypes.c_int, [vp, i32, i32, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
 }
 for _n, (_r, _a) in _sig.items():
     _f = getattr(_lib, _n)
@@ -307,3 +320,75 @@ def device_view(ptr: int, n: int, dtype=torch.int64) -> torch.Tensor:
     """Zero-copy torch view of a library-owned device array (e.g. helios_cache_info.dir)."""
     typestr = {torch.int64: "<i8", torch.int32: "<i4", torch.uint8: "|u1", torch.float32: "<f4"}[dtype]
     return torch.as_tensor(_CudaArray(ptr, n, typestr), device="cuda")
+
+
+# ---- execution plan ------------------------------------------------------------------------------
+
+class Plan:
+    """A helios_plan: `depth` in-flight batch slots, each replaying a CUDA graph of the whole batch.
+    Slot outputs are plan-owned device buffers exposed as zero-copy torch views."""
+
+    def __init__(self, handle: int, graph: Graph, cache: Cache | None, B: int, fanouts, depth: int):
+        self.handle, self.graph, self.cache, self.B, self.fanouts, self.depth = handle, graph, cache, B, list(fanouts), depth
+        L = len(self.fanouts)
+        self.outputs = []
+        for k in range(depth):
+            blk, fp, sp = helios_blocks(), vp(), vp()
+            _check(_lib.helios_plan_outputs(handle, k, ctypes.byref(blk), ctypes.byref(fp), ctypes.byref(sp)),
+                   "helios_plan_outputs")
+            b = Blocks(nodes=device_view(blk.nodes, blk.nodes_cap, torch.int64),
+                       level_counts=device_view(blk.level_counts, L + 1, torch.int64),
+                       edge_counts=device_view(blk.edge_counts, MAX_HOPS, torch.int64),
+                       block_indptr=[device_view(blk.block_indptr[h], blk.indptr_cap[h], torch.int32) for h in range(L)],
+                       block_indices=[device_view(blk.block_indices[h], max(1, blk.edges_cap[h]), torch.int32)
+                                      for h in range(L)],
+                       fanouts=self.fanouts)
+            feats = stats = None
+            if cache is not None:
+                R = cache.info().row_bytes
+                feats = device_view(fp.value, blk.nodes_cap * R, torch.uint8).view(blk.nodes_cap, R)
+                stats = device_view(sp.value, 4, torch.int64)
+            self.outputs.append((b, feats, stats))
+
+    def free(self):
+        if self.handle:
+            _lib.helios_plan_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def helios_plan_create(g: Graph, c: Cache | None, B: int, fanouts, depth: int = 2, flags: int = 0) -> Plan:
+    d = helios_plan_desc()
+    d.max_seeds, d.L, d.depth, d.flags = B, len(fanouts), depth, flags
+    for h, f in enumerate(fanouts):
+        d.fanouts[h] = f
+    h = vp()
+    _check(_lib.helios_plan_create(g.handle, c.handle if c is not None else None, ctypes.byref(d), ctypes.byref(h)),
+           "helios_plan_create")
+    return Plan(h.value, g, c, B, fanouts, depth)
+
+
+def helios_plan_submit(p: Plan, slot: int, seeds, key: int, stream=None) -> None:
+    if isinstance(seeds, torch.Tensor) and seeds.is_cuda:
+        ptr, n, fl = seeds.data_ptr(), seeds.numel(), 0
+    else:
+        arr = np.ascontiguousarray(seeds, dtype=np.int64) if not isinstance(seeds, torch.Tensor) else seeds
+        ptr, n, fl = _ptr(arr), len(arr), SUBMIT_SEEDS_HOST
+    _check(_lib.helios_plan_submit(p.handle, slot, ptr, n, key & (2**64 - 1), fl, _stream(stream)),
+           "helios_plan_submit")
+
+
+def helios_plan_wait(p: Plan, slot: int, stream=None) -> None:
+    _check(_lib.helios_plan_wait(p.handle, slot, _stream(stream)), "helios_plan_wait")
+
+
+def helios_plan_timing(p: Plan, slot: int, back: int = 0) -> tuple[float, float]:
+    """(sample_ms, gather_ms) of slot's batch `back` submissions ago (0 = last)."""
+    a, b = ctypes.c_float(), ctypes.c_float()
+    _check(_lib.helios_plan_timing(p.handle, slot, back, ctypes.byref(a), ctypes.byref(b)), "helios_plan_timing")
+    return a.value, b.value

@@ -45,8 +45,8 @@ def lib():
         L.synth_perm_inv.restype = u64
         L.synth_perm_inv.argtypes = [ctypes.c_int, u64, u64]
         L.synth_graph_degrees.restype = i64
-        L.synth_graph_degrees.argtypes = [i64, i64, u64, vp]
-        L.synth_graph_fill.argtypes = [i64, u64, vp, vp, vp]
+        L.synth_graph_degrees.argtypes = [i64, i64, u64, ctypes.c_double, vp]
+        L.synth_graph_fill.argtypes = [i64, u64, ctypes.c_double, vp, vp, vp]
         L.synth_graph_compact.argtypes = [i64, vp, vp, vp, vp]
         L.synth_features.argtypes = [i64, i64, i32, vp]
         L.synth_features_at.argtypes = [vp, i64, i32, vp]
@@ -95,12 +95,12 @@ class Graph:
                 "max_in_deg": int(indeg.max()), "top1pct_in_share": round(share, 4)}
 
 
-def graph(V: int, E_target: int, seed: int = HELIOS_SEED) -> Graph:
+def graph(V: int, E_target: int, seed: int = HELIOS_SEED, p1: float = 0.24) -> Graph:
     """Power-law CSR: out-degrees and destinations follow the R-MAT (.57,.19,.19,.05) marginals
     over a seeded vertex permutation; self-loops and duplicate (src,dst) pairs removed."""
     L = lib()
     deg = np.empty(V, dtype=np.int64)
-    tot = L.synth_graph_degrees(V, E_target, seed, _p(deg))
+    tot = L.synth_graph_degrees(V, E_target, seed, p1, _p(deg))
     if tot < 0:
         raise ValueError("bad graph parameters")
     prov_indptr = np.zeros(V + 1, dtype=np.int64)
@@ -108,7 +108,7 @@ def graph(V: int, E_target: int, seed: int = HELIOS_SEED) -> Graph:
     del deg
     prov = np.empty(max(1, tot), dtype=np.int32)
     flen = np.empty(V, dtype=np.int64)
-    L.synth_graph_fill(V, seed, _p(prov_indptr), _p(prov), _p(flen))
+    L.synth_graph_fill(V, seed, p1, _p(prov_indptr), _p(prov), _p(flen))
     indptr = np.zeros(V + 1, dtype=np.int64)
     np.cumsum(flen, out=indptr[1:])
     del flen

@@ -70,8 +70,9 @@ void parallel_for_dyn(int64_t n, int64_t grain, const std::function<void(int64_t
 
 // ---- R-MAT-marginal (Kronecker) vertex labelling -------------------------------------------
 // Vertex v in [0,V) sits at Kronecker position x = perm(v) in [0, 2^scale); its weight is the
-// Graph500 R-MAT marginal  w(x) = p1^popcount(x) * p0^(scale - popcount(x)),  p0 = a+b = .76,
-// p1 = c+d = .24 (a,b,c,d = .57,.19,.19,.05; b = c so row and column marginals coincide).
+// R-MAT marginal  w(x) = p1^popcount(x) * (1-p1)^(scale - popcount(x))  (Graph500's
+// a,b,c,d = .57,.19,.19,.05 gives p1 = c+d = .24; larger p1 = less skew).  Row (out-degree) and
+// column (destination) marginals coincide (b = c).
 // perm is a bijection of [0, 2^scale) (xor-shift / odd-multiply rounds) that scatters hubs.
 struct Perm {
   int scale;
@@ -114,7 +115,6 @@ struct Perm {
   }
 };
 
-constexpr uint32_t kP1Q16 = 15729;  // round(0.24 * 65536): P(bit = 1) per Kronecker level
 
 inline int scale_of(int64_t V) {
   int s = 1;
@@ -136,7 +136,7 @@ uint64_t synth_perm_inv(int scale, uint64_t seed, uint64_t y) { return Perm(scal
 
 // Phase 1: target out-degree of every vertex, deg[v] = floor(E * w(perm v) / W + U_v).
 // Returns sum of target degrees (the provisional edge count before row dedup).
-int64_t synth_graph_degrees(int64_t V, int64_t E_target, uint64_t seed, int64_t* deg) {
+int64_t synth_graph_degrees(int64_t V, int64_t E_target, uint64_t seed, double p1, int64_t* deg) {
   if (V < 2 || E_target < 0) return -1;
   int scale = scale_of(V);
   Perm P(scale, seed);
@@ -149,7 +149,7 @@ int64_t synth_graph_degrees(int64_t V, int64_t E_target, uint64_t seed, int64_t*
     for (int64_t v = lo; v < hi; v++) h[__builtin_popcountll(P.fwd((uint64_t)v))]++;
   });
   std::vector<double> wpop(65);
-  for (int k = 0; k <= scale; k++) wpop[k] = std::pow(0.24, k) * std::pow(0.76, scale - k);
+  for (int k = 0; k <= scale; k++) wpop[k] = std::pow(p1, k) * std::pow(1.0 - p1, scale - k);
   double W = 0;
   for (auto& h : hist)
     for (int k = 0; k <= scale; k++) W += (double)h[k] * wpop[k];
@@ -172,8 +172,9 @@ int64_t synth_graph_degrees(int64_t V, int64_t E_target, uint64_t seed, int64_t*
 // duplicates and self-loops.  prov_indptr = exclusive scan of deg (V+1 entries, caller-computed);
 // prov (int32[prov_indptr[V]]) is scratch; final_len[v] receives the deduplicated row length and
 // rows are left sorted at the front of their provisional slice.
-int synth_graph_fill(int64_t V, uint64_t seed, const int64_t* prov_indptr, int32_t* prov, int64_t* final_len) {
+int synth_graph_fill(int64_t V, uint64_t seed, double p1, const int64_t* prov_indptr, int32_t* prov, int64_t* final_len) {
   int scale = scale_of(V);
+  const uint32_t p1q16 = (uint32_t)std::lround(p1 * 65536.0);  // P(bit = 1) per Kronecker level
   Perm P(scale, seed);
   parallel_for_dyn(V, 256, [&](int64_t lo, int64_t hi) {
     for (int64_t v = lo; v < hi; v++) {
@@ -185,7 +186,7 @@ int synth_graph_fill(int64_t V, uint64_t seed, const int64_t* prov_indptr, int32
           for (int l = 0; l < scale; l += 4) {
             uint64_t r = urand(seed ^ ((uint64_t)v << 1), 0x445354ull, ctr++);
             for (int q = 0; q < 4 && l + q < scale; q++)
-              if ((uint32_t)((r >> (16 * q)) & 0xFFFF) < kP1Q16) x |= 1ull << (l + q);
+              if ((uint32_t)((r >> (16 * q)) & 0xFFFF) < p1q16) x |= 1ull << (l + q);
           }
           uint64_t u = P.inv(x);
           if ((int64_t)u < V) { prov[b + j] = (int32_t)u; break; }

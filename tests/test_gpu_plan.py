@@ -1,0 +1,99 @@
+"""GPU parity of the execution plan (helios_plan_*): CUDA-graph replay and direct launches, 1-3
+in-flight slots, device and host seeds, all three tiers (C1 incl. the IO rings) and the HBM+host
+config shape (medium graph) — every batch bit-exact against the oracle."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+import workloads  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_2310_00837_b200 import helios
+    return helios
+
+
+@pytest.fixture(scope="module")
+def c1(tmp_path_factory):
+    return workloads.make_inputs(workloads.CONFIGS["C1"], table=True, file=True,
+                                 workdir=str(tmp_path_factory.mktemp("c1p")))
+
+
+def build(H, inp, Hr, S, flags=0):
+    cfg = inp.cfg
+    g = H.helios_graph_load(inp.graph.indptr, inp.graph.indices)
+    hot = torch.zeros(cfg.V, dtype=torch.int64, device="cuda")
+    pk = workloads.presample_keys(len(inp.batches))
+    H.helios_presample(g, torch.as_tensor(np.concatenate(inp.batches)).cuda(), cfg.B, cfg.fanouts, pk, hot)
+    c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=inp.table, feature_path=inp.feature_path,
+                             header_bytes=inp.header, file_stride=inp.stride, flags=flags)
+    return g, hot, c
+
+
+def check_slot(p, slot, inp, seeds, key, dref):
+    cfg = inp.cfg
+    blocks, feats, stats = p.outputs[slot]
+    got = blocks.to_host()
+    orc = oracle.sample(inp.graph.indptr, inp.graph.indices, seeds, cfg.fanouts, key)
+    assert np.array_equal(got["nodes"], orc.nodes)
+    for h in range(len(cfg.fanouts)):
+        assert np.array_equal(got["block_indptr"][h], orc.block_indptr[h])
+        assert np.array_equal(got["block_indices"][h], orc.block_indices[h])
+    if feats is not None:
+        n = len(orc.nodes)
+        assert np.array_equal(feats[:n].cpu().numpy(), oracle.gather(orc.nodes, cfg.R, table=inp.table))
+        assert stats.cpu().tolist() == oracle.lookup_counts(dref, orc.nodes).tolist()
+
+
+@pytest.mark.parametrize("depth,flags,host_seeds", [(2, 0, False), (1, 0, True), (3, 0, False), (2, 1, True)])
+def test_plan_c1_epoch(H, c1, depth, flags, host_seeds):
+    cfg = c1.cfg
+    Hr, S = workloads.tier_rows(cfg)
+    g, hot, c = build(H, c1, Hr, S, flags=H.HOST_ALIAS)
+    dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S, host_slot_is_id=True)
+    p = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=depth, flags=flags)
+    keys = workloads.batch_keys(0, len(c1.batches))
+    stream = torch.cuda.current_stream()
+    nb = len(c1.batches)
+    for start in range(0, nb, depth):
+        idx = list(range(start, min(nb, start + depth)))
+        for k, b in enumerate(idx):
+            seeds = c1.batches[b] if host_seeds else torch.as_tensor(c1.batches[b]).cuda()
+            H.helios_plan_submit(p, k, seeds, keys[b], stream)
+        for k, b in enumerate(idx):
+            H.helios_plan_wait(p, k, stream)
+        H.helios_sync(c)
+        for k, b in enumerate(idx):
+            check_slot(p, k, c1, c1.batches[b], keys[b], dref)
+        s_ms, g_ms = H.helios_plan_timing(p, 0)
+        assert s_ms > 0 and g_ms > 0
+    p.free()
+    c.free()
+
+
+def test_plan_sample_only_medium(H):
+    gr = synth.graph(400_000, 8_000_000, seed=33)
+    g = H.helios_graph_load(gr.indptr, gr.indices)
+    fan = [15, 10, 5]
+    p = H.helios_plan_create(g, None, 1024, fan, depth=2)
+    rng = np.random.default_rng(4)
+    inp = workloads.Inputs(workloads.Config("m", gr.V, gr.E, 1, 1024, fan, 0, 0), gr, None, None, 0, 0, None, [])
+    for it in range(3):
+        seeds = [rng.choice(gr.V, 1024 - 100 * k, replace=False) for k in range(2)]
+        keys = [it * 7 + 1, it * 7 + 2]
+        for k in range(2):
+            H.helios_plan_submit(p, k, torch.as_tensor(seeds[k]).cuda(), keys[k])
+        torch.cuda.synchronize()
+        for k in range(2):
+            H.helios_plan_wait(p, k)
+            H.helios_graph_sync(g)
+            check_slot(p, k, inp, seeds[k], keys[k], None)
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_plan_submit(p, 0, torch.arange(2000, device="cuda"), 1)
+    assert e.value.name == "E_CAPACITY"
+    p.free()
