@@ -180,6 +180,7 @@ def main():
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no baseline, no parity")
     ap.add_argument("--depth", type=int, default=2, help="batches in flight (plan slots)")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly instead of CUDA graphs")
+    ap.add_argument("--host-alias", action="store_true", help="host tier = canonical table by id (no packed copy)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -241,8 +242,21 @@ def main():
     if cfg.hbm_frac + cfg.host_frac >= 1.0:
         S = max(0, cfg.V - world * Hr)
     t2 = time.time()
-    c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
-                             flags=H.HOST_ALIAS)
+    if args.host_alias or S == 0:
+        c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
+                                 flags=H.HOST_ALIAS)
+    elif world == 1:   # packed host tier in hot-rank order, pinned by the library
+        c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table)
+    else:              # one packed host tier shared by all ranks (/dev/shm), filled by rank 0
+        tier_buf = host_buffer(S * cfg.R, f"{shm}_tier", create=(rank == 0))
+        tier = np.frombuffer(tier_buf, dtype=np.uint8)
+        if rank == 0:
+            c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
+                                     host_tier=tier, flags=H.HOST_FILL)
+        dist.barrier()
+        if rank != 0:
+            c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
+                                     host_tier=tier)
     if world > 1:
         blob = H.helios_cache_export(c)
         blobs = [None] * world
@@ -395,7 +409,7 @@ def main():
                    key=lambda x: x[1])[0]
     value = world * steps / (max_ms / 1e3)
     e2e_val = world * steps / e2e_s
-    launches_per_step = 2 + 3 * L + 1 + (3 if c.info().file_rows > 0 else 0)
+    launches_per_step = 2 + 3 * L + 2 + (3 if c.info().file_rows > 0 else 0)
     out = {
         "metric": "sampled+gathered mini-batches/sec (feature GB/s and tier-roofline fraction alongside)",
         "value": round(value, 3), "unit": "batches/s", "n_gpus": world, "steps": steps, "warmup": args.warmup,
@@ -405,6 +419,8 @@ def main():
         "config": {"workload": cfg.name, "desc": cfg.note, "V": cfg.V, "E": int(inp.graph.E), "dim": cfg.dim,
                    "batch_per_rank": cfg.B, "fanouts": cfg.fanouts, "hbm_rows_per_gpu": Hr, "host_rows": S,
                    "scale": s, "parallelism": f"dp{world} (seeds split per rank, HBM tier sharded)",
+                   "host_tier": "alias of canonical table (by id)" if args.host_alias else "packed, hot-rank order",
+                   "batches_in_flight": depth, "cuda_graphs": not args.no_graph,
                    "l2": "inputs larger than L2 (CSR %.1f GB, feature table %.1f GB); no flush" % (
                        (inp.graph.E * 4 + cfg.V * 8) / 1e9, cfg.V * R / 1e9)},
         "feature_gbs": round(world * n_rows / steps * R * steps / (max_ms / 1e3) / 1e9, 2),
@@ -412,7 +428,7 @@ def main():
                      "note": f"per batch, device events around the two graph segments, {depth} batches in flight"},
         "rows_per_batch": {"n_L": round(nL, 1), "hbm_local": round(n_local, 1), "hbm_peer": round(n_peer, 1),
                            "host": round(n_host, 1), "file": round(n_file, 1)},
-        "roofline": {"bound": dominant, "kernel": "k_lookup_gather (K3+K4)", "achieved": round(achieved, 2),
+        "roofline": {"bound": dominant, "kernel": "k_lookup + k_gather_lists (K3+K4)", "achieved": round(achieved, 2),
                      "peak": round(peak_eff, 2), "unit": "GB/s", "frac": round(t_roof_ms / g_ms, 4),
                      "traffic": None,
                      "peaks_used": {"hbm_gbs": bw_hbm, "hbm_src": "MEASURED_PEAKS.json" if pk else "fallback",
@@ -436,7 +452,7 @@ def main():
     if world > 1:
         dist.barrier()
         if rank == 0:
-            for suf in ("_feat", "_indptr.npy", "_indices.npy"):
+            for suf in ("_feat", "_tier", "_indptr.npy", "_indices.npy"):
                 try:
                     os.unlink(f"/dev/shm/{shm}{suf}")
                 except OSError:

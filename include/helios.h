@@ -144,6 +144,8 @@ helios_status helios_presample(helios_graph* g, const int64_t* seeds, int64_t n_
 #define HELIOS_CACHE_HOST_ALIAS 0x1u     /* host tier IS host_table (slot = v); no second copy   */
 #define HELIOS_CACHE_TABLE_MAPPED 0x2u   /* host_table is already cudaHostRegister'ed + mapped   */
 #define HELIOS_CACHE_NO_DIRECT_IO 0x4u   /* open feature_path without O_DIRECT                    */
+#define HELIOS_CACHE_HOST_FILL 0x8u      /* fill the caller-provided host_tier (else assumed filled) */
+#define HELIOS_CACHE_HOST_TIER_MAPPED 0x10u /* caller-provided host_tier already registered + mapped */
 #define HELIOS_CACHE_IO_FAULT_AT 0x100u  /* test builds: IO workers fail the io_fault_at-th read  */
 
 typedef struct {
@@ -163,6 +165,10 @@ typedef struct {
   int32_t io_ctas;            /* CTA budget of each IO kernel (submit / complete); paper: 32 */
   int32_t io_fault_at;        /* with HELIOS_CACHE_IO_FAULT_AT: 1-based read index that fails   */
   uint32_t flags;
+  void* host_tier;            /* optional caller-provided packed host tier (S*R bytes, e.g. a shared-memory
+                                 mapping used by every rank): row s = vertex at hot rank G*H + s.  Filled by
+                                 the library iff HELIOS_CACHE_HOST_FILL; registered unless HOST_TIER_MAPPED.
+                                 NULL: the library allocates (pinned) and fills it.  Ignored with HOST_ALIAS. */
 } helios_cache_desc;
 
 /* Builds the directory and fills the tiers (blocking).  The HBM tier is filled from host_table

@@ -306,25 +306,45 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
       c->host_tier = (char*)c->host_table;
       c->d_host_tier = table_dev;
     } else {
-      HCUDA(cudaHostAlloc(&c->host_tier, c->S * (int64_t)c->R, cudaHostAllocMapped));
-      c->host_owned = true;
-      HCUDA(cudaHostGetDevicePointer((void**)&c->d_host_tier, c->host_tier, 0));
-      std::vector<int32_t> h_ids(c->S);
-      HCUDA(cudaMemcpy(h_ids.data(), d_order + GH, c->S * 4, cudaMemcpyDeviceToHost));
-      if (c->host_table) {
-        const int T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-        std::vector<std::thread> th;
-        for (int t = 0; t < T; t++)
-          th.emplace_back([&, t]() {
-            for (int64_t s = t; s < c->S; s += T)
-              memcpy(c->host_tier + s * c->R, (const char*)c->host_table + (int64_t)h_ids[s] * c->R, c->R);
-          });
-        for (auto& x : th) x.join();
+      const size_t tier_bytes = (size_t)c->S * c->R;
+      if (d->host_tier) {
+        c->host_tier = (char*)d->host_tier;
+        if (!(c->flags & HELIOS_CACHE_HOST_TIER_MAPPED)) {
+          cudaError_t e = cudaHostRegister(c->host_tier, tier_bytes, cudaHostRegisterMapped);
+          if (e == cudaErrorHostMemoryAlreadyRegistered) cudaGetLastError();
+          else if (e != cudaSuccess) {
+            cudaFree(d_order);
+            return fail(HELIOS_E_CUDA, "cudaHostRegister(host_tier, %zu B): %s", tier_bytes, cudaGetErrorString(e));
+          } else {
+            c->host_tier_registered = true;
+          }
+        }
       } else {
-        st = fill_tier_from_file(c, h_ids.data(), c->S, c->host_tier, false);
-        if (st != HELIOS_OK) {
-          cudaFree(d_order);
-          return st;
+        HCUDA(cudaHostAlloc(&c->host_tier, tier_bytes, cudaHostAllocMapped));
+        c->host_owned = true;
+      }
+      HCUDA(cudaHostGetDevicePointer((void**)&c->d_host_tier, c->host_tier, 0));
+      if (!d->host_tier || (c->flags & HELIOS_CACHE_HOST_FILL)) {
+        // packed in hot-rank order: slot s holds the vertex at hot rank G*H + s (reading 9), so the
+        // warmest host rows share pages (translation locality of zero-copy reads)
+        std::vector<int32_t> h_ids(c->S);
+        HCUDA(cudaMemcpy(h_ids.data(), d_order + GH, c->S * 4, cudaMemcpyDeviceToHost));
+        if (c->host_table) {
+          const int T = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+          std::vector<std::thread> th;
+          for (int t = 0; t < T; t++)
+            th.emplace_back([&, t]() {
+              const int64_t lo = c->S * t / T, hi = c->S * (t + 1) / T;
+              for (int64_t s = lo; s < hi; s++)
+                memcpy(c->host_tier + s * c->R, (const char*)c->host_table + (int64_t)h_ids[s] * c->R, c->R);
+            });
+          for (auto& x : th) x.join();
+        } else {
+          st = fill_tier_from_file(c, h_ids.data(), c->S, c->host_tier, false);
+          if (st != HELIOS_OK) {
+            cudaFree(d_order);
+            return st;
+          }
         }
       }
     }
@@ -360,6 +380,7 @@ void cache_free_impl(helios_cache* c) {
     if (r != c->rank && c->peer_ptrs[r]) cudaIpcCloseMemHandle(c->peer_ptrs[r]);
   if (c->host_registered) cudaHostUnregister((void*)c->host_table);
   if (c->host_owned && c->host_tier) cudaFreeHost(c->host_tier);
+  if (c->host_tier_registered) cudaHostUnregister(c->host_tier);
   if (c->hbm) cudaFree(c->hbm);
   if (c->dir) cudaFree(c->dir);
   if (c->d_peers) cudaFree(c->d_peers);

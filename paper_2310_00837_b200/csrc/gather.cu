@@ -17,22 +17,6 @@
 
 namespace helios {
 
-struct GatherArgs {
-  const int64_t* nodes;
-  const int64_t* n_nodes;
-  const int64_t* dir;
-  char* out;
-  int32_t R;
-  int32_t rank;
-  const char* hbm;          // this rank's shard
-  char* const* peers;       // device [G]
-  const char* host_dev;     // device alias of the host tier
-  int64_t* miss_out;
-  int64_t* miss_row;
-  unsigned long long* miss_count;
-  helios_gather_stats* stats;
-};
-
 __device__ __forceinline__ int4 ld_stream(const int4* p) {
   int4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
@@ -41,86 +25,121 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
   return r;
 }
 
-template <int VPL, int U>
-__global__ void __launch_bounds__(256) k_lookup_gather(GatherArgs a) {
+// K3: one thread per row of N_L: dir[v] -> tier list (local HBM / peer HBM / host / file), appended
+// with warp-aggregated atomics.  The list counts are the per-tier row counts.
+__global__ void __launch_bounds__(256) k_lookup(const int64_t* __restrict__ nodes, const int64_t* __restrict__ n_nodes,
+                                                const int64_t* __restrict__ dir, int32_t rank, int64_t* __restrict__ li,
+                                                uint64_t* __restrict__ lw, int64_t cap, unsigned long long* ctl) {
   const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t n = *a.n_nodes;
+  const int64_t n = *n_nodes;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < n; base += stride) {
+    const int64_t i = base + lane;
+    int t = -1;
+    uint64_t w = 0;
+    if (i < n) {
+      w = (uint64_t)dir[nodes[i]];
+      const uint32_t tier = (uint32_t)(w >> 62);
+      t = tier == 0 ? ((int)((w >> 56) & 63) == rank ? kListLocal : kListPeer) : (tier == 1 ? kListHost : kListFile);
+    }
+#pragma unroll
+    for (int q = 0; q < kLists; q++) {
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, t == q);
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        unsigned long long b = 0;
+        if (lane == leader) b = atomicAdd(&ctl[q], (unsigned long long)__popc(m));
+        b = __shfl_sync(0xFFFFFFFFu, b, leader);
+        if (t == q) {
+          const int64_t pos = (int64_t)b + __popc(m & ((1u << lane) - 1u));
+          li[q * cap + pos] = i;
+          lw[q * cap + pos] = w;
+        }
+      }
+    }
+  }
+}
+
+struct GatherArgs {
+  char* out;
+  int32_t R;
+  const int64_t* li;
+  const uint64_t* lw;
+  int64_t cap;
+  const unsigned long long* ctl;
+  const char* hbm;          // this rank's shard
+  char* const* peers;       // device [G]
+  const char* host_dev;     // device alias of the host tier
+  helios_gather_stats* stats;
+};
+
+// Copies rows [j0, j0+U) of list q (warp-cooperative, VPL 16 B vectors per lane per row, all loads
+// issued before the stores).
+template <int VPL, int U>
+__device__ __forceinline__ void copy_rows(const GatherArgs& a, int q, int64_t j0, int64_t cnt, int lane, int nvec) {
+  for (int c0 = 0; c0 < nvec; c0 += 32 * VPL) {
+    int4 r[U][VPL];
+    const int4* src[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      src[u] = nullptr;
+      if (j0 + u < cnt) {
+        const uint64_t w = a.lw[q * a.cap + j0 + u];
+        const int64_t slot = (int64_t)(w & ((1ull << 56) - 1));
+        const char* base = q == kListLocal ? a.hbm : (q == kListPeer ? a.peers[(w >> 56) & 63] : a.host_dev);
+        src[u] = (const int4*)(base + slot * a.R);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (src[u]) {
+#pragma unroll
+        for (int k = 0; k < VPL; k++) {
+          const int idx = c0 + lane + 32 * k;
+          if (idx < nvec) r[u][k] = ld_stream(src[u] + idx);
+        }
+      }
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (src[u]) {
+        int4* d = (int4*)(a.out + a.li[q * a.cap + j0 + u] * (int64_t)a.R);
+#pragma unroll
+        for (int k = 0; k < VPL; k++) {
+          const int idx = c0 + lane + 32 * k;
+          if (idx < nvec) d[idx] = r[u][k];
+        }
+      }
+  }
+}
+
+// K4: warp-specialised gather.  When the host list is non-empty, one warp in 8 serves host rows
+// (zero-copy over PCIe, UH rows in flight per warp, so every host read is outstanding at once
+// and the link streams) while the others copy peer (NVLink) then local HBM rows.
+template <int VPL, int U, int UH>
+__global__ void __launch_bounds__(256, 4) k_gather_lists(GatherArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int nvec = a.R >> 4;
-  long long c_local = 0, c_peer = 0, c_host = 0, c_file = 0;
-  for (int64_t base = warp * U; base < n; base += nwarps * U) {
-    // lane u < U resolves row base+u
-    const char* src = nullptr;
-    int tier = -1;
-    if (lane < U && base + lane < n) {
-      const int64_t i = base + lane;
-      const int64_t v = a.nodes[i];
-      const uint64_t w = (uint64_t)a.dir[v];
-      tier = (int)(w >> 62);
-      const int owner = (int)((w >> 56) & 63);
-      const int64_t slot = (int64_t)(w & ((1ull << 56) - 1));
-      if (tier == 0) {
-        if (owner == a.rank) {
-          src = a.hbm + slot * a.R;
-          c_local++;
-        } else {
-          src = a.peers[owner] + slot * a.R;
-          c_peer++;
-        }
-      } else if (tier == 1) {
-        src = a.host_dev + slot * a.R;
-        c_host++;
-      } else {
-        c_file++;
-        const unsigned long long m = atomicAdd(a.miss_count, 1ull);
-        a.miss_out[m] = i;
-        a.miss_row[m] = slot;
-      }
-    }
-    for (int c0 = 0; c0 < nvec; c0 += 32 * VPL) {
-      int4 r[U][VPL];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int4* s = (const int4*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)src, u);
-        const int t = __shfl_sync(0xFFFFFFFFu, tier, u);
-        if (t == 0 || t == 1) {
-#pragma unroll
-          for (int k = 0; k < VPL; k++) {
-            const int idx = c0 + lane + 32 * k;
-            if (idx < nvec) r[u][k] = ld_stream(s + idx);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int t = __shfl_sync(0xFFFFFFFFu, tier, u);
-        if (t == 0 || t == 1) {
-          int4* d = (int4*)(a.out + (base + u) * (int64_t)a.R);
-#pragma unroll
-          for (int k = 0; k < VPL; k++) {
-            const int idx = c0 + lane + 32 * k;
-            if (idx < nvec) d[idx] = r[u][k];
-          }
-        }
-      }
-    }
+  const int64_t n_local = (int64_t)a.ctl[kListLocal], n_peer = (int64_t)a.ctl[kListPeer],
+                n_host = (int64_t)a.ctl[kListHost];
+  if (a.stats && gw == 0 && lane == 0) {
+    a.stats->rows_hbm_local = n_local;
+    a.stats->rows_hbm_peer = n_peer;
+    a.stats->rows_host = n_host;
+    a.stats->rows_file = (int64_t)a.ctl[kListFile];
   }
-  if (a.stats) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      c_local += __shfl_xor_sync(0xFFFFFFFFu, c_local, o);
-      c_peer += __shfl_xor_sync(0xFFFFFFFFu, c_peer, o);
-      c_host += __shfl_xor_sync(0xFFFFFFFFu, c_host, o);
-      c_file += __shfl_xor_sync(0xFFFFFFFFu, c_file, o);
-    }
-    if (lane == 0) {
-      if (c_local) atomicAdd((unsigned long long*)&a.stats->rows_hbm_local, (unsigned long long)c_local);
-      if (c_peer) atomicAdd((unsigned long long*)&a.stats->rows_hbm_peer, (unsigned long long)c_peer);
-      if (c_host) atomicAdd((unsigned long long*)&a.stats->rows_host, (unsigned long long)c_host);
-      if (c_file) atomicAdd((unsigned long long*)&a.stats->rows_file, (unsigned long long)c_file);
-    }
+  const bool split = n_host > 0;
+  const int64_t n_hw = split ? (nw + 7) / 8 : 0;
+  if (split && (gw & 7) == 0) {
+    const int64_t hw = gw >> 3;
+    for (int64_t j0 = hw * UH; j0 < n_host; j0 += n_hw * UH) copy_rows<VPL, UH>(a, kListHost, j0, n_host, lane, nvec);
+    return;
   }
+  const int64_t dw = split ? gw - (gw >> 3) - 1 : gw;  // index among data warps
+  const int64_t n_dw = nw - n_hw;
+  for (int64_t j0 = dw * U; j0 < n_peer; j0 += n_dw * U) copy_rows<VPL, U>(a, kListPeer, j0, n_peer, lane, nvec);
+  for (int64_t j0 = dw * U; j0 < n_local; j0 += n_dw * U) copy_rows<VPL, U>(a, kListLocal, j0, n_local, lane, nvec);
 }
 
 // Plain row copy by id (setup: HBM-tier fill from a mapped host table).
@@ -180,9 +199,9 @@ __device__ __forceinline__ int4 ld_volatile_v4(const int4* p) {
 constexpr uint64_t kWatchdogNs = 30ull * 1000000000ull;
 
 struct IoArgs {
-  const int64_t* miss_out;
-  const int64_t* miss_row;
-  unsigned long long* ctl;   // [0] misses, [1] submit ticket, [2] complete ticket
+  const int64_t* miss_out;   // file list: output rows
+  const uint64_t* miss_w;    // file list: directory words (slot bits = file row)
+  unsigned long long* ctl;   // [kListFile] misses, [kCtlSubmit] / [kCtlComplete] tickets
   SqEntry* sq;               // device alias of pinned SQ
   CqEntry* cq;               // device alias of pinned CQ
   const char* staging;       // device alias of pinned staging
@@ -197,11 +216,11 @@ struct IoArgs {
 
 __global__ void __launch_bounds__(256) k_io_submit(IoArgs a) {
   const int lane = threadIdx.x & 31;
-  const unsigned long long M = a.ctl[0];
+  const unsigned long long M = a.ctl[kListFile];
   const uint64_t t0 = globaltimer();
   for (;;) {
     unsigned long long tk = 0;
-    if (lane == 0) tk = atomicAdd(&a.ctl[1], 32ull);
+    if (lane == 0) tk = atomicAdd(&a.ctl[kCtlSubmit], 32ull);
     tk = __shfl_sync(0xFFFFFFFFu, tk, 0);
     if (tk >= M) break;
     const unsigned long long m = tk + lane;
@@ -223,7 +242,7 @@ __global__ void __launch_bounds__(256) k_io_submit(IoArgs a) {
       }
       if (ok) {
         SqEntry* e = a.sq + idx;
-        e->file_off = (uint64_t)(a.header + a.miss_row[m] * a.stride);
+        e->file_off = (uint64_t)(a.header + (int64_t)(a.miss_w[m] & ((1ull << 56) - 1)) * a.stride);
         e->len = (uint32_t)a.len;
         e->slot = (uint32_t)idx;
         e->out_row = (uint64_t)a.miss_out[m];
@@ -236,12 +255,12 @@ __global__ void __launch_bounds__(256) k_io_submit(IoArgs a) {
 
 __global__ void __launch_bounds__(256) k_io_complete(IoArgs a) {
   const int lane = threadIdx.x & 31;
-  const unsigned long long M = a.ctl[0];
+  const unsigned long long M = a.ctl[kListFile];
   const int nvec = a.R >> 4;
   const uint64_t t0 = globaltimer();
   for (;;) {
     unsigned long long m = 0;
-    if (lane == 0) m = atomicAdd(&a.ctl[2], 1ull);
+    if (lane == 0) m = atomicAdd(&a.ctl[kCtlComplete], 1ull);
     m = __shfl_sync(0xFFFFFFFFu, m, 0);
     if (m >= M) break;
     const int r = (int)(m % a.rings);
@@ -279,7 +298,7 @@ __global__ void __launch_bounds__(256) k_io_complete(IoArgs a) {
 }
 
 __global__ void k_io_finish(unsigned long long* ctl, uint32_t* base_seq, int rings) {
-  const unsigned long long M = ctl[0];
+  const unsigned long long M = ctl[kListFile];
   for (int r = threadIdx.x; r < rings; r += blockDim.x)
     base_seq[r] += (uint32_t)(M / rings + ((unsigned long long)r < M % rings ? 1 : 0));
 }
@@ -294,27 +313,35 @@ helios_status io_preload_kernels() {
   return HELIOS_OK;
 }
 
-template <int VPL, int U>
+// Persistent grid: exactly the resident CTAs, so every host-row warp is live from the start.
+template <int VPL, int U, int UH>
 static void launch_gather(const GatherArgs& a, int sms, cudaStream_t st) {
-  k_lookup_gather<VPL, U><<<sms * 8, 256, 0, st>>>(a);
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_lists<VPL, U, UH>, 256, 0);
+    per_sm = std::max(per_sm, 1);
+  }
+  k_gather_lists<VPL, U, UH><<<sms * per_sm, 256, 0, st>>>(a);
 }
 
 void gws_free(GatherWS& w) {
-  if (w.d_miss_out) cudaFree(w.d_miss_out);
-  if (w.d_miss_row) cudaFree(w.d_miss_row);
+  if (w.d_list_i) cudaFree(w.d_list_i);
+  if (w.d_list_w) cudaFree(w.d_list_w);
   if (w.d_ctl) cudaFree(w.d_ctl);
   w = GatherWS{};
 }
 
 helios_status gws_ensure(helios_cache* c, GatherWS& w, int64_t max_nodes) {
-  if (!c->has_file || (w.d_ctl && max_nodes <= w.miss_cap)) return HELIOS_OK;
+  (void)c;
+  if (w.d_ctl && max_nodes <= w.cap) return HELIOS_OK;
   HCUDA(cudaDeviceSynchronize());
   gws_free(w);
-  HCUDA(cudaMalloc(&w.d_miss_out, std::max<int64_t>(max_nodes, 1) * 8));
-  HCUDA(cudaMalloc(&w.d_miss_row, std::max<int64_t>(max_nodes, 1) * 8));
-  HCUDA(cudaMalloc(&w.d_ctl, 4 * sizeof(unsigned long long)));
-  HCUDA(cudaMemset(w.d_ctl, 0, 4 * sizeof(unsigned long long)));
-  w.miss_cap = max_nodes;
+  const int64_t cap = std::max<int64_t>(max_nodes, 1);
+  HCUDA(cudaMalloc(&w.d_list_i, kLists * cap * 8));
+  HCUDA(cudaMalloc(&w.d_list_w, kLists * cap * 8));
+  HCUDA(cudaMalloc(&w.d_ctl, kCtlWords * sizeof(unsigned long long)));
+  HCUDA(cudaMemset(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long)));
+  w.cap = cap;
   return HELIOS_OK;
 }
 
@@ -322,29 +349,27 @@ helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, 
                             void* out, helios_gather_stats* stats, cudaStream_t st) {
   HCHECK(nodes && n_nodes && (out || max_nodes == 0), HELIOS_E_INVALID, "null gather argument");
   HCHECK(c->G == 1 || c->peers_attached, HELIOS_E_STATE, "world_size %d but peers not attached", c->G);
-  HCHECK(!c->has_file || (w.d_ctl && max_nodes <= w.miss_cap), HELIOS_E_CAPACITY,
-         "max_nodes %lld > miss list cap %lld", (long long)max_nodes, (long long)w.miss_cap);
-  if (stats) HCUDA(cudaMemsetAsync(stats, 0, sizeof(helios_gather_stats), st));
-  if (c->has_file) HCUDA(cudaMemsetAsync(w.d_ctl, 0, 4 * sizeof(unsigned long long), st));
+  HCHECK(w.d_ctl && max_nodes <= w.cap, HELIOS_E_CAPACITY, "max_nodes %lld > gather list cap %lld",
+         (long long)max_nodes, (long long)w.cap);
+  HCUDA(cudaMemsetAsync(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long), st));
+  const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_nodes + 255) / 256), (int64_t)c->sms * 8);
+  k_lookup<<<lg, 256, 0, st>>>(nodes, n_nodes, c->dir, c->rank, w.d_list_i, w.d_list_w, w.cap, w.d_ctl);
   GatherArgs a;
-  a.nodes = nodes;
-  a.n_nodes = n_nodes;
-  a.dir = c->dir;
   a.out = (char*)out;
   a.R = c->R;
-  a.rank = c->rank;
+  a.li = w.d_list_i;
+  a.lw = w.d_list_w;
+  a.cap = w.cap;
+  a.ctl = w.d_ctl;
   a.hbm = c->hbm;
   a.peers = c->d_peers;
   a.host_dev = c->d_host_tier;
-  a.miss_out = w.d_miss_out;
-  a.miss_row = w.d_miss_row;
-  a.miss_count = w.d_ctl;
   a.stats = stats;
   const int nvec = c->R / 16;
-  if (nvec <= 32) launch_gather<1, 4>(a, c->sms, st);
-  else if (nvec <= 64) launch_gather<2, 2>(a, c->sms, st);
-  else if (nvec <= 128) launch_gather<4, 1>(a, c->sms, st);
-  else launch_gather<8, 1>(a, c->sms, st);
+  if (nvec <= 32) launch_gather<1, 4, 8>(a, c->sms, st);
+  else if (nvec <= 64) launch_gather<2, 2, 4>(a, c->sms, st);
+  else if (nvec <= 128) launch_gather<4, 1, 2>(a, c->sms, st);
+  else launch_gather<8, 1, 1>(a, c->sms, st);
   HCUDA(cudaGetLastError());
   return HELIOS_OK;
 }
@@ -355,8 +380,8 @@ helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, 
 helios_status io_launch(helios_cache* c, GatherWS& w, void* out, cudaStream_t st) {
   if (!c->has_file) return HELIOS_OK;
   IoArgs io;
-  io.miss_out = w.d_miss_out;
-  io.miss_row = w.d_miss_row;
+  io.miss_out = w.d_list_i + kListFile * w.cap;
+  io.miss_w = w.d_list_w + kListFile * w.cap;
   io.ctl = w.d_ctl;
   io.sq = c->io.d_sq;
   io.cq = c->io.d_cq;

@@ -77,12 +77,15 @@ struct SampleWS {
   cudaEvent_t params_ev = nullptr;
 };
 
-// Per-gather IO bookkeeping (miss list + tickets); one per gather context.
+// Per-gather bookkeeping (one per gather context): per-tier work lists written by the lookup
+// kernel, and the ticket / count words shared with the gather and IO kernels.
+enum : int { kListLocal = 0, kListPeer = 1, kListHost = 2, kListFile = 3, kLists = 4 };
+enum : int { kCtlSubmit = 4, kCtlComplete = 5, kCtlWords = 8 };
 struct GatherWS {
-  int64_t miss_cap = 0;
-  int64_t* d_miss_out = nullptr;    // output row of each FILE-tier miss
-  int64_t* d_miss_row = nullptr;    // file row of each miss
-  unsigned long long* d_ctl = nullptr;  // [0] miss count, [1] submit ticket, [2] complete ticket
+  int64_t cap = 0;                      // rows per list
+  int64_t* d_list_i = nullptr;          // [kLists * cap] output row of each entry
+  uint64_t* d_list_w = nullptr;         // [kLists * cap] directory word of each entry
+  unsigned long long* d_ctl = nullptr;  // [kCtlWords]: counts per list, then IO tickets
 };
 
 struct helios_graph_impl;
@@ -160,6 +163,7 @@ struct helios_cache {
   char* host_tier = nullptr;      // host pointer
   char* d_host_tier = nullptr;    // device-mapped alias
   bool host_owned = false;        // packed host tier allocated by us
+  bool host_tier_registered = false;  // we registered a caller-provided host tier
   bool host_registered = false;   // we registered host_table
   const void* host_table = nullptr;
   char** d_peers = nullptr;       // device [G] HBM shard base per rank (self included)
@@ -227,7 +231,8 @@ helios_status hot_count_enqueue(const int64_t* nodes, const int64_t* n_nodes, in
                                 int sms, cudaStream_t st);
 helios_status gws_ensure(helios_cache* c, GatherWS& w, int64_t max_nodes);
 void gws_free(GatherWS& w);
-// Lookup + gather of the HBM / host tiers; FILE-tier rows are appended to w's miss list.
+// K3 lookup (per-tier lists) + K4 gather of the HBM / host tiers; FILE-tier rows stay in w's
+// file list for io_launch.
 helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes,
                             void* out, helios_gather_stats* stats, cudaStream_t st);
 // IO rings for the misses of the last gather_launch on `st` (not capturable: cross-stream events).
