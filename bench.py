@@ -195,10 +195,32 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # HELIOS_BENCH_ONE_GPU=1: every rank on cuda:0 with gloo (exercises the N>1 path on one GPU;
+    # not a scaling measurement).  Default: one rank per GPU over NCCL.
+    one_gpu = os.environ.get("HELIOS_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
+    backend = "gloo" if one_gpu else "nccl"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+
+    def allreduce(t, op=None):
+        if world == 1:
+            return t
+        op = op or dist.ReduceOp.SUM
+        if backend == "gloo":
+            c_ = t.cpu()
+            dist.all_reduce(c_, op=op)
+            t.copy_(c_)
+        else:
+            dist.all_reduce(t, op=op)
+        return t
     from paper_2310_00837_b200 import helios as H
+    from paper_2310_00837_b200 import dist as hdist
 
     # ---- inputs (rank 0 generates; shared through /dev/shm when N > 1) ----
     t_setup = time.time()
@@ -234,8 +256,7 @@ def main():
     for b in mine:
         H.helios_presample(g, torch.as_tensor(inp.batches[b]).cuda(), cfg.B, cfg.fanouts, [pkeys[b]], hot)
     H.helios_graph_sync(g)
-    if world > 1:
-        dist.all_reduce(hot)
+    allreduce(hot)
     presample_s = time.time() - t1
     Hr, S = workloads.tier_rows(cfg, world)
     S = max(0, min(S, cfg.V - world * Hr)) if cfg.host_frac + cfg.hbm_frac >= 1.0 else S
@@ -258,10 +279,7 @@ def main():
             c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
                                      host_tier=tier)
     if world > 1:
-        blob = H.helios_cache_export(c)
-        blobs = [None] * world
-        dist.all_gather_object(blobs, blob)
-        H.helios_cache_attach_peers(c, blobs)
+        hdist.attach_peers(H, c)
         dist.barrier()
     build_s = time.time() - t2
     log(f"graph load + presample {presample_s:.1f}s, cache build {build_s:.1f}s (H={Hr}/GPU, S={S})")
@@ -309,8 +327,8 @@ def main():
             sample_ms.append(a)
             gather_ms.append(b_)
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    allreduce(t, dist.ReduceOp.MAX)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
     max_ms = float(t.item())
     if args.profile:
@@ -355,8 +373,7 @@ def main():
     e2e_s = time.perf_counter() - t_e2e
     H.helios_sync(c)
     e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    allreduce(e2e_t, dist.ReduceOp.MAX)
     e2e_s = float(e2e_t.item())
     # ---- parity at full size: GPU batches vs the oracle, bit for bit (rank 0) ----
     parity = None
@@ -412,7 +429,7 @@ def main():
     launches_per_step = 2 + 3 * L + 2 + (3 if c.info().file_rows > 0 else 0)
     out = {
         "metric": "sampled+gathered mini-batches/sec (feature GB/s and tier-roofline fraction alongside)",
-        "value": round(value, 3), "unit": "batches/s", "n_gpus": world, "steps": steps, "warmup": args.warmup,
+        "value": round(value, 3), "unit": "batches/s", "n_gpus": 1 if one_gpu else world, "steps": steps, "warmup": args.warmup,
         "ms_per_step": round(max_ms / steps, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int64 ids / fp32 feature bytes (u8 copy)",
         "data": "synthetic (seeded R-MAT-marginal power-law graph, synth_feature rows; no datasets)",
