@@ -178,7 +178,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--parity-batches", type=int, default=2)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no baseline, no parity")
-    ap.add_argument("--depth", type=int, default=2, help="batches in flight (plan slots)")
+    ap.add_argument("--depth", type=int, default=6, help="batches in flight (plan slots)")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly instead of CUDA graphs")
     ap.add_argument("--host-alias", action="store_true", help="host tier = canonical table by id (no packed copy)")
     args = ap.parse_args()
@@ -269,13 +269,15 @@ def main():
     elif world == 1:   # packed host tier in hot-rank order, pinned by the library
         c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table)
     else:              # one packed host tier shared by all ranks (/dev/shm), filled by rank 0
-        tier_buf = host_buffer(S * cfg.R, f"{shm}_tier", create=(rank == 0))
-        tier = np.frombuffer(tier_buf, dtype=np.uint8)
-        if rank == 0:
+        if rank == 0:  # creator first; the other ranks map the filled tier after the barrier
+            tier_buf = host_buffer(S * cfg.R, f"{shm}_tier", create=True)
+            tier = np.frombuffer(tier_buf, dtype=np.uint8)
             c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
                                      host_tier=tier, flags=H.HOST_FILL)
         dist.barrier()
         if rank != 0:
+            tier_buf = host_buffer(S * cfg.R, f"{shm}_tier", create=False)
+            tier = np.frombuffer(tier_buf, dtype=np.uint8)
             c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
                                      host_tier=tier)
     if world > 1:
@@ -309,9 +311,9 @@ def main():
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         start.record(stream)
-        for i in range(args.steps):
+        for i in range(args.steps):   # device timing events on every 4th batch (sampled stage times)
             b = seq[args.warmup + i]
-            H.helios_plan_submit(plan, i % depth, seed_of[b], keys[b], stream)
+            H.helios_plan_submit(plan, i % depth, seed_of[b], keys[b], stream, timing=(i % 4 == 0))
         for k in range(depth):
             H.helios_plan_wait(plan, k, stream)
         end.record(stream)
@@ -321,7 +323,7 @@ def main():
     total_ms = start.elapsed_time(end)
     sample_ms, gather_ms = [], []
     for k in range(depth):
-        n_k = len(range(k, args.steps, depth))
+        n_k = sum(1 for i in range(k, args.steps, depth) if i % 4 == 0)
         for back in range(min(n_k, 255)):
             a, b_ = H.helios_plan_timing(plan, k, back)
             sample_ms.append(a)
@@ -426,7 +428,7 @@ def main():
                    key=lambda x: x[1])[0]
     value = world * steps / (max_ms / 1e3)
     e2e_val = world * steps / e2e_s
-    launches_per_step = 2 + 3 * L + 2 + (3 if c.info().file_rows > 0 else 0)
+    launches_per_step = 3 * L + 2 + 2 + (3 if c.info().file_rows > 0 else 0)
     out = {
         "metric": "sampled+gathered mini-batches/sec (feature GB/s and tier-roofline fraction alongside)",
         "value": round(value, 3), "unit": "batches/s", "n_gpus": 1 if one_gpu else world, "steps": steps, "warmup": args.warmup,
@@ -442,7 +444,7 @@ def main():
                        (inp.graph.E * 4 + cfg.V * 8) / 1e9, cfg.V * R / 1e9)},
         "feature_gbs": round(world * n_rows / steps * R * steps / (max_ms / 1e3) / 1e9, 2),
         "stage_ms": {"sample": round(statistics.mean(sample_ms), 4), "gather": round(g_ms, 4),
-                     "note": f"per batch, device events around the two graph segments, {depth} batches in flight"},
+                     "note": f"per batch, device events around the two graph segments on every 4th batch, {depth} batches in flight"},
         "rows_per_batch": {"n_L": round(nL, 1), "hbm_local": round(n_local, 1), "hbm_peer": round(n_peer, 1),
                            "host": round(n_host, 1), "file": round(n_file, 1)},
         "roofline": {"bound": dominant, "kernel": "k_lookup + k_gather_lists (K3+K4)", "achieved": round(achieved, 2),

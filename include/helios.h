@@ -228,7 +228,8 @@ helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64
  *   c                cache, or NULL for a sampling-only plan (no features / stats).
  * Blocking create/free. */
 #define HELIOS_PLAN_NO_GRAPH 0x1u
-#define HELIOS_SUBMIT_SEEDS_HOST 0x1u  /* seeds pointer is host memory (copied to the slot, H2D) */
+#define HELIOS_SUBMIT_SEEDS_HOST 0x1u  /* seeds pointer is host memory (copied with the parameters, H2D) */
+#define HELIOS_SUBMIT_TIMING 0x2u      /* record device timing events around the sample / gather phases */
 typedef struct helios_plan helios_plan;
 typedef struct {
   int64_t max_seeds;
@@ -252,9 +253,10 @@ helios_status helios_plan_submit(helios_plan* p, int32_t slot, const int64_t* se
                                  uint32_t flags, void* stream);
 /* Makes `stream` wait for the last batch submitted to `slot`. */
 helios_status helios_plan_wait(helios_plan* p, int32_t slot, void* stream);
-/* Device time (ms) of the sampling and gather phases of a batch of `slot`: back = 0 is the slot's
- * last submitted batch, back = k the k-th before it (k < 256; CUDA events recorded around the two
- * graph segments).  Blocks until that batch is done; E_RANGE if it is no longer recorded. */
+/* Device time (ms) of the sampling and gather phases of a batch submitted to `slot` with
+ * HELIOS_SUBMIT_TIMING: back = 0 is the slot's last timed batch, back = k the k-th before it
+ * (k < 256; CUDA events recorded around the two graph segments, which are then launched as two
+ * graphs instead of one).  Blocks until that batch is done; E_RANGE if it is not recorded. */
 helios_status helios_plan_timing(helios_plan* p, int32_t slot, int32_t back, float* sample_ms, float* gather_ms);
 
 /* Waits for `stream` and the cache's IO streams; returns and clears latched errors of the cache

@@ -41,9 +41,9 @@ static helios_status sample_default(helios_graph* g, const int64_t* seeds, int64
   HCHECK(B == 0 || seeds, HELIOS_E_INVALID, "null seeds");
   s = ws_ensure(g, g->ws, B, fanouts, L);
   if (s != HELIOS_OK) return s;
-  s = ws_upload_params(g->ws, key, B, st);
+  s = ws_upload_params(g->ws, key, B, seeds, false, st);
   if (s != HELIOS_OK) return s;
-  return sample_launch(g, g->ws, seeds, B, fanouts, L, out, st);
+  return sample_launch(g, g->ws, B, fanouts, L, out, st);
 }
 
 static helios_status read_latched(int* d_err, helios_status* out) {

@@ -27,6 +27,10 @@ __device__ __forceinline__ uint32_t philox_word(uint64_t key, uint32_t h, uint64
   return w == 0 ? c0 : (w == 1 ? c1 : (w == 2 ? c2 : c3));
 }
 
+// PDL: wait for the predecessor grid's completion + memory flush / let dependents start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
   x ^= x >> 16;
   x *= 0x85EBCA6Bu;
@@ -85,31 +89,42 @@ __device__ __forceinline__ unsigned tile_ticket(const ScanState& s, unsigned* sm
   return *sm;
 }
 
-// Decoupled look-back (Merrill & Garland 2016): publish this tile's aggregate, walk back to the
-// nearest inclusive prefix, publish our inclusive prefix; returns the exclusive prefix of the tile.
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+// Decoupled look-back (Merrill & Garland 2016): publish this tile's aggregate, then warp 0 inspects
+// 32 predecessors per step (closest first) until one carries an inclusive prefix, and publishes
+// this tile's inclusive prefix.  Returns the exclusive prefix of the tile to every thread.
 __device__ __forceinline__ long long tile_lookback(const ScanState& s, unsigned tile, long long agg, long long* sm) {
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
     long long prefix = 0;
     if (tile == 0) {
-      atomicExch(&s.status[0], kStatusIncl | (unsigned long long)agg);
+      if (lane == 0) atomicExch(&s.status[0], kStatusIncl | (unsigned long long)agg);
     } else {
-      atomicExch(&s.status[tile], (unsigned long long)agg);
+      if (lane == 0) atomicExch(&s.status[tile], (unsigned long long)agg);
       long long acc = 0;
-      int j = (int)tile - 1;
-      for (;;) {
-        unsigned long long w = ld_volatile_u64(&s.status[j]);
-        if (w == kStatusInvalid) continue;
-        if (w & kStatusIncl) {
-          acc += (long long)(w & ~kStatusIncl);
+      for (long long base = (long long)tile - 1;; base -= 32) {
+        const long long j = base - lane;
+        unsigned long long w = (j >= 0) ? ld_volatile_u64(&s.status[j]) : kStatusIncl;  // before tile 0: 0
+        while (__any_sync(0xFFFFFFFFu, w == kStatusInvalid))
+          if (w == kStatusInvalid) w = ld_volatile_u64(&s.status[j]);
+        const unsigned incl = __ballot_sync(0xFFFFFFFFu, (w & kStatusIncl) != 0);
+        long long v = (long long)(w & ~kStatusIncl);
+        if (incl) {
+          const int stop = __ffs(incl) - 1;  // closest predecessor with an inclusive prefix
+          acc += warp_sum_ll(lane <= stop ? v : 0);
           break;
         }
-        acc += (long long)w;
-        j--;
+        acc += warp_sum_ll(v);
       }
       prefix = acc;
-      atomicExch(&s.status[tile], kStatusIncl | (unsigned long long)(acc + agg));
+      if (lane == 0) atomicExch(&s.status[tile], kStatusIncl | (unsigned long long)(acc + agg));
     }
-    *sm = prefix;
+    if (lane == 0) *sm = prefix;
   }
   __syncthreads();
   return *sm;

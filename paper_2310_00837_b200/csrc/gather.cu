@@ -30,6 +30,7 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
 __global__ void __launch_bounds__(256) k_lookup(const int64_t* __restrict__ nodes, const int64_t* __restrict__ n_nodes,
                                                 const int64_t* __restrict__ dir, int32_t rank, int64_t* __restrict__ li,
                                                 uint64_t* __restrict__ lw, int64_t cap, unsigned long long* ctl) {
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t n = *n_nodes;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -117,6 +118,8 @@ __device__ __forceinline__ void copy_rows(const GatherArgs& a, int q, int64_t j0
 // and the link streams) while the others copy peer (NVLink) then local HBM rows.
 template <int VPL, int U, int UH>
 __global__ void __launch_bounds__(256, 4) k_gather_lists(GatherArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -321,7 +324,7 @@ static void launch_gather(const GatherArgs& a, int sms, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_lists<VPL, U, UH>, 256, 0);
     per_sm = std::max(per_sm, 1);
   }
-  k_gather_lists<VPL, U, UH><<<sms * per_sm, 256, 0, st>>>(a);
+  launch_pdl(k_gather_lists<VPL, U, UH>, dim3(sms * per_sm), dim3(256), st, a);
 }
 
 void gws_free(GatherWS& w) {
@@ -352,7 +355,7 @@ helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, 
   HCHECK(w.d_ctl && max_nodes <= w.cap, HELIOS_E_CAPACITY, "max_nodes %lld > gather list cap %lld",
          (long long)max_nodes, (long long)w.cap);
   HCUDA(cudaMemsetAsync(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long), st));
-  const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_nodes + 255) / 256), (int64_t)c->sms * 8);
+  const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_nodes + 255) / 256), (int64_t)c->sms * 2);
   k_lookup<<<lg, 256, 0, st>>>(nodes, n_nodes, c->dir, c->rank, w.d_list_i, w.d_list_w, w.cap, w.d_ctl);
   GatherArgs a;
   a.out = (char*)out;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <utility>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -45,6 +46,24 @@ struct DeviceGuard {
   }
 };
 
+// Programmatic dependent launch (sm_90+): the kernel may start launching while its predecessor in
+// the stream drains; it must execute griddepcontrol.wait (pdl_wait) before touching the
+// predecessor's results.  Captured into CUDA graphs as programmatic edges.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // empty hash key / unassigned local id / no minpos
 constexpr int kScanBlock = 256;
 constexpr int kScanItems = 4;
@@ -70,8 +89,16 @@ struct SampleWS {
   ScanState row_scan[HELIOS_MAX_HOPS];
   ScanState edge_scan[HELIOS_MAX_HOPS];
   uint32_t* slot_of = nullptr;  // [cap_edges] hash slot of each sampled edge of the current hop
+  uint32_t* node_slot = nullptr;  // [cap_nodes] hash slot of every node of the batch (table clear)
+  int64_t cap_nodes = 0;
+  // The table is all-EMPTY between batches: it is memset once at allocation and every batch
+  // clears exactly the slots it occupied (k_table_clear); only the small scan-state region
+  // [scan_base, scan_base + scan_bytes) is memset per batch.
+  char* scan_base = nullptr;
+  size_t scan_bytes = 0;
   // per-batch parameters, read by the kernels from device memory so that a captured CUDA graph
-  // can be replayed for every batch: [0] key, [1] n_seeds
+  // can be replayed for every batch: [0] key, [1] n_seeds, [2] seeds device pointer, [3] reserved,
+  // [4, 4 + cap_seeds) inline seeds (host-seed submits: one H2D copy carries parameters + seeds)
   int64_t* d_params = nullptr;
   int64_t* h_params = nullptr;  // pinned staging for the parameter upload
   cudaEvent_t params_ev = nullptr;
@@ -191,14 +218,13 @@ struct PlanSlot {
   void* mem = nullptr;
   char* feats = nullptr;
   helios_gather_stats* stats = nullptr;
-  int64_t* d_seeds = nullptr;
-  int64_t* h_seeds = nullptr;
   cudaStream_t stream = nullptr;
-  cudaGraphExec_t g_sample = nullptr, g_gather = nullptr;
+  cudaGraphExec_t g_sample = nullptr, g_gather = nullptr, g_all = nullptr;
   cudaEvent_t ev_caller = nullptr, ev_end = nullptr;
   static constexpr int kRing = 256;
-  std::vector<cudaEvent_t> ring;  // kRing x {start, mid, end} timing events
+  std::vector<cudaEvent_t> ring;  // kRing x {start, mid, end} timing events (timed submits only)
   int64_t count = 0;              // batches submitted to this slot
+  int64_t tcount = 0;             // timed batches submitted to this slot
   bool submitted = false;
 };
 
@@ -222,11 +248,13 @@ helios_status sample_check_out(const helios_graph* g, int64_t B, const int32_t* 
                                const helios_blocks* out);
 helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* fanouts, int32_t L);
 void ws_free(SampleWS& w);
-// Uploads (key, n_seeds) into w.d_params on `st` (not capturable; done before a graph replay).
-helios_status ws_upload_params(SampleWS& w, uint64_t key, int64_t B, cudaStream_t st);
-// Enqueues the sampling kernels; they read key / n_seeds from w.d_params.  B_max sizes the grids.
-helios_status sample_launch(helios_graph* g, SampleWS& w, const int64_t* seeds, int64_t B_max, const int32_t* fanouts,
-                            int32_t L, const helios_blocks* out, cudaStream_t st);
+// Uploads (key, n_seeds, seeds) into w.d_params on `st` with ONE copy (not capturable; done before
+// a graph replay).  seeds_host: copy the seeds inline (host memory), else pass the device pointer.
+helios_status ws_upload_params(SampleWS& w, uint64_t key, int64_t B, const int64_t* seeds, bool seeds_host,
+                               cudaStream_t st);
+// Enqueues the sampling kernels; they read key / n_seeds / seeds from w.d_params.  B_max sizes the grids.
+helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const int32_t* fanouts, int32_t L,
+                            const helios_blocks* out, cudaStream_t st);
 helios_status hot_count_enqueue(const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, uint64_t* hot,
                                 int sms, cudaStream_t st);
 helios_status gws_ensure(helios_cache* c, GatherWS& w, int64_t max_nodes);

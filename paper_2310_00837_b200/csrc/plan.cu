@@ -22,10 +22,9 @@ void plan_free_impl(helios_plan* p) {
     gws_free(s.gws);
     if (s.mem) cudaFree(s.mem);
     if (s.feats) cudaFree(s.feats);
-    if (s.d_seeds) cudaFree(s.d_seeds);
-    if (s.h_seeds) cudaFreeHost(s.h_seeds);
     if (s.g_sample) cudaGraphExecDestroy(s.g_sample);
     if (s.g_gather) cudaGraphExecDestroy(s.g_gather);
+    if (s.g_all) cudaGraphExecDestroy(s.g_all);
     for (cudaEvent_t e : {s.ev_caller, s.ev_end})
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : s.ring)
@@ -82,8 +81,6 @@ helios_status plan_create_impl(helios_plan* p) {
       q += (edg[h] * 4 + 255) / 256 * 256;
     }
     HCUDA(cudaMemset(sl.blocks.level_counts, 0, 256));
-    HCUDA(cudaMalloc(&sl.d_seeds, std::max<int64_t>(d.max_seeds, 1) * 8));
-    HCUDA(cudaHostAlloc(&sl.h_seeds, std::max<int64_t>(d.max_seeds, 1) * 8, cudaHostAllocDefault));
     if (p->c) {
       HCUDA(cudaMalloc(&sl.feats, std::max<int64_t>(p->maxn, 1) * (int64_t)p->c->R));
       HCUDA(cudaMalloc(&sl.stats, sizeof(helios_gather_stats)));
@@ -99,17 +96,22 @@ helios_status plan_create_impl(helios_plan* p) {
     sl.ring.assign(3 * PlanSlot::kRing, nullptr);
     for (auto& e : sl.ring) HCUDA(cudaEventCreate(&e));
     if (p->graphs) {
-      s = capture(sl.stream, &sl.g_sample, [&]() {
-        return sample_launch(g, sl.ws, sl.d_seeds, d.max_seeds, d.fanouts, d.L, &sl.blocks, sl.stream);
-      });
+      auto sample_ops = [&]() { return sample_launch(g, sl.ws, d.max_seeds, d.fanouts, d.L, &sl.blocks, sl.stream); };
+      auto gather_ops = [&]() {
+        return gather_launch(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + d.L, sl.blocks.nodes_cap,
+                             sl.feats, sl.stats, sl.stream);
+      };
+      s = capture(sl.stream, &sl.g_sample, sample_ops);
       if (s != HELIOS_OK) return s;
       if (p->c) {
-        s = capture(sl.stream, &sl.g_gather, [&]() {
-          return gather_launch(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + d.L, sl.blocks.nodes_cap,
-                               sl.feats, sl.stats, sl.stream);
-        });
+        s = capture(sl.stream, &sl.g_gather, gather_ops);
         if (s != HELIOS_OK) return s;
       }
+      s = capture(sl.stream, &sl.g_all, [&]() {  // the whole batch in one graph (untimed submits)
+        helios_status r = sample_ops();
+        return (r == HELIOS_OK && p->c) ? gather_ops() : r;
+      });
+      if (s != HELIOS_OK) return s;
     }
   }
   HCUDA(cudaDeviceSynchronize());
@@ -125,38 +127,39 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
   PlanSlot& sl = p->slots[slot];
   HCUDA(cudaEventRecord(sl.ev_caller, caller));
   HCUDA(cudaStreamWaitEvent(sl.stream, sl.ev_caller, 0));
-  if (n > 0) {
-    if (flags & HELIOS_SUBMIT_SEEDS_HOST) {
-      HCUDA(cudaEventSynchronize(sl.ws.params_ev));  // previous H2D from h_seeds is done
-      memcpy(sl.h_seeds, seeds, n * 8);
-      HCUDA(cudaMemcpyAsync(sl.d_seeds, sl.h_seeds, n * 8, cudaMemcpyHostToDevice, sl.stream));
-    } else {
-      HCUDA(cudaMemcpyAsync(sl.d_seeds, seeds, n * 8, cudaMemcpyDeviceToDevice, sl.stream));
-    }
-  }
-  helios_status s = ws_upload_params(sl.ws, key, n, sl.stream);
+  helios_status s = ws_upload_params(sl.ws, key, n, seeds, (flags & HELIOS_SUBMIT_SEEDS_HOST) != 0, sl.stream);
   if (s != HELIOS_OK) return s;
-  cudaEvent_t* ev = &sl.ring[3 * (sl.count % PlanSlot::kRing)];
-  HCUDA(cudaEventRecord(ev[0], sl.stream));
-  if (p->graphs) {
-    HCUDA(cudaGraphLaunch(sl.g_sample, sl.stream));
+  const bool timed = (flags & HELIOS_SUBMIT_TIMING) != 0;
+  cudaEvent_t* ev = &sl.ring[3 * (sl.tcount % PlanSlot::kRing)];
+  if (timed) HCUDA(cudaEventRecord(ev[0], sl.stream));
+  if (p->graphs && !timed) {
+    HCUDA(cudaGraphLaunch(sl.g_all, sl.stream));
   } else {
-    s = sample_launch(p->g, sl.ws, sl.d_seeds, p->d.max_seeds, p->d.fanouts, p->d.L, &sl.blocks, sl.stream);
-    if (s != HELIOS_OK) return s;
-  }
-  HCUDA(cudaEventRecord(ev[1], sl.stream));
-  if (p->c) {
     if (p->graphs) {
-      HCUDA(cudaGraphLaunch(sl.g_gather, sl.stream));
+      HCUDA(cudaGraphLaunch(sl.g_sample, sl.stream));
     } else {
-      s = gather_launch(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + p->d.L, sl.blocks.nodes_cap, sl.feats,
-                        sl.stats, sl.stream);
+      s = sample_launch(p->g, sl.ws, p->d.max_seeds, p->d.fanouts, p->d.L, &sl.blocks, sl.stream);
       if (s != HELIOS_OK) return s;
     }
+    if (timed) HCUDA(cudaEventRecord(ev[1], sl.stream));
+    if (p->c) {
+      if (p->graphs) {
+        HCUDA(cudaGraphLaunch(sl.g_gather, sl.stream));
+      } else {
+        s = gather_launch(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + p->d.L, sl.blocks.nodes_cap,
+                          sl.feats, sl.stats, sl.stream);
+        if (s != HELIOS_OK) return s;
+      }
+    }
+  }
+  if (p->c) {
     s = io_launch(p->c, sl.gws, sl.feats, sl.stream);
     if (s != HELIOS_OK) return s;
   }
-  HCUDA(cudaEventRecord(ev[2], sl.stream));
+  if (timed) {
+    HCUDA(cudaEventRecord(ev[2], sl.stream));
+    sl.tcount++;
+  }
   HCUDA(cudaEventRecord(sl.ev_end, sl.stream));
   sl.count++;
   sl.submitted = true;
@@ -174,9 +177,9 @@ helios_status plan_wait_impl(helios_plan* p, int32_t slot, cudaStream_t st) {
 helios_status plan_timing_impl(helios_plan* p, int32_t slot, int32_t back, float* sample_ms, float* gather_ms) {
   HCHECK(slot >= 0 && slot < (int32_t)p->slots.size(), HELIOS_E_INVALID, "slot %d of %zu", slot, p->slots.size());
   PlanSlot& sl = p->slots[slot];
-  HCHECK(back >= 0 && back < PlanSlot::kRing && back < sl.count, HELIOS_E_RANGE, "slot %d: batch -%d not recorded", slot,
-         back);
-  cudaEvent_t* ev = &sl.ring[3 * ((sl.count - 1 - back) % PlanSlot::kRing)];
+  HCHECK(back >= 0 && back < PlanSlot::kRing && back < sl.tcount, HELIOS_E_RANGE,
+         "slot %d: timed batch -%d not recorded", slot, back);
+  cudaEvent_t* ev = &sl.ring[3 * ((sl.tcount - 1 - back) % PlanSlot::kRing)];
   HCUDA(cudaEventSynchronize(ev[2]));
   float a = 0, b = 0;
   HCUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));

@@ -3,10 +3,10 @@
 //
 // A batch is 2 + 3L kernels (all enqueue-only; grids sized from host bounds, actual counts read
 // from device memory, so the whole sequence is captured once into a CUDA graph and replayed):
-//   k_insert_seeds     N_0 = seeds into the batch hash table (duplicate / out-of-range latched).
 //   per hop h:
 //   k_row_count_scan   k_i = min(deg(N_h[i]), f_h); block_indptr[h] = exclusive scan (single-pass
-//                      decoupled look-back), e_h = total.  Side job: relabel hop h-1's edges.
+//                      decoupled look-back), e_h = total.  Side job: relabel hop h-1's edges (h > 0)
+//                      or insert N_0 = seeds into the batch hash table (h = 0: k_seed_count_scan).
 //   k_fill_insert<G>   one G-lane group per row: copy the whole adjacency when k == d, else Floyd's
 //                      k-subset with Philox draws resolved by group ballots; every sampled id is
 //                      inserted into the open-addressing table right away (slot kept per edge) and
@@ -15,6 +15,7 @@
 //                      the flags numbers the new ids n_h, n_h+1, ... in first-occurrence order and
 //                      appends them to N_{h+1}.
 //   k_relabel          (last hop only) block_indices[L-1][e] = local id of the edge's slot.
+//   k_table_clear      resets the slots of N_L so the table is all-EMPTY for the next batch.
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
@@ -46,26 +47,95 @@ helios_status validate_csr_device(const int64_t* indptr, const int32_t* indices,
   return HELIOS_OK;
 }
 
-__global__ void k_insert_seeds(const int64_t* __restrict__ seeds, const int64_t* __restrict__ params, int64_t V,
-                               uint32_t* keys, uint32_t* local, uint32_t mask, int64_t* __restrict__ nodes,
-                               int64_t* level_counts, int* err) {
-  const int64_t B = params[1];
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i == 0) level_counts[0] = B;
-  if (i >= B) return;
+// N_0 = seeds: copy into nodes, insert into the table with local id = position.  Duplicate or
+// out-of-range seeds are latched (reading 7).
+__device__ __forceinline__ void insert_seed(int64_t i, const int64_t* __restrict__ seeds, int64_t V, uint32_t* keys,
+                                            uint32_t* local, uint32_t mask, int64_t* __restrict__ nodes,
+                                            uint32_t* __restrict__ node_slot, int* err) {
   const int64_t u = seeds[i];
   nodes[i] = u;
+  node_slot[i] = kEmpty;
   if (u < 0 || u >= V) {
     latch(err, HELIOS_E_RANGE);
     return;
   }
   bool fresh;
   const uint32_t s = table_insert(keys, mask, (uint32_t)u, &fresh);
+  node_slot[i] = s;
   if (!fresh) {
-    latch(err, HELIOS_E_INVALID);  // duplicate seed (reading 7)
+    latch(err, HELIOS_E_INVALID);
     return;
   }
   local[s] = (uint32_t)i;
+}
+
+__global__ void k_insert_seeds(const int64_t* __restrict__ params, int64_t V,
+                               uint32_t* keys, uint32_t* local, uint32_t mask, int64_t* __restrict__ nodes,
+                               uint32_t* __restrict__ node_slot, int64_t* level_counts, int* err) {
+  const int64_t B = params[1];
+  const int64_t* seeds = (const int64_t*)params[2];
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i == 0) level_counts[0] = B;
+  if (i < B) insert_seed(i, seeds, V, keys, local, mask, nodes, node_slot, err);
+}
+
+// Hop 0 of a batch: the degree scan reads the seeds straight from the batch parameters (n_0 = B)
+// and inserts them into the table on the side (k_fill_insert of hop 0, the next kernel, needs them).
+__global__ void __launch_bounds__(kScanBlock) k_seed_count_scan(const int64_t* __restrict__ params,
+                                                                const int64_t* __restrict__ indptr, int64_t V,
+                                                                int32_t f, int32_t* __restrict__ bp,
+                                                                int64_t* edge_counts, int64_t* level_counts,
+                                                                ScanState ss, uint32_t* keys, uint32_t* local,
+                                                                uint32_t mask, int64_t* __restrict__ nodes,
+                                                                uint32_t* __restrict__ node_slot, int* err) {
+  pdl_trigger();
+  using BS = cub::BlockScan<long long, kScanBlock>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ unsigned s_tile;
+  __shared__ long long s_prefix;
+  const int64_t n = params[1];
+  const int64_t* seeds = (const int64_t*)params[2];
+  for (;;) {  // persistent: tiles are taken in ticket order until they pass n
+    const unsigned tile = tile_ticket(ss, &s_tile);
+    const int64_t base = (int64_t)tile * kScanTile;
+    if (tile > 0 && base >= n) break;
+    if (tile == 0 && threadIdx.x == 0) level_counts[0] = n;
+    long long k[kScanItems];
+    long long sum = 0;
+#pragma unroll
+    for (int q = 0; q < kScanItems; q++) {
+      const int64_t i = base + threadIdx.x * kScanItems + q;
+      k[q] = 0;
+      if (i < n) {
+        const int64_t v = seeds[i];
+        if ((uint64_t)v < (uint64_t)V) {
+          const int64_t d = indptr[v + 1] - indptr[v];
+          k[q] = (f < 0) ? d : min(d, (int64_t)f);
+        }
+      }
+      sum += k[q];
+    }
+    long long excl, agg;
+    BS(tmp).ExclusiveSum(sum, excl, agg);
+    const long long prefix = tile_lookback(ss, tile, agg, &s_prefix);
+    long long run = prefix + excl;
+#pragma unroll
+    for (int q = 0; q < kScanItems; q++) {
+      const int64_t i = base + threadIdx.x * kScanItems + q;
+      if (i < n) bp[i] = (int32_t)run;
+      run += k[q];
+    }
+    if (threadIdx.x == 0 && ((n == 0 && tile == 0) || (base < n && n <= base + kScanTile))) {
+      bp[n] = (int32_t)(prefix + agg);
+      edge_counts[0] = prefix + agg;
+    }
+#pragma unroll
+    for (int q = 0; q < kScanItems; q++) {
+      const int64_t i = base + threadIdx.x * kScanItems + q;
+      if (i < n) insert_seed(i, seeds, V, keys, local, mask, nodes, node_slot, err);
+    }
+    __syncthreads();
+  }
 }
 
 // k_i = min(deg, f) and the exclusive scan of k into block_indptr[h]; relabels hop h-1 on the side.
@@ -76,14 +146,17 @@ __global__ void __launch_bounds__(kScanBlock) k_row_count_scan(const int64_t* __
                                                                ScanState ss, int32_t* __restrict__ prev_bi,
                                                                const uint32_t* __restrict__ slot_of,
                                                                const uint32_t* __restrict__ local) {
+  pdl_wait();
+  pdl_trigger();
   using BS = cub::BlockScan<long long, kScanBlock>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ unsigned s_tile;
   __shared__ long long s_prefix;
-  const unsigned tile = tile_ticket(ss, &s_tile);
   const int64_t n = level_counts[h];
-  const int64_t base = (int64_t)tile * kScanTile;
-  if (tile == 0 || base < n) {
+  for (;;) {  // persistent: tiles are taken in ticket order until they pass n
+    const unsigned tile = tile_ticket(ss, &s_tile);
+    const int64_t base = (int64_t)tile * kScanTile;
+    if (tile > 0 && base >= n) break;
     long long k[kScanItems];
     long long sum = 0;
 #pragma unroll
@@ -113,10 +186,11 @@ __global__ void __launch_bounds__(kScanBlock) k_row_count_scan(const int64_t* __
       bp[n] = (int32_t)(prefix + agg);
       edge_counts[h] = prefix + agg;
     }
+    __syncthreads();
   }
   if (prev_bi) {  // side job: hop h-1's local ids are final (its k_dedup_assign has completed)
     const int64_t ep = edge_counts[h - 1];
-    for (int64_t e = (int64_t)tile * blockDim.x + threadIdx.x; e < ep; e += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ep; e += (int64_t)gridDim.x * blockDim.x)
       prev_bi[e] = (int32_t)local[slot_of[e]];
   }
 }
@@ -131,6 +205,8 @@ __global__ void __launch_bounds__(256) k_fill_insert(const int64_t* __restrict__
                                                      const int32_t* __restrict__ bp, int32_t* scratch,
                                                      uint32_t* keys, uint32_t* minpos, const uint32_t* local,
                                                      uint32_t mask, uint32_t* __restrict__ slot_of) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   const unsigned gmask = (G == 32) ? 0xFFFFFFFFu : (((1u << G) - 1u) << (lane & ~(G - 1)));
@@ -210,52 +286,78 @@ __global__ void __launch_bounds__(kScanBlock) k_dedup_assign(const int64_t* __re
                                                              const uint32_t* __restrict__ keys,
                                                              const uint32_t* __restrict__ minpos, uint32_t* local,
                                                              int64_t* __restrict__ nodes, int64_t* level_counts,
-                                                             ScanState ss) {
+                                                             ScanState ss, uint32_t* __restrict__ node_slot) {
+  pdl_wait();
+  pdl_trigger();
   using BS = cub::BlockScan<int, kScanBlock>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ unsigned s_tile;
   __shared__ long long s_prefix;
-  const unsigned tile = tile_ticket(ss, &s_tile);
   const int64_t eh = edge_counts[h];
   const int64_t nh = level_counts[h];
-  const int64_t base = (int64_t)tile * kScanTile;
-  if (tile > 0 && base >= eh) return;
-  int flag[kScanItems];
-  uint32_t slot[kScanItems];
-  int sum = 0;
+  for (;;) {  // persistent: tiles are taken in ticket order until they pass e_h
+    const unsigned tile = tile_ticket(ss, &s_tile);
+    const int64_t base = (int64_t)tile * kScanTile;
+    if (tile > 0 && base >= eh) break;
+    int flag[kScanItems];
+    uint32_t slot[kScanItems];
+    int sum = 0;
 #pragma unroll
-  for (int q = 0; q < kScanItems; q++) {
-    const int64_t e = base + threadIdx.x * kScanItems + q;
-    flag[q] = 0;
-    slot[q] = 0;
-    if (e < eh) {
-      slot[q] = slot_of[e];
-      flag[q] = (ld_volatile_u32(local + slot[q]) == kEmpty && minpos[slot[q]] == (uint32_t)e) ? 1 : 0;
+    for (int q = 0; q < kScanItems; q++) {
+      const int64_t e = base + threadIdx.x * kScanItems + q;
+      flag[q] = 0;
+      slot[q] = 0;
+      if (e < eh) {
+        slot[q] = slot_of[e];
+        flag[q] = (ld_volatile_u32(local + slot[q]) == kEmpty && minpos[slot[q]] == (uint32_t)e) ? 1 : 0;
+      }
+      sum += flag[q];
     }
-    sum += flag[q];
-  }
-  int excl, agg;
-  BS(tmp).ExclusiveSum(sum, excl, agg);
-  const long long prefix = tile_lookback(ss, tile, agg, &s_prefix);
-  long long run = prefix + excl;
+    int excl, agg;
+    BS(tmp).ExclusiveSum(sum, excl, agg);
+    const long long prefix = tile_lookback(ss, tile, agg, &s_prefix);
+    long long run = prefix + excl;
 #pragma unroll
-  for (int q = 0; q < kScanItems; q++) {
-    if (flag[q]) {
-      const int64_t id = nh + run;
-      nodes[id] = (int64_t)keys[slot[q]];
-      local[slot[q]] = (uint32_t)id;
-      run++;
+    for (int q = 0; q < kScanItems; q++) {
+      if (flag[q]) {
+        const int64_t id = nh + run;
+        nodes[id] = (int64_t)keys[slot[q]];
+        node_slot[id] = slot[q];
+        local[slot[q]] = (uint32_t)id;
+        run++;
+      }
     }
+    if (threadIdx.x == 0 && ((eh == 0 && tile == 0) || (base < eh && eh <= base + kScanTile)))
+      level_counts[h + 1] = nh + prefix + agg;
+    __syncthreads();
   }
-  if (threadIdx.x == 0 && ((eh == 0 && tile == 0) || (base < eh && eh <= base + kScanTile)))
-    level_counts[h + 1] = nh + prefix + agg;
 }
 
 __global__ void __launch_bounds__(256) k_relabel(int32_t* bi, const int64_t* __restrict__ edge_counts, int h,
                                                  const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ local) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t eh = edge_counts[h];
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < eh; e += (int64_t)gridDim.x * blockDim.x)
     bi[e] = (int32_t)local[slot_of[e]];
+}
+
+// Returns the batch hash table to all-EMPTY by clearing exactly the slots of the batch's nodes
+// (every occupied slot belongs to one node of N_L).
+__global__ void __launch_bounds__(256) k_table_clear(const int64_t* __restrict__ n_nodes,
+                                                     const uint32_t* __restrict__ node_slot, uint32_t* keys,
+                                                     uint32_t* minpos, uint32_t* local) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t n = *n_nodes;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = node_slot[i];
+    if (s != kEmpty) {
+      keys[s] = kEmpty;
+      minpos[s] = kEmpty;
+      local[s] = kEmpty;
+    }
+  }
 }
 
 __global__ void k_hot_count(const int64_t* __restrict__ nodes, const int64_t* __restrict__ n_nodes, uint64_t* hot) {
@@ -321,6 +423,7 @@ static uint32_t pow2_at_least(int64_t x) {
 void ws_free(SampleWS& w) {
   if (w.reset_base) cudaFree(w.reset_base);
   if (w.slot_of) cudaFree(w.slot_of);
+  if (w.node_slot) cudaFree(w.node_slot);
   if (w.d_params) cudaFree(w.d_params);
   if (w.h_params) cudaFreeHost(w.h_params);
   if (w.params_ev) cudaEventDestroy(w.params_ev);
@@ -338,8 +441,9 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
     tiles_e = std::max(tiles_e, (edg[h] + kScanTile - 1) / kScanTile);
   }
   uint32_t T = pow2_at_least(2 * std::min<int64_t>(g->V, std::max<int64_t>(maxn, 1)));
+  const int64_t max_nodes = std::max<int64_t>(maxn, 1);
   if (w.reset_base && T <= w.table_size && max_e <= w.cap_edges && tiles_r <= w.cap_tiles_rows &&
-      tiles_e <= w.cap_tiles_edges)
+      tiles_e <= w.cap_tiles_edges && max_nodes <= w.cap_nodes && B <= w.cap_seeds)
     return HELIOS_OK;
   HCUDA(cudaDeviceSynchronize());
   ws_free(w);
@@ -349,8 +453,11 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
   w.reset_bytes = 3 * table_bytes + status_bytes + counter_bytes;
   HCUDA(cudaMalloc(&w.reset_base, w.reset_bytes));
   HCUDA(cudaMalloc(&w.slot_of, (size_t)max_e * 4));
-  HCUDA(cudaMalloc(&w.d_params, 4 * sizeof(int64_t)));
-  HCUDA(cudaHostAlloc(&w.h_params, 4 * sizeof(int64_t), cudaHostAllocDefault));
+  HCUDA(cudaMalloc(&w.node_slot, (size_t)max_nodes * 4));
+  w.cap_nodes = max_nodes;
+  w.cap_seeds = std::max<int64_t>(B, 1);
+  HCUDA(cudaMalloc(&w.d_params, (4 + w.cap_seeds) * sizeof(int64_t)));
+  HCUDA(cudaHostAlloc(&w.h_params, (4 + w.cap_seeds) * sizeof(int64_t), cudaHostAllocDefault));
   HCUDA(cudaEventCreateWithFlags(&w.params_ev, cudaEventDisableTiming));
   w.table_size = T;
   w.cap_edges = max_e;
@@ -363,6 +470,7 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
   p += table_bytes;
   w.local = (uint32_t*)p;
   p += table_bytes;
+  w.scan_base = p;
   for (int h = 0; h < HELIOS_MAX_HOPS; h++) {
     w.row_scan[h].status = (unsigned long long*)p;
     p += tiles_r * 8;
@@ -375,14 +483,27 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
     w.edge_scan[h].counter = (unsigned*)p;
     p += 4;
   }
+  w.scan_bytes = (size_t)(p - w.scan_base);
+  HCUDA(cudaMemset(w.reset_base, 0xFF, w.reset_bytes));  // the table starts all-EMPTY
   return HELIOS_OK;
 }
 
-helios_status ws_upload_params(SampleWS& w, uint64_t key, int64_t B, cudaStream_t st) {
+helios_status ws_upload_params(SampleWS& w, uint64_t key, int64_t B, const int64_t* seeds, bool seeds_host,
+                               cudaStream_t st) {
+  HCHECK(B <= w.cap_seeds, HELIOS_E_CAPACITY, "n_seeds %lld > workspace capacity %lld", (long long)B,
+         (long long)w.cap_seeds);
   HCUDA(cudaEventSynchronize(w.params_ev));  // the previous upload has been consumed
   w.h_params[0] = (int64_t)key;
   w.h_params[1] = B;
-  HCUDA(cudaMemcpyAsync(w.d_params, w.h_params, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  size_t bytes = 4 * sizeof(int64_t);
+  if (seeds_host) {
+    if (B > 0) memcpy(w.h_params + 4, seeds, B * sizeof(int64_t));
+    w.h_params[2] = (int64_t)(uintptr_t)(w.d_params + 4);
+    bytes += B * sizeof(int64_t);
+  } else {
+    w.h_params[2] = (int64_t)(uintptr_t)seeds;
+  }
+  HCUDA(cudaMemcpyAsync(w.d_params, w.h_params, bytes, cudaMemcpyHostToDevice, st));
   HCUDA(cudaEventRecord(w.params_ev, st));
   return HELIOS_OK;
 }
@@ -391,39 +512,53 @@ template <int G>
 static void launch_fill(const helios_graph* g, SampleWS& w, const helios_blocks* out, int h, int64_t rows, int32_t f,
                         cudaStream_t st) {
   const int64_t threads = std::max<int64_t>(rows, 1) * G;
-  const int grid = (int)std::min<int64_t>((threads + 255) / 256, (int64_t)g->sms * 16);
-  k_fill_insert<G><<<grid, 256, 0, st>>>(out->nodes, out->level_counts, h, g->indptr, g->indices, g->V, f, w.d_params,
-                                         out->block_indptr[h], out->block_indices[h], w.keys, w.minpos, w.local,
-                                         w.table_size - 1, w.slot_of);
+  const int grid = (int)std::min<int64_t>((threads + 255) / 256, (int64_t)g->sms * 4);
+  launch_pdl(k_fill_insert<G>, dim3(grid), dim3(256), st, out->nodes, (const int64_t*)out->level_counts, h,
+             (const int64_t*)g->indptr, (const int32_t*)g->indices, g->V, f, (const int64_t*)w.d_params,
+             (const int32_t*)out->block_indptr[h], out->block_indices[h], w.keys, w.minpos, (const uint32_t*)w.local,
+             w.table_size - 1, w.slot_of);
 }
 
-helios_status sample_launch(helios_graph* g, SampleWS& w, const int64_t* seeds, int64_t B_max, const int32_t* fanouts,
-                            int32_t L, const helios_blocks* out, cudaStream_t st) {
+helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const int32_t* fanouts, int32_t L,
+                            const helios_blocks* out, cudaStream_t st) {
   int64_t maxn, lvl[HELIOS_MAX_HOPS + 1], edg[HELIOS_MAX_HOPS];
   helios_status s = sample_bounds(B_max, fanouts, L, g->V, g->E, &maxn, lvl, edg);
   if (s != HELIOS_OK) return s;
   const uint32_t mask = w.table_size - 1;
-  HCUDA(cudaMemsetAsync(w.reset_base, 0xFF, w.reset_bytes, st));
-  k_insert_seeds<<<(int)std::max<int64_t>(1, (B_max + 255) / 256), 256, 0, st>>>(
-      seeds, w.d_params, g->V, w.keys, w.local, mask, out->nodes, out->level_counts, g->d_err);
+  HCUDA(cudaMemsetAsync(w.scan_base, 0xFF, w.scan_bytes, st));
+  if (L == 0)
+    k_insert_seeds<<<(int)std::max<int64_t>(1, (B_max + 255) / 256), 256, 0, st>>>(
+        w.d_params, g->V, w.keys, w.local, mask, out->nodes, w.node_slot, out->level_counts, g->d_err);
   for (int h = 0; h < L; h++) {
     const int32_t f = fanouts[h];
-    const int rt = (int)std::max<int64_t>(1, (lvl[h] + kScanTile - 1) / kScanTile);
-    k_row_count_scan<<<rt, kScanBlock, 0, st>>>(out->nodes, out->level_counts, h, g->indptr, g->V, f,
-                                                out->block_indptr[h], out->edge_counts, w.row_scan[h],
-                                                h > 0 ? out->block_indices[h - 1] : nullptr, w.slot_of, w.local);
+    // persistent tile loops: a grid of at most one CTA per SM, tiles taken by ticket
+    const int rt = (int)std::min<int64_t>(std::max<int64_t>(1, (lvl[h] + kScanTile - 1) / kScanTile), g->sms);
+    if (h == 0)
+      k_seed_count_scan<<<rt, kScanBlock, 0, st>>>(w.d_params, g->indptr, g->V, f, out->block_indptr[0],
+                                                   out->edge_counts, out->level_counts, w.row_scan[0], w.keys,
+                                                   w.local, mask, out->nodes, w.node_slot, g->d_err);
+    else
+      launch_pdl(k_row_count_scan, dim3(rt), dim3(kScanBlock), st, (const int64_t*)out->nodes,
+                 (const int64_t*)out->level_counts, h, (const int64_t*)g->indptr, g->V, f, out->block_indptr[h],
+                 out->edge_counts, w.row_scan[h], out->block_indices[h - 1], (const uint32_t*)w.slot_of,
+                 (const uint32_t*)w.local);
     if (f < 0 || f > 16) launch_fill<32>(g, w, out, h, lvl[h], f, st);
     else if (f > 8) launch_fill<16>(g, w, out, h, lvl[h], f, st);
     else if (f > 4) launch_fill<8>(g, w, out, h, lvl[h], f, st);
     else launch_fill<4>(g, w, out, h, lvl[h], f, st);
-    const int et = (int)std::max<int64_t>(1, (edg[h] + kScanTile - 1) / kScanTile);
-    k_dedup_assign<<<et, kScanBlock, 0, st>>>(out->edge_counts, h, w.slot_of, w.keys, w.minpos, w.local, out->nodes,
-                                              out->level_counts, w.edge_scan[h]);
+    const int et = (int)std::min<int64_t>(std::max<int64_t>(1, (edg[h] + kScanTile - 1) / kScanTile), g->sms);
+    launch_pdl(k_dedup_assign, dim3(et), dim3(kScanBlock), st, (const int64_t*)out->edge_counts, h,
+               (const uint32_t*)w.slot_of, (const uint32_t*)w.keys, (const uint32_t*)w.minpos, w.local, out->nodes,
+               out->level_counts, w.edge_scan[h], w.node_slot);
   }
   if (L > 0) {
-    const int ge = (int)std::min<int64_t>(std::max<int64_t>(1, (edg[L - 1] + 255) / 256), (int64_t)g->sms * 16);
-    k_relabel<<<ge, 256, 0, st>>>(out->block_indices[L - 1], out->edge_counts, L - 1, w.slot_of, w.local);
+    const int ge = (int)std::min<int64_t>(std::max<int64_t>(1, (edg[L - 1] + 255) / 256), (int64_t)g->sms * 2);
+    launch_pdl(k_relabel, dim3(ge), dim3(256), st, out->block_indices[L - 1], (const int64_t*)out->edge_counts, L - 1,
+               (const uint32_t*)w.slot_of, (const uint32_t*)w.local);
   }
+  const int gc = (int)std::min<int64_t>(std::max<int64_t>(1, (maxn + 255) / 256), (int64_t)g->sms * 2);
+  launch_pdl(k_table_clear, dim3(gc), dim3(256), st, (const int64_t*)(out->level_counts + L),
+             (const uint32_t*)w.node_slot, w.keys, w.minpos, w.local);
   HCUDA(cudaGetLastError());
   return HELIOS_OK;
 }

@@ -27,7 +27,7 @@ STATUS = ["OK", "E_INVALID", "E_RANGE", "E_CAPACITY", "E_NOMEM", "E_CUDA", "E_IO
 HOST_ALIAS, TABLE_MAPPED, NO_DIRECT_IO, IO_FAULT_AT = 0x1, 0x2, 0x4, 0x100
 HOST_FILL, HOST_TIER_MAPPED = 0x8, 0x10
 PLAN_NO_GRAPH = 0x1
-SUBMIT_SEEDS_HOST = 0x1
+SUBMIT_SEEDS_HOST, SUBMIT_TIMING = 0x1, 0x2
 
 i64, i32, u32, u64, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p
 
@@ -376,12 +376,14 @@ def helios_plan_create(g: Graph, c: Cache | None, B: int, fanouts, depth: int = 
     return Plan(h.value, g, c, B, fanouts, depth)
 
 
-def helios_plan_submit(p: Plan, slot: int, seeds, key: int, stream=None) -> None:
+def helios_plan_submit(p: Plan, slot: int, seeds, key: int, stream=None, timing: bool = False) -> None:
     if isinstance(seeds, torch.Tensor) and seeds.is_cuda:
         ptr, n, fl = seeds.data_ptr(), seeds.numel(), 0
     else:
         arr = np.ascontiguousarray(seeds, dtype=np.int64) if not isinstance(seeds, torch.Tensor) else seeds
         ptr, n, fl = _ptr(arr), len(arr), SUBMIT_SEEDS_HOST
+    if timing:
+        fl |= SUBMIT_TIMING
     _check(_lib.helios_plan_submit(p.handle, slot, ptr, n, key & (2**64 - 1), fl, _stream(stream)),
            "helios_plan_submit")
 

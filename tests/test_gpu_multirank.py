@@ -25,6 +25,8 @@ def _free_port():
 
 
 def _worker(rank, world, port, tag, q):
+    import faulthandler
+    faulthandler.dump_traceback_later(100, exit=True)
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -51,15 +53,18 @@ def _worker(rank, world, port, tag, q):
         Hr = int(0.1 * cfg.V)
         S = cfg.V - world * Hr
         name = f"helios_mr_{tag}"
-        tier, m = hd.shared_array(name, (S * cfg.R,), np.uint8, create=(rank == 0))
-        if rank == 0:
+        if rank == 0:   # creator first, then the others map it (after the barrier)
+            tier, m = hd.shared_array(name, (S * cfg.R,), np.uint8, create=True)
             c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=inp.table, world_size=world, rank=rank,
                                      host_tier=tier, flags=H.HOST_FILL)
         dist.barrier()
         if rank != 0:
+            tier, m = hd.shared_array(name, (S * cfg.R,), np.uint8, create=False)
             c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=inp.table, world_size=world, rank=rank,
                                      host_tier=tier)
+        print(f"[rank {rank}] cache built", file=sys.stderr, flush=True)
         hd.attach_peers(H, c)
+        print(f"[rank {rank}] peers attached", file=sys.stderr, flush=True)
         dref, _ = oracle.cache_dir(hot_cpu.numpy().astype(np.uint64), world, Hr, S)
         p = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=2)
         keys = workloads.batch_keys(0, len(inp.batches))
@@ -78,6 +83,7 @@ def _worker(rank, world, port, tag, q):
             st = stats.cpu().tolist()
             ok &= st == oracle.lookup_counts(dref, orc.nodes, rank).tolist()
             peer_rows += st[1]
+        print(f"[rank {rank}] batches done", file=sys.stderr, flush=True)
         dist.barrier()
         p.free()
         c.free()
@@ -98,7 +104,7 @@ def test_two_ranks_one_gpu():
     ps = [ctx.Process(target=_worker, args=(r, 2, port, tag, q)) for r in range(2)]
     for p in ps:
         p.start()
-    res = [q.get(timeout=280) for _ in ps]
+    res = [q.get(timeout=150) for _ in ps]
     for p in ps:
         p.join(timeout=60)
         assert p.exitcode == 0

@@ -64,14 +64,15 @@ def test_plan_c1_epoch(H, c1, depth, flags, host_seeds):
         idx = list(range(start, min(nb, start + depth)))
         for k, b in enumerate(idx):
             seeds = c1.batches[b] if host_seeds else torch.as_tensor(c1.batches[b]).cuda()
-            H.helios_plan_submit(p, k, seeds, keys[b], stream)
+            H.helios_plan_submit(p, k, seeds, keys[b], stream, timing=(b % 2 == 0))
         for k, b in enumerate(idx):
             H.helios_plan_wait(p, k, stream)
         H.helios_sync(c)
         for k, b in enumerate(idx):
             check_slot(p, k, c1, c1.batches[b], keys[b], dref)
-        s_ms, g_ms = H.helios_plan_timing(p, 0)
-        assert s_ms > 0 and g_ms > 0
+        if depth > 1 or start % 2 == 0:
+            s_ms, g_ms = H.helios_plan_timing(p, 0)
+            assert s_ms > 0 and g_ms > 0
     p.free()
     c.free()
 
