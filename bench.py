@@ -135,27 +135,56 @@ def pcie_h2d_peak(torch, nbytes: int = 1 << 30) -> float:
     return nbytes / best / 1e6
 
 
-def pick_scale(cfg: workloads.Config, world: int) -> float:
-    """Capacity rule: shrink V, E by s if host RAM cannot hold the canonical table."""
+def has_file_tier(cfg: workloads.Config) -> bool:
+    return cfg.hbm_frac + cfg.host_frac < 1.0
+
+
+def keeps_table(cfg: workloads.Config) -> bool:
+    """The canonical host table is kept when it is small or the tiers are HBM+host only; file-tier
+    configs at scale read their tier contents (and the oracle its rows) from the feature file."""
+    return (not has_file_tier(cfg)) or cfg.V * cfg.R < (8 << 30)
+
+
+def pick_scale(cfg: workloads.Config, world: int, workdir: str = "/tmp") -> float:
+    """Capacity rule: shrink V, E by s if host RAM (canonical table, packed host tier,
+    CSR) or free disk (feature file) cannot hold the config."""
+    import shutil
     try:
         avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
-    except Exception:
+    except (ValueError, OSError):
         return 1.0
-    need = cfg.V * cfg.R + cfg.E * 4 * 3 + cfg.V * 8 * 4
-    return 1.0 if need < 0.8 * avail else max(0.01, math.floor(0.8 * avail / need * 100) / 100)
+    ram = cfg.V * cfg.R * ((1.0 if keeps_table(cfg) else 0.0) + cfg.host_frac) + cfg.E * 4 * 3 + cfg.V * 8 * 4
+    s = 1.0 if ram < 0.7 * avail else 0.7 * avail / ram
+    if has_file_tier(cfg):
+        stride = (cfg.R + 511) // 512 * 512
+        free = shutil.disk_usage(workdir).free
+        s = min(s, 0.6 * free / (cfg.V * stride))
+    return 1.0 if s >= 1.0 else max(0.01, math.floor(s * 100) / 100)
+
+
+def file_peak(path: str, stride: int, header: int, threads: int, secs: float = 3.0) -> dict:
+    """Random O_DIRECT reads of `stride` bytes with the IO workers' thread count (tools/filebench)."""
+    exe = os.path.join(ROOT, "tools", "filebench")
+    if not os.path.exists(exe):
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-pthread", "-o", exe, exe + ".cpp"])
+    out = subprocess.check_output([exe, path, str(stride), str(threads), str(secs), str(header)], text=True)
+    return json.loads(out)
 
 
 # ---------------------------------------------------------------------------------------------
 
-def run_oracle_baseline(inp, keys, budget_s: float, check=None) -> dict:
-    """The oracle as it stands (single-threaded C++), on a bounded sample of the same batches."""
+def run_oracle_baseline(inp, keys, budget_s: float, check=None, dir_=None) -> dict:
+    """The oracle as it stands (single-threaded C++), on a bounded sample of the same batches.
+    Rows come from the canonical host table, or by pread from the feature file when the config
+    keeps no table (a CPU-managed cache)."""
     import oracle
     cfg = inp.cfg
     t0 = time.perf_counter()
     done, rows = 0, 0
     for b, (seeds, key) in enumerate(zip(inp.batches, keys)):
         ob = oracle.sample(inp.graph.indptr, inp.graph.indices, seeds, cfg.fanouts, key)
-        feats = oracle.gather(ob.nodes, cfg.R, table=inp.table)
+        feats = oracle.gather(ob.nodes, cfg.R, table=inp.table, path=inp.feature_path, header=inp.header,
+                              stride=inp.stride, dir_=dir_)
         if check is not None:
             check(b, ob, feats)
         done += 1
@@ -181,13 +210,17 @@ def main():
     ap.add_argument("--depth", type=int, default=6, help="batches in flight (plan slots)")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly instead of CUDA graphs")
     ap.add_argument("--host-alias", action="store_true", help="host tier = canonical table by id (no packed copy)")
+    ap.add_argument("--io-rings", type=int, default=8, help="SQ/CQ ring pairs = host IO worker threads")
+    ap.add_argument("--ring-depth", type=int, default=256)
+    ap.add_argument("--io-ctas", type=int, default=32, help="CTA budget of each IO kernel (PAPER.md:244)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg0 = workloads.CONFIGS[args.config]
-    s = args.scale if args.scale > 0 else pick_scale(cfg0, world)
+    workdir = os.environ.get("HELIOS_BENCH_DIR", "/tmp")
+    s = args.scale if args.scale > 0 else pick_scale(cfg0, world, workdir)
     cfg = workloads.scaled(cfg0, s)
 
     if args.impl == "reference":
@@ -226,22 +259,32 @@ def main():
     t_setup = time.time()
     shm = f"helios_bench_{os.getppid()}" if world > 1 else None
     tab_bytes = cfg.V * cfg.R
+    file_cfg = has_file_tier(cfg)
+    fdir = os.path.join(workdir, f"helios_bench_{os.getppid() if world > 1 else os.getpid()}")
     if rank == 0:
-        buf = host_buffer(tab_bytes, f"{shm}_feat" if shm else None, create=True)
-        table = np.frombuffer(buf, dtype=np.float32).reshape(cfg.V, cfg.dim)
-        inp = workloads.make_inputs(cfg, table=True, table_buffer=table)
+        if keeps_table(cfg):
+            buf = host_buffer(tab_bytes, f"{shm}_feat" if shm else None, create=True)
+            table = np.frombuffer(buf, dtype=np.float32).reshape(cfg.V, cfg.dim)
+        else:
+            table = None
+        if file_cfg:
+            os.makedirs(fdir, exist_ok=True)
+        inp = workloads.make_inputs(cfg, table=table is not None, table_buffer=table, file=file_cfg, workdir=fdir)
         if world > 1:
             np.save(f"/dev/shm/{shm}_indptr.npy", inp.graph.indptr)
             np.save(f"/dev/shm/{shm}_indices.npy", inp.graph.indices)
     if world > 1:
         dist.barrier()
         if rank != 0:
-            buf = host_buffer(tab_bytes, f"{shm}_feat", create=False)
-            table = np.frombuffer(buf, dtype=np.float32).reshape(cfg.V, cfg.dim)
+            table = None
+            if keeps_table(cfg):
+                buf = host_buffer(tab_bytes, f"{shm}_feat", create=False)
+                table = np.frombuffer(buf, dtype=np.float32).reshape(cfg.V, cfg.dim)
             gr = synth.Graph(cfg.V, np.load(f"/dev/shm/{shm}_indptr.npy", mmap_mode="r"),
                              np.load(f"/dev/shm/{shm}_indices.npy", mmap_mode="r"))
             train = synth.train_set(cfg.V, workloads.SEED, cfg.train_pct)
-            inp = workloads.Inputs(cfg, gr, table, None, 0, 0, train,
+            path = os.path.join(fdir, f"features_{cfg.name}.bin") if file_cfg else None
+            inp = workloads.Inputs(cfg, gr, table, path, 4096, (cfg.R + 511) // 512 * 512, train,
                                    synth.epoch_batches(train, cfg.B, 0, workloads.SEED))
     gen_s = time.time() - t_setup
     log(f"inputs {cfg.name}: V={cfg.V} E={inp.graph.E} dim={cfg.dim} gen {gen_s:.1f}s")
@@ -259,27 +302,30 @@ def main():
     allreduce(hot)
     presample_s = time.time() - t1
     Hr, S = workloads.tier_rows(cfg, world)
-    S = max(0, min(S, cfg.V - world * Hr)) if cfg.host_frac + cfg.hbm_frac >= 1.0 else S
     if cfg.hbm_frac + cfg.host_frac >= 1.0:
         S = max(0, cfg.V - world * Hr)
+    else:
+        S = max(0, min(S, cfg.V - world * Hr))
     t2 = time.time()
-    if args.host_alias or S == 0:
+    fkw = dict(feature_path=inp.feature_path, header_bytes=inp.header, file_stride=inp.stride,
+               io_rings=args.io_rings, ring_depth=args.ring_depth, io_ctas=args.io_ctas) if file_cfg else {}
+    if (args.host_alias and table is not None) or S == 0:
         c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
-                                 flags=H.HOST_ALIAS)
+                                 flags=H.HOST_ALIAS if S else 0, **fkw)
     elif world == 1:   # packed host tier in hot-rank order, pinned by the library
-        c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table)
+        c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, **fkw)
     else:              # one packed host tier shared by all ranks (/dev/shm), filled by rank 0
         if rank == 0:  # creator first; the other ranks map the filled tier after the barrier
             tier_buf = host_buffer(S * cfg.R, f"{shm}_tier", create=True)
             tier = np.frombuffer(tier_buf, dtype=np.uint8)
             c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
-                                     host_tier=tier, flags=H.HOST_FILL)
+                                     host_tier=tier, flags=H.HOST_FILL, **fkw)
         dist.barrier()
         if rank != 0:
             tier_buf = host_buffer(S * cfg.R, f"{shm}_tier", create=False)
             tier = np.frombuffer(tier_buf, dtype=np.uint8)
             c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
-                                     host_tier=tier)
+                                     host_tier=tier, **fkw)
     if world > 1:
         hdist.attach_peers(H, c)
         dist.barrier()
@@ -396,15 +442,21 @@ def main():
             for h in range(L):
                 ok &= np.array_equal(got["block_indptr"][h], ob.block_indptr[h])
                 ok &= np.array_equal(got["block_indices"][h], ob.block_indices[h])
-            ref = oracle.gather(ob.nodes, cfg.R, table=table)
+            ref = oracle.gather(ob.nodes, cfg.R, table=table, path=inp.feature_path, header=inp.header,
+                                stride=inp.stride)
             ok &= np.array_equal(feats[: len(ob.nodes)].cpu().numpy(), ref)
             checked += 1
         parity = {"batches": checked, "bit_exact": bool(ok), "checks": "nodes, block CSR, feature bytes"}
         if not args.no_cpu_baseline:
-            r = run_oracle_baseline(inp, keys, args.cpu_budget)
+            dir_host = None
+            if file_cfg:   # CPU-managed cache: FILE-tier rows by pread, the rest from memory
+                dir_host = H.device_view(c.info().dir, cfg.V, torch.int64).cpu().numpy()
+            r = run_oracle_baseline(inp, keys, args.cpu_budget, dir_=dir_host)
             cpu = {"value": round(r["value"], 4), "unit": "batches/s", "cores": 1, "kind": "oracle",
                    "sample": f"{r['batches']} batches of {cfg.name} (first of epoch 0), single-threaded C++ oracle "
-                             f"sample+gather from the canonical host table, {r['seconds']:.1f}s",
+                             f"sample+gather ({'FILE-tier rows by buffered pread, ' if file_cfg else ''}"
+                             f"{'other rows from the canonical host table' if table is not None else 'rows by pread from the feature file'}), "
+                             f"{r['seconds']:.1f}s",
                    "feature_gbs": round(r["gbs"], 3)}
 
     # ---- roofline of the dominant kernel (lookup+gather, K3/K4) ----
@@ -419,13 +471,17 @@ def main():
     hbm_bytes = R * n_local + R * nL + 16 * nL         # tier read + output write + nodes/dir reads
     pcie_bytes = R * (n_host + n_file)
     nvl_bytes = R * n_peer
+    stor_bytes = inp.stride * n_file if file_cfg else 0.0
+    fpk = file_peak(inp.feature_path, inp.stride, inp.header, args.io_rings) if (file_cfg and rank == 0) else None
+    bw_file = fpk["gbs"] if fpk else 1.0
     g_ms = statistics.mean(gather_ms)
-    t_roof_ms = (hbm_bytes / bw_hbm + pcie_bytes / max(bw_pcie, 1e-9) + nvl_bytes / bw_nvl) / 1e6
-    alg_bytes = hbm_bytes + pcie_bytes + nvl_bytes
+    terms = {"hbm": hbm_bytes / bw_hbm, "pcie": pcie_bytes / max(bw_pcie, 1e-9), "nvlink": nvl_bytes / bw_nvl,
+             "storage": stor_bytes / bw_file}
+    t_roof_ms = sum(terms.values()) / 1e6
+    alg_bytes = hbm_bytes + pcie_bytes + nvl_bytes + stor_bytes
     achieved = alg_bytes / (g_ms * 1e6)
     peak_eff = alg_bytes / (t_roof_ms * 1e6)
-    dominant = max((("hbm", hbm_bytes / bw_hbm), ("pcie", pcie_bytes / max(bw_pcie, 1e-9)), ("nvlink", nvl_bytes / bw_nvl)),
-                   key=lambda x: x[1])[0]
+    dominant = max(terms.items(), key=lambda x: x[1])[0]
     value = world * steps / (max_ms / 1e3)
     e2e_val = world * steps / e2e_s
     launches_per_step = 3 * L + 2 + 2 + (3 if c.info().file_rows > 0 else 0)
@@ -436,6 +492,9 @@ def main():
         "dtype": "int64 ids / fp32 feature bytes (u8 copy)",
         "data": "synthetic (seeded R-MAT-marginal power-law graph, synth_feature rows; no datasets)",
         "config": {"workload": cfg.name, "desc": cfg.note, "V": cfg.V, "E": int(inp.graph.E), "dim": cfg.dim,
+                   "file_tier": {"rows": int(c.info().file_rows), "direct_io": bool(c.info().direct_io),
+                                 "io_rings": args.io_rings, "ring_depth": args.ring_depth, "io_ctas": args.io_ctas}
+                   if file_cfg else None,
                    "batch_per_rank": cfg.B, "fanouts": cfg.fanouts, "hbm_rows_per_gpu": Hr, "host_rows": S,
                    "scale": s, "parallelism": f"dp{world} (seeds split per rank, HBM tier sharded)",
                    "host_tier": "alias of canonical table (by id)" if args.host_alias else "packed, hot-rank order",
@@ -452,9 +511,14 @@ def main():
                      "traffic": None,
                      "peaks_used": {"hbm_gbs": bw_hbm, "hbm_src": "MEASURED_PEAKS.json" if pk else "fallback",
                                     "pcie_gbs": round(bw_pcie, 2), "pcie_src": "pinned H2D copy measured in this run",
-                                    "nvlink_gbs": bw_nvl},
-                     "bytes_per_launch": {"hbm": round(hbm_bytes), "pcie": round(pcie_bytes), "nvlink": round(nvl_bytes)},
-                     "t_roof_ms": round(t_roof_ms, 4)},
+                                    "nvlink_gbs": bw_nvl, "file_gbs": round(bw_file, 4) if fpk else None,
+                                    "file_src": f"tools/filebench random {inp.stride} B O_DIRECT={fpk['direct']} x{args.io_rings} threads" if fpk else None},
+                     "bytes_per_launch": {"hbm": round(hbm_bytes), "pcie": round(pcie_bytes), "nvlink": round(nvl_bytes),
+                                          "storage": round(stor_bytes)},
+                     "t_roof_ms": round(t_roof_ms, 4),
+                     "frac_throughput": round(t_roof_ms / (max_ms / steps), 4),
+                     "note": "frac = T_roof / mean per-launch gather time (CUDA events, batches overlapping); "
+                             "frac_throughput = T_roof / ms_per_step (whole-path throughput vs the tier roofline)"},
         "e2e": {"value": round(e2e_val, 3), "unit": "batches/s", "h2d_bytes_per_step": cfg.B * 8,
                 "d2h_bytes_per_step": (L + 1 + 4) * 8},
         "gpu_launches": launches_per_step * steps,
@@ -468,6 +532,9 @@ def main():
     plan.free()
     c.free()
     g.free()
+    if file_cfg and rank == 0:
+        import shutil
+        shutil.rmtree(fdir, ignore_errors=True)
     if world > 1:
         dist.barrier()
         if rank == 0:
@@ -485,23 +552,30 @@ def reference_arm(args, cfg, rank, world):
         return
     import oracle
     t0 = time.time()
-    inp = workloads.make_inputs(cfg, table=True)
+    file_cfg = has_file_tier(cfg)
+    fdir = os.path.join(os.environ.get("HELIOS_BENCH_DIR", "/tmp"), f"helios_ref_{os.getpid()}")
+    if file_cfg:
+        os.makedirs(fdir, exist_ok=True)
+    inp = workloads.make_inputs(cfg, table=keeps_table(cfg), file=file_cfg and not keeps_table(cfg), workdir=fdir)
     gen_s = time.time() - t0
     keys = workloads.batch_keys(0, len(inp.batches))
     full = [b for b in inp.batches if len(b) == cfg.B]
     L = len(cfg.fanouts)
     for i in range(args.warmup):
         ob = oracle.sample(inp.graph.indptr, inp.graph.indices, full[i % len(full)], cfg.fanouts, keys[i % len(full)])
-        oracle.gather(ob.nodes, cfg.R, table=inp.table)
+        oracle.gather(ob.nodes, cfg.R, table=inp.table, path=inp.feature_path, header=inp.header, stride=inp.stride)
     t1 = time.perf_counter()
     rows = 0
     for i in range(args.steps):
         b = (args.warmup + i) % len(full)
         ob = oracle.sample(inp.graph.indptr, inp.graph.indices, full[b], cfg.fanouts, keys[b])
-        oracle.gather(ob.nodes, cfg.R, table=inp.table)
+        oracle.gather(ob.nodes, cfg.R, table=inp.table, path=inp.feature_path, header=inp.header, stride=inp.stride)
         rows += len(ob.nodes)
     dt = time.perf_counter() - t1
     v = args.steps / dt
+    if file_cfg:
+        import shutil
+        shutil.rmtree(fdir, ignore_errors=True)
     print(json.dumps({
         "impl": "reference", "metric": "sampled+gathered mini-batches/sec (feature GB/s and tier-roofline fraction alongside)",
         "value": round(v, 4), "unit": "batches/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
