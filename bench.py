@@ -83,7 +83,15 @@ class ClockSampler:
         self.device = device
         self.proc = None
 
+    def _oneshot(self):
+        try:
+            return subprocess.check_output(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                            "--format=csv,noheader,nounits"], text=True, timeout=10).strip()
+        except Exception:
+            return ""
+
     def __enter__(self):
+        self.first = ""
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
@@ -94,6 +102,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         self.lines = []
+        last = self._oneshot()
         if self.proc:
             self.proc.terminate()
             try:
@@ -101,6 +110,8 @@ class ClockSampler:
                 self.lines = [l for l in out.splitlines() if l.strip()]
             except Exception:
                 pass
+        if last:
+            self.lines.append(last)
 
     def summary(self) -> dict:
         sm, mx, reasons = [], None, set()
@@ -117,6 +128,18 @@ class ClockSampler:
                 continue
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+def traffic_of(name: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")
+    try:
+        d = json.load(open(p)).get(name)
+    except (OSError, ValueError):
+        return None
+    if not d:
+        return None
+    return round(d["dram_bytes_read_per_launch"] + d["dram_bytes_write_per_launch"])
 
 
 def pcie_h2d_peak(torch, nbytes: int = 1 << 30) -> float:
@@ -198,8 +221,8 @@ def run_oracle_baseline(inp, keys, budget_s: float, check=None, dir_=None) -> di
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="C3")
     ap.add_argument("--scale", type=float, default=0.0, help="V,E scale factor (0 = auto from host RAM)")
     ap.add_argument("--impl", default="helios", choices=["helios", "reference"])
@@ -508,7 +531,7 @@ def main():
                            "host": round(n_host, 1), "file": round(n_file, 1)},
         "roofline": {"bound": dominant, "kernel": "k_lookup + k_gather_lists (K3+K4)", "achieved": round(achieved, 2),
                      "peak": round(peak_eff, 2), "unit": "GB/s", "frac": round(t_roof_ms / g_ms, 4),
-                     "traffic": None,
+                     "traffic": traffic_of(cfg.name),
                      "peaks_used": {"hbm_gbs": bw_hbm, "hbm_src": "MEASURED_PEAKS.json" if pk else "fallback",
                                     "pcie_gbs": round(bw_pcie, 2), "pcie_src": "pinned H2D copy measured in this run",
                                     "nvlink_gbs": bw_nvl, "file_gbs": round(bw_file, 4) if fpk else None,
