@@ -234,6 +234,9 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly instead of CUDA graphs")
     ap.add_argument("--host-alias", action="store_true", help="host tier = canonical table by id (no packed copy)")
     ap.add_argument("--io-rings", type=int, default=8, help="SQ/CQ ring pairs = host IO worker threads")
+    ap.add_argument("--host-staged", type=float, default=0.0,
+                    help="share of host-tier rows copied by host stager threads (0 = pure zero-copy)")
+    ap.add_argument("--stage-workers", type=int, default=8)
     ap.add_argument("--ring-depth", type=int, default=256)
     ap.add_argument("--io-ctas", type=int, default=32, help="CTA budget of each IO kernel (PAPER.md:244)")
     args = ap.parse_args()
@@ -332,23 +335,26 @@ def main():
     t2 = time.time()
     fkw = dict(feature_path=inp.feature_path, header_bytes=inp.header, file_stride=inp.stride,
                io_rings=args.io_rings, ring_depth=args.ring_depth, io_ctas=args.io_ctas) if file_cfg else {}
+    if args.host_staged > 0:
+        fkw.update(stage_workers=args.stage_workers, stage_frac=args.host_staged)
+    sflag = H.HOST_STAGED if args.host_staged > 0 else 0
     if (args.host_alias and table is not None) or S == 0:
         c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
-                                 flags=H.HOST_ALIAS if S else 0, **fkw)
+                                 flags=(H.HOST_ALIAS if S else 0) | sflag, **fkw)
     elif world == 1:   # packed host tier in hot-rank order, pinned by the library
-        c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, **fkw)
+        c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, flags=sflag, **fkw)
     else:              # one packed host tier shared by all ranks (/dev/shm), filled by rank 0
         if rank == 0:  # creator first; the other ranks map the filled tier after the barrier
             tier_buf = host_buffer(S * cfg.R, f"{shm}_tier", create=True)
             tier = np.frombuffer(tier_buf, dtype=np.uint8)
             c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
-                                     host_tier=tier, flags=H.HOST_FILL, **fkw)
+                                     host_tier=tier, flags=H.HOST_FILL | sflag, **fkw)
         dist.barrier()
         if rank != 0:
             tier_buf = host_buffer(S * cfg.R, f"{shm}_tier", create=False)
             tier = np.frombuffer(tier_buf, dtype=np.uint8)
             c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
-                                     host_tier=tier, **fkw)
+                                     host_tier=tier, flags=sflag, **fkw)
     if world > 1:
         hdist.attach_peers(H, c)
         dist.barrier()
@@ -520,7 +526,9 @@ def main():
                    if file_cfg else None,
                    "batch_per_rank": cfg.B, "fanouts": cfg.fanouts, "hbm_rows_per_gpu": Hr, "host_rows": S,
                    "scale": s, "parallelism": f"dp{world} (seeds split per rank, HBM tier sharded)",
-                   "host_tier": "alias of canonical table (by id)" if args.host_alias else "packed, hot-rank order",
+                   "host_tier": ("alias of canonical table (by id)" if args.host_alias else "packed, hot-rank order")
+                   + (f"; {args.host_staged:.0%} of host rows staged by {args.stage_workers} host threads"
+                      if args.host_staged > 0 else "; GPU zero-copy reads"),
                    "batches_in_flight": depth, "cuda_graphs": not args.no_graph,
                    "l2": "inputs larger than L2 (CSR %.1f GB, feature table %.1f GB); no flush" % (
                        (inp.graph.E * 4 + cfg.V * 8) / 1e9, cfg.V * R / 1e9)},

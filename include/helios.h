@@ -146,6 +146,8 @@ helios_status helios_presample(helios_graph* g, const int64_t* seeds, int64_t n_
 #define HELIOS_CACHE_NO_DIRECT_IO 0x4u   /* open feature_path without O_DIRECT                    */
 #define HELIOS_CACHE_HOST_FILL 0x8u      /* fill the caller-provided host_tier (else assumed filled) */
 #define HELIOS_CACHE_HOST_TIER_MAPPED 0x10u /* caller-provided host_tier already registered + mapped */
+#define HELIOS_CACHE_HOST_STAGED 0x20u  /* split host-tier rows: a share is copied by host stager threads into
+                                           a contiguous pinned staging buffer read sequentially by the GPU */
 #define HELIOS_CACHE_IO_FAULT_AT 0x100u  /* test builds: IO workers fail the io_fault_at-th read  */
 
 typedef struct {
@@ -169,6 +171,8 @@ typedef struct {
                                  mapping used by every rank): row s = vertex at hot rank G*H + s.  Filled by
                                  the library iff HELIOS_CACHE_HOST_FILL; registered unless HOST_TIER_MAPPED.
                                  NULL: the library allocates (pinned) and fills it.  Ignored with HOST_ALIAS. */
+  int32_t stage_workers;      /* HOST_STAGED: host stager threads (0 = 8)                                */
+  float stage_frac;           /* HOST_STAGED: share of each batch's host rows staged by the CPU (0 = 0.6) */
 } helios_cache_desc;
 
 /* Builds the directory and fills the tiers (blocking).  The HBM tier is filled from host_table

@@ -234,6 +234,9 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
   c->header = d->header_bytes;
   c->stride = d->file_stride > 0 ? d->file_stride : c->R;
   c->io_ctas = d->io_ctas > 0 ? d->io_ctas : 32;
+  c->staged = (d->flags & HELIOS_CACHE_HOST_STAGED) != 0;
+  c->stage_workers = d->stage_workers > 0 ? d->stage_workers : 8;
+  c->stage_frac = d->stage_frac > 0.f ? std::min(d->stage_frac, 1.0f) : 0.6f;
   const int64_t V = c->V;
   // clamp tiers to V
   const int64_t GH = std::min<int64_t>((int64_t)c->G * c->H, V);
@@ -369,6 +372,11 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
     st = io_start(c, d);
     if (st != HELIOS_OK) return st;
   }
+  c->staged = c->staged && c->S > 0;
+  if (c->staged) {
+    st = stager_start(c);
+    if (st != HELIOS_OK) return st;
+  }
   return HELIOS_OK;
 }
 
@@ -376,6 +384,7 @@ void cache_free_impl(helios_cache* c) {
   cudaDeviceSynchronize();
   io_stop(c);
   gws_free(c->gws);
+  stager_stop(c);
   for (int r = 0; r < HELIOS_MAX_RANKS; r++)
     if (r != c->rank && c->peer_ptrs[r]) cudaIpcCloseMemHandle(c->peer_ptrs[r]);
   if (c->host_registered) cudaHostUnregister((void*)c->host_table);

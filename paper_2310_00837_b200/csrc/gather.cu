@@ -25,11 +25,17 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
   return r;
 }
 
+// Base pointers of the four tier lists (the host list is in pinned memory in staged mode).
+struct ListPtrs {
+  int64_t* i[kLists];
+  uint64_t* w[kLists];
+};
+
 // K3: one thread per row of N_L: dir[v] -> tier list (local HBM / peer HBM / host / file), appended
 // with warp-aggregated atomics.  The list counts are the per-tier row counts.
 __global__ void __launch_bounds__(256) k_lookup(const int64_t* __restrict__ nodes, const int64_t* __restrict__ n_nodes,
-                                                const int64_t* __restrict__ dir, int32_t rank, int64_t* __restrict__ li,
-                                                uint64_t* __restrict__ lw, int64_t cap, unsigned long long* ctl) {
+                                                const int64_t* __restrict__ dir, int32_t rank, ListPtrs L,
+                                                unsigned long long* ctl) {
   pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t n = *n_nodes;
@@ -53,21 +59,47 @@ __global__ void __launch_bounds__(256) k_lookup(const int64_t* __restrict__ node
         b = __shfl_sync(0xFFFFFFFFu, b, leader);
         if (t == q) {
           const int64_t pos = (int64_t)b + __popc(m & ((1u << lane) - 1u));
-          li[q * cap + pos] = i;
-          lw[q * cap + pos] = w;
+          L.i[q][pos] = i;
+          L.w[q][pos] = w;
         }
       }
     }
   }
 }
 
+__device__ __forceinline__ void st_release_sys_u32_(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Staged mode: split this batch's host rows between the zero-copy path [0, n_gpu) and the host
+// stagers [n_gpu, n_host), then post the mailbox {seq, n_host, n_gpu, n_stage} (release, system).
+__global__ void k_stage_publish(unsigned long long* ctl, uint32_t* seq_ctr, uint32_t* mail, float frac,
+                                int64_t stage_cap) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t n_host = (int64_t)ctl[kListHost];
+  const int64_t n_stage = min((int64_t)((double)n_host * frac), stage_cap);
+  const int64_t n_gpu = n_host - n_stage;
+  const uint32_t seq = *seq_ctr + 1u;
+  *seq_ctr = seq;
+  ctl[kCtlStageGpu] = (unsigned long long)n_gpu;
+  ctl[kCtlStageSeq] = seq;
+  mail[1] = (uint32_t)n_host;
+  mail[2] = (uint32_t)n_gpu;
+  mail[3] = (uint32_t)n_stage;
+  __threadfence_system();
+  st_release_sys_u32_(&mail[0], seq);
+}
+
 struct GatherArgs {
   char* out;
   int32_t R;
-  const int64_t* li;
-  const uint64_t* lw;
-  int64_t cap;
+  ListPtrs L;
   const unsigned long long* ctl;
+  bool staged;
+  const char* stage;        // device alias of the pinned staging rows
+  const uint32_t* done;     // device alias of the per-chunk completion flags
+  int* err;
   const char* hbm;          // this rank's shard
   char* const* peers;       // device [G]
   const char* host_dev;     // device alias of the host tier
@@ -85,7 +117,7 @@ __device__ __forceinline__ void copy_rows(const GatherArgs& a, int q, int64_t j0
     for (int u = 0; u < U; u++) {
       src[u] = nullptr;
       if (j0 + u < cnt) {
-        const uint64_t w = a.lw[q * a.cap + j0 + u];
+        const uint64_t w = a.L.w[q][j0 + u];
         const int64_t slot = (int64_t)(w & ((1ull << 56) - 1));
         const char* base = q == kListLocal ? a.hbm : (q == kListPeer ? a.peers[(w >> 56) & 63] : a.host_dev);
         src[u] = (const int4*)(base + slot * a.R);
@@ -103,7 +135,7 @@ __device__ __forceinline__ void copy_rows(const GatherArgs& a, int q, int64_t j0
 #pragma unroll
     for (int u = 0; u < U; u++)
       if (src[u]) {
-        int4* d = (int4*)(a.out + a.li[q * a.cap + j0 + u] * (int64_t)a.R);
+        int4* d = (int4*)(a.out + a.L.i[q][j0 + u] * (int64_t)a.R);
 #pragma unroll
         for (int k = 0; k < VPL; k++) {
           const int idx = c0 + lane + 32 * k;
@@ -116,6 +148,21 @@ __device__ __forceinline__ void copy_rows(const GatherArgs& a, int q, int64_t j0
 // K4: warp-specialised gather.  When the host list is non-empty, one warp in 8 serves host rows
 // (zero-copy over PCIe, UH rows in flight per warp, so every host read is outstanding at once
 // and the link streams) while the others copy peer (NVLink) then local HBM rows.
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32_(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int4 ld_volatile_v4_(const int4* p) {
+  int4 r;
+  asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+constexpr uint64_t kStageWatchdogNs = 30ull * 1000000000ull;
+
 template <int VPL, int U, int UH>
 __global__ void __launch_bounds__(256, 4) k_gather_lists(GatherArgs a) {
   pdl_wait();
@@ -126,21 +173,51 @@ __global__ void __launch_bounds__(256, 4) k_gather_lists(GatherArgs a) {
   const int nvec = a.R >> 4;
   const int64_t n_local = (int64_t)a.ctl[kListLocal], n_peer = (int64_t)a.ctl[kListPeer],
                 n_host = (int64_t)a.ctl[kListHost];
+  const int64_t n_gpu = a.staged ? (int64_t)a.ctl[kCtlStageGpu] : n_host;
+  const int64_t n_stage = n_host - n_gpu;
   if (a.stats && gw == 0 && lane == 0) {
     a.stats->rows_hbm_local = n_local;
     a.stats->rows_hbm_peer = n_peer;
     a.stats->rows_host = n_host;
     a.stats->rows_file = (int64_t)a.ctl[kListFile];
   }
-  const bool split = n_host > 0;
-  const int64_t n_hw = split ? (nw + 7) / 8 : 0;
-  if (split && (gw & 7) == 0) {
-    const int64_t hw = gw >> 3;
-    for (int64_t j0 = hw * UH; j0 < n_host; j0 += n_hw * UH) copy_rows<VPL, UH>(a, kListHost, j0, n_host, lane, nvec);
+  // warp roles: r = gw % 8.  r == 0: zero-copy host rows [0, n_gpu); r == 1 (staged mode): stage
+  // consumers for rows [n_gpu, n_host); other warps: peer then local HBM rows.
+  const int nspecial = (n_host > 0) ? (a.staged ? 2 : 1) : 0;
+  const int r = (int)(gw & 7);
+  if (r < nspecial) {
+    const int64_t sw = gw >> 3, n_sw = nw >> 3;
+    if (r == 0) {
+      for (int64_t j0 = sw * UH; j0 < n_gpu; j0 += n_sw * UH) copy_rows<VPL, UH>(a, kListHost, j0, n_gpu, lane, nvec);
+    } else {
+      const uint32_t seq = (uint32_t)a.ctl[kCtlStageSeq];
+      const int64_t n_chunks = (n_stage + kStageChunk - 1) / kStageChunk;
+      const uint64_t t0 = globaltimer();
+      for (int64_t ch = sw; ch < n_chunks; ch += n_sw) {
+        bool ok = true;
+        while (ld_acquire_sys_u32_(&a.done[ch]) != seq) {  // every lane polls (one request)
+          if (globaltimer() - t0 > kStageWatchdogNs) {
+            ok = false;
+            break;
+          }
+          __nanosleep(200);
+        }
+        if (!__all_sync(0xFFFFFFFFu, ok)) {
+          if (lane == 0) latch(a.err, HELIOS_E_TIMEOUT);
+          return;
+        }
+        const int64_t j1 = min(n_stage, (ch + 1) * kStageChunk);
+        for (int64_t j = ch * kStageChunk; j < j1; j++) {
+          const int4* src = (const int4*)(a.stage + j * a.R);
+          int4* dst = (int4*)(a.out + a.L.i[kListHost][n_gpu + j] * (int64_t)a.R);
+          for (int k = lane; k < nvec; k += 32) dst[k] = ld_volatile_v4_(src + k);
+        }
+      }
+    }
     return;
   }
-  const int64_t dw = split ? gw - (gw >> 3) - 1 : gw;  // index among data warps
-  const int64_t n_dw = nw - n_hw;
+  const int64_t dw = (gw >> 3) * (8 - nspecial) + (r - nspecial);  // index among data warps
+  const int64_t n_dw = (nw >> 3) * (8 - nspecial);
   for (int64_t j0 = dw * U; j0 < n_peer; j0 += n_dw * U) copy_rows<VPL, U>(a, kListPeer, j0, n_peer, lane, nvec);
   for (int64_t j0 = dw * U; j0 < n_local; j0 += n_dw * U) copy_rows<VPL, U>(a, kListLocal, j0, n_local, lane, nvec);
 }
@@ -169,11 +246,6 @@ helios_status gather_rows_by_id(const char* src_dev, int32_t R, const int32_t* i
 
 // ---- IO rings --------------------------------------------------------------------------------
 
-__device__ __forceinline__ uint64_t globaltimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -328,14 +400,20 @@ static void launch_gather(const GatherArgs& a, int sms, cudaStream_t st) {
 }
 
 void gws_free(GatherWS& w) {
+  stager_unregister(w.owner, w);
   if (w.d_list_i) cudaFree(w.d_list_i);
   if (w.d_list_w) cudaFree(w.d_list_w);
   if (w.d_ctl) cudaFree(w.d_ctl);
+  if (w.h_host_i) cudaFreeHost(w.h_host_i);
+  if (w.h_host_w) cudaFreeHost(w.h_host_w);
+  if (w.h_stage) cudaFreeHost(w.h_stage);
+  if (w.h_done) cudaFreeHost(w.h_done);
+  if (w.h_mail) cudaFreeHost(w.h_mail);
+  if (w.d_seq) cudaFree(w.d_seq);
   w = GatherWS{};
 }
 
 helios_status gws_ensure(helios_cache* c, GatherWS& w, int64_t max_nodes) {
-  (void)c;
   if (w.d_ctl && max_nodes <= w.cap) return HELIOS_OK;
   HCUDA(cudaDeviceSynchronize());
   gws_free(w);
@@ -345,6 +423,26 @@ helios_status gws_ensure(helios_cache* c, GatherWS& w, int64_t max_nodes) {
   HCUDA(cudaMalloc(&w.d_ctl, kCtlWords * sizeof(unsigned long long)));
   HCUDA(cudaMemset(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long)));
   w.cap = cap;
+  w.owner = c;
+  if (c->staged) {
+    const int64_t chunks = kStageCapRows / kStageChunk + 1;
+    HCUDA(cudaHostAlloc(&w.h_host_i, cap * 8, cudaHostAllocMapped));
+    HCUDA(cudaHostAlloc(&w.h_host_w, cap * 8, cudaHostAllocMapped));
+    HCUDA(cudaHostAlloc(&w.h_stage, kStageCapRows * (int64_t)c->R, cudaHostAllocMapped));
+    HCUDA(cudaHostAlloc(&w.h_done, chunks * 4, cudaHostAllocMapped));
+    HCUDA(cudaHostAlloc(&w.h_mail, 16, cudaHostAllocMapped));
+    memset(w.h_done, 0, chunks * 4);
+    memset(w.h_mail, 0, 16);
+    HCUDA(cudaHostGetDevicePointer((void**)&w.d_host_i, w.h_host_i, 0));
+    HCUDA(cudaHostGetDevicePointer((void**)&w.d_host_w, w.h_host_w, 0));
+    HCUDA(cudaHostGetDevicePointer((void**)&w.d_stage, w.h_stage, 0));
+    HCUDA(cudaHostGetDevicePointer((void**)&w.d_done, w.h_done, 0));
+    HCUDA(cudaHostGetDevicePointer((void**)&w.d_mail, w.h_mail, 0));
+    HCUDA(cudaMalloc(&w.d_seq, 4));
+    HCUDA(cudaMemset(w.d_seq, 0, 4));
+    helios_status st = stager_register(c, w);
+    if (st != HELIOS_OK) return st;
+  }
   return HELIOS_OK;
 }
 
@@ -355,15 +453,28 @@ helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, 
   HCHECK(w.d_ctl && max_nodes <= w.cap, HELIOS_E_CAPACITY, "max_nodes %lld > gather list cap %lld",
          (long long)max_nodes, (long long)w.cap);
   HCUDA(cudaMemsetAsync(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long), st));
+  ListPtrs L;
+  for (int q = 0; q < kLists; q++) {
+    L.i[q] = w.d_list_i + q * w.cap;
+    L.w[q] = w.d_list_w + q * w.cap;
+  }
+  const bool staged = c->staged && w.d_host_i;
+  if (staged) {
+    L.i[kListHost] = w.d_host_i;
+    L.w[kListHost] = w.d_host_w;
+  }
   const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_nodes + 255) / 256), (int64_t)c->sms * 2);
-  k_lookup<<<lg, 256, 0, st>>>(nodes, n_nodes, c->dir, c->rank, w.d_list_i, w.d_list_w, w.cap, w.d_ctl);
+  k_lookup<<<lg, 256, 0, st>>>(nodes, n_nodes, c->dir, c->rank, L, w.d_ctl);
+  if (staged) launch_pdl(k_stage_publish, dim3(1), dim3(1), st, w.d_ctl, w.d_seq, w.d_mail, c->stage_frac, kStageCapRows);
   GatherArgs a;
   a.out = (char*)out;
   a.R = c->R;
-  a.li = w.d_list_i;
-  a.lw = w.d_list_w;
-  a.cap = w.cap;
+  a.L = L;
   a.ctl = w.d_ctl;
+  a.staged = staged;
+  a.stage = w.d_stage;
+  a.done = w.d_done;
+  a.err = c->d_err;
   a.hbm = c->hbm;
   a.peers = c->d_peers;
   a.host_dev = c->d_host_tier;

@@ -96,6 +96,9 @@ struct SampleWS {
   // [scan_base, scan_base + scan_bytes) is memset per batch.
   char* scan_base = nullptr;
   size_t scan_bytes = 0;
+  unsigned* bar = nullptr;      // persistent-sampler grid barrier {arrivals, generation} (in the scan region)
+  bool persistent = false;      // one cooperative kernel per batch instead of the 2+3L-kernel chain
+                                // (HELIOS_SAMPLE_PERSISTENT=1; measured slower)
   // per-batch parameters, read by the kernels from device memory so that a captured CUDA graph
   // can be replayed for every batch: [0] key, [1] n_seeds, [2] seeds device pointer, [3] reserved,
   // [4, 4 + cap_seeds) inline seeds (host-seed submits: one H2D copy carries parameters + seeds)
@@ -107,12 +110,31 @@ struct SampleWS {
 // Per-gather bookkeeping (one per gather context): per-tier work lists written by the lookup
 // kernel, and the ticket / count words shared with the gather and IO kernels.
 enum : int { kListLocal = 0, kListPeer = 1, kListHost = 2, kListFile = 3, kLists = 4 };
-enum : int { kCtlSubmit = 4, kCtlComplete = 5, kCtlWords = 8 };
+enum : int { kCtlSubmit = 4, kCtlComplete = 5, kCtlStageGpu = 6, kCtlStageSeq = 7, kCtlWords = 8 };
+constexpr int kStageChunk = 64;              // rows per staging chunk (one completion flag each)
+constexpr int64_t kStageCapRows = 1 << 16;   // staged rows per batch at most (the rest: zero-copy)
+struct StageCtx;
+struct Stager;
 struct GatherWS {
   int64_t cap = 0;                      // rows per list
   int64_t* d_list_i = nullptr;          // [kLists * cap] output row of each entry
   uint64_t* d_list_w = nullptr;         // [kLists * cap] directory word of each entry
-  unsigned long long* d_ctl = nullptr;  // [kCtlWords]: counts per list, then IO tickets
+  unsigned long long* d_ctl = nullptr;  // [kCtlWords]: counts per list, IO tickets, staging split
+  // HELIOS_CACHE_HOST_STAGED: the host list lives in pinned memory (host stager threads read it),
+  // rows [n_gpu, n_host) are copied by the stagers into a contiguous pinned buffer, chunk by chunk.
+  helios_cache* owner = nullptr;
+  int64_t* h_host_i = nullptr;          // pinned [cap] (device alias d_host_i)
+  uint64_t* h_host_w = nullptr;         // pinned [cap] (device alias d_host_w)
+  int64_t* d_host_i = nullptr;
+  uint64_t* d_host_w = nullptr;
+  char* h_stage = nullptr;              // pinned [kStageCapRows, R]
+  char* d_stage = nullptr;
+  uint32_t* h_done = nullptr;           // pinned [chunks]: batch sequence of each finished chunk
+  uint32_t* d_done = nullptr;
+  uint32_t* h_mail = nullptr;           // pinned {seq, n_host, n_gpu, n_stage}, published by the GPU
+  uint32_t* d_mail = nullptr;
+  uint32_t* d_seq = nullptr;            // device batch counter of this context
+  StageCtx* sctx = nullptr;
 };
 
 struct helios_graph_impl;
@@ -202,6 +224,11 @@ struct helios_cache {
   int io_ctas = 32;
   helios::IoRings io;
   bool has_file = false;
+  // host staging (HELIOS_CACHE_HOST_STAGED)
+  bool staged = false;
+  float stage_frac = 0.6f;
+  int stage_workers = 8;
+  helios::Stager* stager = nullptr;
   helios::GatherWS gws;            // default gather context (helios_gather / helios_batch_prepare)
   cudaStream_t s_submit = nullptr, s_complete = nullptr;
   cudaEvent_t ev_lookup = nullptr, ev_submit = nullptr, ev_complete = nullptr, ev_io_done = nullptr;
@@ -273,5 +300,9 @@ helios_status gather_rows_by_id(const char* src_dev, int32_t R, const int32_t* i
 helios_status io_start(helios_cache* c, const helios_cache_desc* d);
 helios_status io_preload_kernels();
 void io_stop(helios_cache* c);
+helios_status stager_start(helios_cache* c);
+void stager_stop(helios_cache* c);
+helios_status stager_register(helios_cache* c, GatherWS& w);
+void stager_unregister(helios_cache* c, GatherWS& w);
 
 }  // namespace helios

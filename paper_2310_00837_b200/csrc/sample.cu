@@ -47,59 +47,70 @@ helios_status validate_csr_device(const int64_t* indptr, const int32_t* indices,
   return HELIOS_OK;
 }
 
+// Everything a batch's sampling kernels need, passed by value (one struct for every kernel).
+struct SampleCtx {
+  const int64_t* indptr;
+  const int32_t* indices;
+  int64_t V;
+  const int64_t* params;  // [0] key, [1] n_seeds, [2] seeds pointer (device)
+  int* err;
+  uint32_t* keys;
+  uint32_t* minpos;
+  uint32_t* local;
+  uint32_t mask;
+  uint32_t* slot_of;
+  uint32_t* node_slot;
+  int64_t* nodes;
+  int64_t* level_counts;
+  int64_t* edge_counts;
+  int32_t* bp[HELIOS_MAX_HOPS];
+  int32_t* bi[HELIOS_MAX_HOPS];
+  ScanState row_scan[HELIOS_MAX_HOPS];
+  ScanState edge_scan[HELIOS_MAX_HOPS];
+  int32_t fan[HELIOS_MAX_HOPS];
+  int32_t L;
+  unsigned* bar;  // grid barrier {arrivals, generation} (reset with the scan state every batch)
+};
+
 // N_0 = seeds: copy into nodes, insert into the table with local id = position.  Duplicate or
 // out-of-range seeds are latched (reading 7).
-__device__ __forceinline__ void insert_seed(int64_t i, const int64_t* __restrict__ seeds, int64_t V, uint32_t* keys,
-                                            uint32_t* local, uint32_t mask, int64_t* __restrict__ nodes,
-                                            uint32_t* __restrict__ node_slot, int* err) {
+__device__ __forceinline__ void insert_seed(const SampleCtx& c, int64_t i, const int64_t* __restrict__ seeds) {
   const int64_t u = seeds[i];
-  nodes[i] = u;
-  node_slot[i] = kEmpty;
-  if (u < 0 || u >= V) {
-    latch(err, HELIOS_E_RANGE);
+  c.nodes[i] = u;
+  c.node_slot[i] = kEmpty;
+  if (u < 0 || u >= c.V) {
+    latch(c.err, HELIOS_E_RANGE);
     return;
   }
   bool fresh;
-  const uint32_t s = table_insert(keys, mask, (uint32_t)u, &fresh);
-  node_slot[i] = s;
+  const uint32_t s = table_insert(c.keys, c.mask, (uint32_t)u, &fresh);
+  c.node_slot[i] = s;
   if (!fresh) {
-    latch(err, HELIOS_E_INVALID);
+    latch(c.err, HELIOS_E_INVALID);
     return;
   }
-  local[s] = (uint32_t)i;
+  c.local[s] = (uint32_t)i;
 }
 
-__global__ void k_insert_seeds(const int64_t* __restrict__ params, int64_t V,
-                               uint32_t* keys, uint32_t* local, uint32_t mask, int64_t* __restrict__ nodes,
-                               uint32_t* __restrict__ node_slot, int64_t* level_counts, int* err) {
-  const int64_t B = params[1];
-  const int64_t* seeds = (const int64_t*)params[2];
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i == 0) level_counts[0] = B;
-  if (i < B) insert_seed(i, seeds, V, keys, local, mask, nodes, node_slot, err);
-}
-
-// Hop 0 of a batch: the degree scan reads the seeds straight from the batch parameters (n_0 = B)
-// and inserts them into the table on the side (k_fill_insert of hop 0, the next kernel, needs them).
-__global__ void __launch_bounds__(kScanBlock) k_seed_count_scan(const int64_t* __restrict__ params,
-                                                                const int64_t* __restrict__ indptr, int64_t V,
-                                                                int32_t f, int32_t* __restrict__ bp,
-                                                                int64_t* edge_counts, int64_t* level_counts,
-                                                                ScanState ss, uint32_t* keys, uint32_t* local,
-                                                                uint32_t mask, int64_t* __restrict__ nodes,
-                                                                uint32_t* __restrict__ node_slot, int* err) {
-  pdl_trigger();
+// Hop h degree scan: k_i = min(deg(N_h[i]), f_h), block_indptr[h] = exclusive scan (persistent tile
+// loop + decoupled look-back), e_h = total.  Hop 0 reads N_0 = seeds from the parameters and inserts
+// them into the table on the side; hop h > 0 relabels hop h-1's edges on the side.
+__device__ __forceinline__ void dev_count_scan(const SampleCtx& c, int h) {
   using BS = cub::BlockScan<long long, kScanBlock>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ unsigned s_tile;
   __shared__ long long s_prefix;
-  const int64_t n = params[1];
-  const int64_t* seeds = (const int64_t*)params[2];
-  for (;;) {  // persistent: tiles are taken in ticket order until they pass n
+  const int32_t f = c.fan[h];
+  const int64_t* seeds = (const int64_t*)c.params[2];
+  const int64_t* rows = (h == 0) ? seeds : c.nodes;
+  const int64_t n = (h == 0) ? c.params[1] : c.level_counts[h];
+  const ScanState& ss = c.row_scan[h];
+  int32_t* __restrict__ bp = c.bp[h];
+  for (;;) {  // tiles are taken in ticket order until they pass n
     const unsigned tile = tile_ticket(ss, &s_tile);
     const int64_t base = (int64_t)tile * kScanTile;
     if (tile > 0 && base >= n) break;
-    if (tile == 0 && threadIdx.x == 0) level_counts[0] = n;
+    if (h == 0 && tile == 0 && threadIdx.x == 0) c.level_counts[0] = n;
     long long k[kScanItems];
     long long sum = 0;
 #pragma unroll
@@ -107,9 +118,9 @@ __global__ void __launch_bounds__(kScanBlock) k_seed_count_scan(const int64_t* _
       const int64_t i = base + threadIdx.x * kScanItems + q;
       k[q] = 0;
       if (i < n) {
-        const int64_t v = seeds[i];
-        if ((uint64_t)v < (uint64_t)V) {
-          const int64_t d = indptr[v + 1] - indptr[v];
+        const int64_t v = rows[i];
+        if ((uint64_t)v < (uint64_t)c.V) {
+          const int64_t d = c.indptr[v + 1] - c.indptr[v];
           k[q] = (f < 0) ? d : min(d, (int64_t)f);
         }
       }
@@ -127,175 +138,107 @@ __global__ void __launch_bounds__(kScanBlock) k_seed_count_scan(const int64_t* _
     }
     if (threadIdx.x == 0 && ((n == 0 && tile == 0) || (base < n && n <= base + kScanTile))) {
       bp[n] = (int32_t)(prefix + agg);
-      edge_counts[0] = prefix + agg;
+      c.edge_counts[h] = prefix + agg;
     }
+    if (h == 0) {
 #pragma unroll
-    for (int q = 0; q < kScanItems; q++) {
-      const int64_t i = base + threadIdx.x * kScanItems + q;
-      if (i < n) insert_seed(i, seeds, V, keys, local, mask, nodes, node_slot, err);
-    }
-    __syncthreads();
-  }
-}
-
-// k_i = min(deg, f) and the exclusive scan of k into block_indptr[h]; relabels hop h-1 on the side.
-__global__ void __launch_bounds__(kScanBlock) k_row_count_scan(const int64_t* __restrict__ nodes,
-                                                               const int64_t* __restrict__ level_counts, int h,
-                                                               const int64_t* __restrict__ indptr, int64_t V, int32_t f,
-                                                               int32_t* __restrict__ bp, int64_t* edge_counts,
-                                                               ScanState ss, int32_t* __restrict__ prev_bi,
-                                                               const uint32_t* __restrict__ slot_of,
-                                                               const uint32_t* __restrict__ local) {
-  pdl_wait();
-  pdl_trigger();
-  using BS = cub::BlockScan<long long, kScanBlock>;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ unsigned s_tile;
-  __shared__ long long s_prefix;
-  const int64_t n = level_counts[h];
-  for (;;) {  // persistent: tiles are taken in ticket order until they pass n
-    const unsigned tile = tile_ticket(ss, &s_tile);
-    const int64_t base = (int64_t)tile * kScanTile;
-    if (tile > 0 && base >= n) break;
-    long long k[kScanItems];
-    long long sum = 0;
-#pragma unroll
-    for (int q = 0; q < kScanItems; q++) {
-      const int64_t i = base + threadIdx.x * kScanItems + q;
-      k[q] = 0;
-      if (i < n) {
-        const int64_t v = nodes[i];
-        if ((uint64_t)v < (uint64_t)V) {
-          const int64_t d = indptr[v + 1] - indptr[v];
-          k[q] = (f < 0) ? d : min(d, (int64_t)f);
-        }
+      for (int q = 0; q < kScanItems; q++) {
+        const int64_t i = base + threadIdx.x * kScanItems + q;
+        if (i < n) insert_seed(c, i, seeds);
       }
-      sum += k[q];
-    }
-    long long excl, agg;
-    BS(tmp).ExclusiveSum(sum, excl, agg);
-    const long long prefix = tile_lookback(ss, tile, agg, &s_prefix);
-    long long run = prefix + excl;
-#pragma unroll
-    for (int q = 0; q < kScanItems; q++) {
-      const int64_t i = base + threadIdx.x * kScanItems + q;
-      if (i < n) bp[i] = (int32_t)run;
-      run += k[q];
-    }
-    if (threadIdx.x == 0 && ((n == 0 && tile == 0) || (base < n && n <= base + kScanTile))) {
-      bp[n] = (int32_t)(prefix + agg);
-      edge_counts[h] = prefix + agg;
     }
     __syncthreads();
   }
-  if (prev_bi) {  // side job: hop h-1's local ids are final (its k_dedup_assign has completed)
-    const int64_t ep = edge_counts[h - 1];
+  if (h > 0) {  // side job: hop h-1's local ids are final (its dedup_assign has completed)
+    const int64_t ep = c.edge_counts[h - 1];
+    int32_t* __restrict__ prev = c.bi[h - 1];
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ep; e += (int64_t)gridDim.x * blockDim.x)
-      prev_bi[e] = (int32_t)local[slot_of[e]];
+      prev[e] = (int32_t)c.local[c.slot_of[e]];
   }
 }
 
-// One G-lane group per frontier row.  G = power of two >= min(f, 32) (>= 4).
+__device__ __forceinline__ void insert_edge(const SampleCtx& c, int64_t e, uint32_t u) {
+  bool fresh;
+  const uint32_t s = table_insert(c.keys, c.mask, u, &fresh);
+  c.slot_of[e] = s;
+  if (fresh || ld_volatile_u32(c.local + s) == kEmpty) atomicMin(c.minpos + s, (uint32_t)e);
+}
+
+// Hop h fill: one G-lane group per frontier row (G = power of two >= min(f, 32), >= 4).  Copy the
+// whole adjacency when k == d; else Floyd's k-subset, lane j owning draw j and the sequential
+// resolution done with group ballots.  Every sampled id is inserted into the table right away and
+// atomicMin records the first edge position of ids new at this hop.
 template <int G>
-__global__ void __launch_bounds__(256) k_fill_insert(const int64_t* __restrict__ nodes,
-                                                     const int64_t* __restrict__ level_counts, int h,
-                                                     const int64_t* __restrict__ indptr,
-                                                     const int32_t* __restrict__ indices, int64_t V, int32_t f,
-                                                     const int64_t* __restrict__ params,
-                                                     const int32_t* __restrict__ bp, int32_t* scratch,
-                                                     uint32_t* keys, uint32_t* minpos, const uint32_t* local,
-                                                     uint32_t mask, uint32_t* __restrict__ slot_of) {
-  pdl_wait();
-  pdl_trigger();
+__device__ __forceinline__ void dev_fill_insert(const SampleCtx& c, int h) {
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   const unsigned gmask = (G == 32) ? 0xFFFFFFFFu : (((1u << G) - 1u) << (lane & ~(G - 1)));
-  const uint64_t key = (uint64_t)params[0];
-  const int64_t n = level_counts[h];
+  const int32_t f = c.fan[h];
+  const uint64_t key = (uint64_t)c.params[0];
+  const int64_t n = c.level_counts[h];
+  const int32_t* __restrict__ bp = c.bp[h];
+  int32_t* scratch = c.bi[h];
   const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
   const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
   for (int64_t i = grp; i < n; i += ngrp) {
-    const int64_t v = nodes[i];
+    const int64_t v = c.nodes[i];
     int64_t base = 0, d = 0;
-    if ((uint64_t)v < (uint64_t)V) {
-      base = indptr[v];
-      d = indptr[v + 1] - base;
+    if ((uint64_t)v < (uint64_t)c.V) {
+      base = c.indptr[v];
+      d = c.indptr[v + 1] - base;
     }
     const int64_t off = bp[i];
     const int64_t k = (f < 0) ? d : min(d, (int64_t)f);
     if (k == d) {  // every neighbour, CSR order, no RNG consumed
-      for (int64_t p = gl; p < d; p += G) {
-        const int64_t e = off + p;
-        bool fresh;
-        const uint32_t s = table_insert(keys, mask, (uint32_t)indices[base + p], &fresh);
-        slot_of[e] = s;
-        if (fresh || ld_volatile_u32(local + s) == kEmpty) atomicMin(minpos + s, (uint32_t)e);
+      for (int64_t p = gl; p < d; p += G) insert_edge(c, off + p, (uint32_t)c.indices[base + p]);
+    } else if (k <= G) {
+      uint32_t t = 0, m = 0;
+      if (gl < k) {
+        m = (uint32_t)(d - k + gl + 1);
+        t = __umulhi(philox_word(key, (uint32_t)h, (uint64_t)v, (uint32_t)gl), m);
       }
-    } else {
-      int32_t pos = 0;
-      if (k <= G) {  // Floyd: lane j owns draw j; sequential resolution by group ballots
-        uint32_t t = 0, m = 0;
-        if (gl < k) {
-          m = (uint32_t)(d - k + gl + 1);
-          t = __umulhi(philox_word(key, (uint32_t)h, (uint64_t)v, (uint32_t)gl), m);
-        }
-        uint32_t P = 0;
-        for (int j = 0; j < (int)k; j++) {
-          const uint32_t tj = __shfl_sync(gmask, t, j, G);
-          const unsigned hit = __ballot_sync(gmask, gl < j && P == tj);
-          if (gl == j) P = hit ? (m - 1) : tj;
-        }
-        pos = (int32_t)P;
-        if (gl < k) {
-          const int64_t e = off + gl;
-          bool fresh;
-          const uint32_t s = table_insert(keys, mask, (uint32_t)indices[base + pos], &fresh);
-          slot_of[e] = s;
-          if (fresh || ld_volatile_u32(local + s) == kEmpty) atomicMin(minpos + s, (uint32_t)e);
-        }
-      } else {  // k > G (fanout > 32): leader runs Floyd serially, positions kept in the scratch row
-        if (gl == 0) {
-          for (int64_t j = 0; j < k; j++) {
-            const uint32_t m = (uint32_t)(d - k + j + 1);
-            const uint32_t tj = __umulhi(philox_word(key, (uint32_t)h, (uint64_t)v, (uint32_t)j), m);
-            bool seen = false;
-            for (int64_t q = 0; q < j; q++)
-              if ((uint32_t)scratch[off + q] == tj) {
-                seen = true;
-                break;
-              }
-            scratch[off + j] = (int32_t)(seen ? m - 1 : tj);
-          }
-        }
-        __syncwarp(gmask);
-        for (int64_t j = gl; j < k; j += G) {
-          const int64_t e = off + j;
-          bool fresh;
-          const uint32_t s = table_insert(keys, mask, (uint32_t)indices[base + scratch[e]], &fresh);
-          slot_of[e] = s;
-          if (fresh || ld_volatile_u32(local + s) == kEmpty) atomicMin(minpos + s, (uint32_t)e);
-        }
-        __syncwarp(gmask);
+      uint32_t P = 0;
+      for (int j = 0; j < (int)k; j++) {
+        const uint32_t tj = __shfl_sync(gmask, t, j, G);
+        const unsigned hit = __ballot_sync(gmask, gl < j && P == tj);
+        if (gl == j) P = hit ? (m - 1) : tj;
       }
+      if (gl < k) insert_edge(c, off + gl, (uint32_t)c.indices[base + P]);
+    } else {  // k > G (fanout > 32): leader runs Floyd serially, positions kept in the scratch row
+      if (gl == 0) {
+        for (int64_t j = 0; j < k; j++) {
+          const uint32_t m = (uint32_t)(d - k + j + 1);
+          const uint32_t tj = __umulhi(philox_word(key, (uint32_t)h, (uint64_t)v, (uint32_t)j), m);
+          bool seen = false;
+          for (int64_t q = 0; q < j; q++)
+            if ((uint32_t)scratch[off + q] == tj) {
+              seen = true;
+              break;
+            }
+          scratch[off + j] = (int32_t)(seen ? m - 1 : tj);
+        }
+      }
+      __syncwarp(gmask);
+      for (int64_t j = gl; j < k; j += G) insert_edge(c, off + j, (uint32_t)c.indices[base + scratch[off + j]]);
+      __syncwarp(gmask);
     }
   }
 }
 
-__global__ void __launch_bounds__(kScanBlock) k_dedup_assign(const int64_t* __restrict__ edge_counts, int h,
-                                                             const uint32_t* __restrict__ slot_of,
-                                                             const uint32_t* __restrict__ keys,
-                                                             const uint32_t* __restrict__ minpos, uint32_t* local,
-                                                             int64_t* __restrict__ nodes, int64_t* level_counts,
-                                                             ScanState ss, uint32_t* __restrict__ node_slot) {
-  pdl_wait();
-  pdl_trigger();
+__device__ __forceinline__ int fill_group(int32_t f) { return (f < 0 || f > 16) ? 32 : (f > 8 ? 16 : (f > 4 ? 8 : 4)); }
+
+// Hop h dedup/relabel: flag = "this edge is the first occurrence of an id new at this hop"; the
+// scan of the flags numbers the new ids n_h, n_h+1, ... in first-occurrence order and appends them
+// to N_{h+1} (persistent tile loop + decoupled look-back).
+__device__ __forceinline__ void dev_assign(const SampleCtx& c, int h) {
   using BS = cub::BlockScan<int, kScanBlock>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ unsigned s_tile;
   __shared__ long long s_prefix;
-  const int64_t eh = edge_counts[h];
-  const int64_t nh = level_counts[h];
-  for (;;) {  // persistent: tiles are taken in ticket order until they pass e_h
+  const int64_t eh = c.edge_counts[h];
+  const int64_t nh = c.level_counts[h];
+  const ScanState& ss = c.edge_scan[h];
+  for (;;) {
     const unsigned tile = tile_ticket(ss, &s_tile);
     const int64_t base = (int64_t)tile * kScanTile;
     if (tile > 0 && base >= eh) break;
@@ -308,8 +251,8 @@ __global__ void __launch_bounds__(kScanBlock) k_dedup_assign(const int64_t* __re
       flag[q] = 0;
       slot[q] = 0;
       if (e < eh) {
-        slot[q] = slot_of[e];
-        flag[q] = (ld_volatile_u32(local + slot[q]) == kEmpty && minpos[slot[q]] == (uint32_t)e) ? 1 : 0;
+        slot[q] = c.slot_of[e];
+        flag[q] = (ld_volatile_u32(c.local + slot[q]) == kEmpty && c.minpos[slot[q]] == (uint32_t)e) ? 1 : 0;
       }
       sum += flag[q];
     }
@@ -321,43 +264,136 @@ __global__ void __launch_bounds__(kScanBlock) k_dedup_assign(const int64_t* __re
     for (int q = 0; q < kScanItems; q++) {
       if (flag[q]) {
         const int64_t id = nh + run;
-        nodes[id] = (int64_t)keys[slot[q]];
-        node_slot[id] = slot[q];
-        local[slot[q]] = (uint32_t)id;
+        c.nodes[id] = (int64_t)c.keys[slot[q]];
+        c.node_slot[id] = slot[q];
+        c.local[slot[q]] = (uint32_t)id;
         run++;
       }
     }
     if (threadIdx.x == 0 && ((eh == 0 && tile == 0) || (base < eh && eh <= base + kScanTile)))
-      level_counts[h + 1] = nh + prefix + agg;
+      c.level_counts[h + 1] = nh + prefix + agg;
     __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(256) k_relabel(int32_t* bi, const int64_t* __restrict__ edge_counts, int h,
-                                                 const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ local) {
-  pdl_wait();
-  pdl_trigger();
-  const int64_t eh = edge_counts[h];
+__device__ __forceinline__ void dev_relabel(const SampleCtx& c, int h) {
+  const int64_t eh = c.edge_counts[h];
+  int32_t* __restrict__ bi = c.bi[h];
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < eh; e += (int64_t)gridDim.x * blockDim.x)
-    bi[e] = (int32_t)local[slot_of[e]];
+    bi[e] = (int32_t)c.local[c.slot_of[e]];
 }
 
 // Returns the batch hash table to all-EMPTY by clearing exactly the slots of the batch's nodes
 // (every occupied slot belongs to one node of N_L).
-__global__ void __launch_bounds__(256) k_table_clear(const int64_t* __restrict__ n_nodes,
-                                                     const uint32_t* __restrict__ node_slot, uint32_t* keys,
-                                                     uint32_t* minpos, uint32_t* local) {
-  pdl_wait();
-  pdl_trigger();
-  const int64_t n = *n_nodes;
+__device__ __forceinline__ void dev_table_clear(const SampleCtx& c) {
+  const int64_t n = c.level_counts[c.L];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t s = node_slot[i];
+    const uint32_t s = c.node_slot[i];
     if (s != kEmpty) {
-      keys[s] = kEmpty;
-      minpos[s] = kEmpty;
-      local[s] = kEmpty;
+      c.keys[s] = kEmpty;
+      c.minpos[s] = kEmpty;
+      c.local[s] = kEmpty;
     }
   }
+}
+
+__device__ __forceinline__ void dev_insert_seeds(const SampleCtx& c) {  // L = 0
+  const int64_t B = c.params[1];
+  const int64_t* seeds = (const int64_t*)c.params[2];
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i0 == 0) c.level_counts[0] = B;
+  for (int64_t i = i0; i < B; i += (int64_t)gridDim.x * blockDim.x) insert_seed(c, i, seeds);
+}
+
+// ---- multi-kernel path: one kernel per phase, chained with programmatic dependent launch ----
+__global__ void __launch_bounds__(kScanBlock) k_count_scan(SampleCtx c, int h) {
+  if (h > 0) pdl_wait();
+  pdl_trigger();
+  dev_count_scan(c, h);
+}
+template <int G>
+__global__ void __launch_bounds__(256) k_fill_insert(SampleCtx c, int h) {
+  pdl_wait();
+  pdl_trigger();
+  dev_fill_insert<G>(c, h);
+}
+__global__ void __launch_bounds__(kScanBlock) k_dedup_assign(SampleCtx c, int h) {
+  pdl_wait();
+  pdl_trigger();
+  dev_assign(c, h);
+}
+__global__ void __launch_bounds__(256) k_relabel(SampleCtx c, int h) {
+  pdl_wait();
+  pdl_trigger();
+  dev_relabel(c, h);
+}
+__global__ void __launch_bounds__(256) k_table_clear(SampleCtx c) {
+  pdl_wait();
+  pdl_trigger();
+  dev_table_clear(c);
+}
+__global__ void __launch_bounds__(256) k_insert_seeds(SampleCtx c) { dev_insert_seeds(c); }
+
+// ---- persistent path: the whole batch in one cooperative kernel, phases separated by a grid
+// barrier (3 per hop + 1), so a batch costs one launch instead of 2 + 3L ----
+constexpr uint64_t kBarrierTimeoutNs = 10ull * 1000000000ull;
+
+// Generation barrier over the cooperative grid.  bar[0] counts arrivals (all-ones = none: the scan
+// state memset resets it every batch), bar[1] is the generation.  A watchdog latches E_TIMEOUT
+// instead of hanging if the grid is ever not co-resident.
+__device__ __forceinline__ bool grid_sync(const SampleCtx& c) {
+  __shared__ int s_ok;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ok = 1;
+    const unsigned gen = ld_volatile_u32(c.bar + 1);
+    __threadfence();
+    const unsigned arrived = atomicAdd(c.bar, 1u) + 2u;  // all-ones + 1 arrival -> 1
+    if (arrived == gridDim.x) {
+      atomicExch(c.bar, 0xFFFFFFFFu);
+      __threadfence();
+      atomicAdd(c.bar + 1, 1u);
+    } else {
+      const uint64_t t0 = globaltimer();
+      while (ld_volatile_u32(c.bar + 1) == gen) {
+        if (globaltimer() - t0 > kBarrierTimeoutNs) {
+          latch(c.err, HELIOS_E_TIMEOUT);
+          ok = 0;
+          break;
+        }
+        __nanosleep(20);
+      }
+    }
+    __threadfence();
+    s_ok = ok;
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+__global__ void __launch_bounds__(256, 2) k_sample_batch(SampleCtx c) {
+  if (c.L == 0) {
+    dev_insert_seeds(c);
+    if (!grid_sync(c)) return;
+  }
+  for (int h = 0; h < c.L; h++) {
+    dev_count_scan(c, h);
+    if (!grid_sync(c)) return;
+    switch (fill_group(c.fan[h])) {
+      case 4: dev_fill_insert<4>(c, h); break;
+      case 8: dev_fill_insert<8>(c, h); break;
+      case 16: dev_fill_insert<16>(c, h); break;
+      default: dev_fill_insert<32>(c, h); break;
+    }
+    if (!grid_sync(c)) return;
+    dev_assign(c, h);
+    if (!grid_sync(c)) return;
+  }
+  if (c.L > 0) {
+    dev_relabel(c, c.L - 1);
+    if (!grid_sync(c)) return;
+  }
+  dev_table_clear(c);
 }
 
 __global__ void k_hot_count(const int64_t* __restrict__ nodes, const int64_t* __restrict__ n_nodes, uint64_t* hot) {
@@ -449,7 +485,7 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
   ws_free(w);
   const size_t table_bytes = (size_t)T * 4;
   const size_t status_bytes = (size_t)(tiles_r + tiles_e) * HELIOS_MAX_HOPS * 8;
-  const size_t counter_bytes = (size_t)2 * HELIOS_MAX_HOPS * 4;
+  const size_t counter_bytes = (size_t)2 * HELIOS_MAX_HOPS * 4 + 8;
   w.reset_bytes = 3 * table_bytes + status_bytes + counter_bytes;
   HCUDA(cudaMalloc(&w.reset_base, w.reset_bytes));
   HCUDA(cudaMalloc(&w.slot_of, (size_t)max_e * 4));
@@ -483,7 +519,10 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
     w.edge_scan[h].counter = (unsigned*)p;
     p += 4;
   }
+  w.bar = (unsigned*)p;
+  p += 8;
   w.scan_bytes = (size_t)(p - w.scan_base);
+  if (const char* e = getenv("HELIOS_SAMPLE_PERSISTENT")) w.persistent = atoi(e) != 0;
   HCUDA(cudaMemset(w.reset_base, 0xFF, w.reset_bytes));  // the table starts all-EMPTY
   return HELIOS_OK;
 }
@@ -508,15 +547,49 @@ helios_status ws_upload_params(SampleWS& w, uint64_t key, int64_t B, const int64
   return HELIOS_OK;
 }
 
+static SampleCtx make_ctx(const helios_graph* g, const SampleWS& w, const int32_t* fanouts, int32_t L,
+                          const helios_blocks* out) {
+  SampleCtx c{};
+  c.indptr = g->indptr;
+  c.indices = g->indices;
+  c.V = g->V;
+  c.params = w.d_params;
+  c.err = g->d_err;
+  c.keys = w.keys;
+  c.minpos = w.minpos;
+  c.local = w.local;
+  c.mask = w.table_size - 1;
+  c.slot_of = w.slot_of;
+  c.node_slot = w.node_slot;
+  c.nodes = out->nodes;
+  c.level_counts = out->level_counts;
+  c.edge_counts = out->edge_counts;
+  for (int h = 0; h < L; h++) {
+    c.bp[h] = out->block_indptr[h];
+    c.bi[h] = out->block_indices[h];
+    c.row_scan[h] = w.row_scan[h];
+    c.edge_scan[h] = w.edge_scan[h];
+    c.fan[h] = fanouts[h];
+  }
+  c.L = L;
+  c.bar = w.bar;
+  return c;
+}
+
 template <int G>
-static void launch_fill(const helios_graph* g, SampleWS& w, const helios_blocks* out, int h, int64_t rows, int32_t f,
-                        cudaStream_t st) {
+static void launch_fill(const helios_graph* g, const SampleCtx& c, int h, int64_t rows, cudaStream_t st) {
   const int64_t threads = std::max<int64_t>(rows, 1) * G;
   const int grid = (int)std::min<int64_t>((threads + 255) / 256, (int64_t)g->sms * 4);
-  launch_pdl(k_fill_insert<G>, dim3(grid), dim3(256), st, out->nodes, (const int64_t*)out->level_counts, h,
-             (const int64_t*)g->indptr, (const int32_t*)g->indices, g->V, f, (const int64_t*)w.d_params,
-             (const int32_t*)out->block_indptr[h], out->block_indices[h], w.keys, w.minpos, (const uint32_t*)w.local,
-             w.table_size - 1, w.slot_of);
+  launch_pdl(k_fill_insert<G>, dim3(grid), dim3(256), st, c, h);
+}
+
+static int persistent_grid(int sms) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample_batch, 256, 0);
+    per_sm = std::max(1, std::min(per_sm, 2));
+  }
+  return sms * per_sm;
 }
 
 helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const int32_t* fanouts, int32_t L,
@@ -524,41 +597,42 @@ helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const i
   int64_t maxn, lvl[HELIOS_MAX_HOPS + 1], edg[HELIOS_MAX_HOPS];
   helios_status s = sample_bounds(B_max, fanouts, L, g->V, g->E, &maxn, lvl, edg);
   if (s != HELIOS_OK) return s;
-  const uint32_t mask = w.table_size - 1;
+  const SampleCtx c = make_ctx(g, w, fanouts, L, out);
   HCUDA(cudaMemsetAsync(w.scan_base, 0xFF, w.scan_bytes, st));
+  if (w.persistent) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(persistent_grid(g->sms));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HCUDA(cudaLaunchKernelEx(&cfg, k_sample_batch, c));
+    return HELIOS_OK;
+  }
   if (L == 0)
-    k_insert_seeds<<<(int)std::max<int64_t>(1, (B_max + 255) / 256), 256, 0, st>>>(
-        w.d_params, g->V, w.keys, w.local, mask, out->nodes, w.node_slot, out->level_counts, g->d_err);
+    k_insert_seeds<<<(int)std::max<int64_t>(1, (B_max + 255) / 256), 256, 0, st>>>(c);
   for (int h = 0; h < L; h++) {
     const int32_t f = fanouts[h];
     // persistent tile loops: a grid of at most one CTA per SM, tiles taken by ticket
     const int rt = (int)std::min<int64_t>(std::max<int64_t>(1, (lvl[h] + kScanTile - 1) / kScanTile), g->sms);
-    if (h == 0)
-      k_seed_count_scan<<<rt, kScanBlock, 0, st>>>(w.d_params, g->indptr, g->V, f, out->block_indptr[0],
-                                                   out->edge_counts, out->level_counts, w.row_scan[0], w.keys,
-                                                   w.local, mask, out->nodes, w.node_slot, g->d_err);
-    else
-      launch_pdl(k_row_count_scan, dim3(rt), dim3(kScanBlock), st, (const int64_t*)out->nodes,
-                 (const int64_t*)out->level_counts, h, (const int64_t*)g->indptr, g->V, f, out->block_indptr[h],
-                 out->edge_counts, w.row_scan[h], out->block_indices[h - 1], (const uint32_t*)w.slot_of,
-                 (const uint32_t*)w.local);
-    if (f < 0 || f > 16) launch_fill<32>(g, w, out, h, lvl[h], f, st);
-    else if (f > 8) launch_fill<16>(g, w, out, h, lvl[h], f, st);
-    else if (f > 4) launch_fill<8>(g, w, out, h, lvl[h], f, st);
-    else launch_fill<4>(g, w, out, h, lvl[h], f, st);
+    if (h == 0) k_count_scan<<<rt, kScanBlock, 0, st>>>(c, 0);
+    else launch_pdl(k_count_scan, dim3(rt), dim3(kScanBlock), st, c, h);
+    if (f < 0 || f > 16) launch_fill<32>(g, c, h, lvl[h], st);
+    else if (f > 8) launch_fill<16>(g, c, h, lvl[h], st);
+    else if (f > 4) launch_fill<8>(g, c, h, lvl[h], st);
+    else launch_fill<4>(g, c, h, lvl[h], st);
     const int et = (int)std::min<int64_t>(std::max<int64_t>(1, (edg[h] + kScanTile - 1) / kScanTile), g->sms);
-    launch_pdl(k_dedup_assign, dim3(et), dim3(kScanBlock), st, (const int64_t*)out->edge_counts, h,
-               (const uint32_t*)w.slot_of, (const uint32_t*)w.keys, (const uint32_t*)w.minpos, w.local, out->nodes,
-               out->level_counts, w.edge_scan[h], w.node_slot);
+    launch_pdl(k_dedup_assign, dim3(et), dim3(kScanBlock), st, c, h);
   }
   if (L > 0) {
     const int ge = (int)std::min<int64_t>(std::max<int64_t>(1, (edg[L - 1] + 255) / 256), (int64_t)g->sms * 2);
-    launch_pdl(k_relabel, dim3(ge), dim3(256), st, out->block_indices[L - 1], (const int64_t*)out->edge_counts, L - 1,
-               (const uint32_t*)w.slot_of, (const uint32_t*)w.local);
+    launch_pdl(k_relabel, dim3(ge), dim3(256), st, c, L - 1);
   }
   const int gc = (int)std::min<int64_t>(std::max<int64_t>(1, (maxn + 255) / 256), (int64_t)g->sms * 2);
-  launch_pdl(k_table_clear, dim3(gc), dim3(256), st, (const int64_t*)(out->level_counts + L),
-             (const uint32_t*)w.node_slot, w.keys, w.minpos, w.local);
+  launch_pdl(k_table_clear, dim3(gc), dim3(256), st, c);
   HCUDA(cudaGetLastError());
   return HELIOS_OK;
 }

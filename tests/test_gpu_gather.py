@@ -69,13 +69,15 @@ def gather_and_check(H, c, inp, nodes_np, stats_ref):
     assert stats.cpu().numpy().tolist() == stats_ref.tolist()
 
 
-@pytest.mark.parametrize("alias", [False, True])
-def test_gather_three_tiers_c1(H, c1, c1_hot, alias):
+@pytest.mark.parametrize("alias,staged", [(False, False), (True, False), (False, True), (True, True)])
+def test_gather_three_tiers_c1(H, c1, c1_hot, alias, staged):
     g, hot = c1_hot
     cfg = c1.cfg
     Hr, S = workloads.tier_rows(cfg)
     c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=c1.table, feature_path=c1.feature_path,
-                             header_bytes=c1.header, file_stride=c1.stride, flags=H.HOST_ALIAS if alias else 0)
+                             header_bytes=c1.header, file_stride=c1.stride,
+                             flags=(H.HOST_ALIAS if alias else 0) | (H.HOST_STAGED if staged else 0),
+                             stage_workers=3, stage_frac=0.5)
     assert c.info().file_rows == cfg.V - Hr - S
     dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S, host_slot_is_id=alias)
     rng = np.random.default_rng(0)

@@ -25,13 +25,15 @@ def c1(tmp_path_factory):
 
 
 def build(H, inp, Hr, S, flags=0):
+    # staged-mode caches use 3 stager threads and stage 70 % of each batch's host rows
     cfg = inp.cfg
     g = H.helios_graph_load(inp.graph.indptr, inp.graph.indices)
     hot = torch.zeros(cfg.V, dtype=torch.int64, device="cuda")
     pk = workloads.presample_keys(len(inp.batches))
     H.helios_presample(g, torch.as_tensor(np.concatenate(inp.batches)).cuda(), cfg.B, cfg.fanouts, pk, hot)
     c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=inp.table, feature_path=inp.feature_path,
-                             header_bytes=inp.header, file_stride=inp.stride, flags=flags)
+                             header_bytes=inp.header, file_stride=inp.stride, flags=flags, stage_workers=3,
+                             stage_frac=0.7)
     return g, hot, c
 
 
@@ -50,11 +52,13 @@ def check_slot(p, slot, inp, seeds, key, dref):
         assert stats.cpu().tolist() == oracle.lookup_counts(dref, orc.nodes).tolist()
 
 
-@pytest.mark.parametrize("depth,flags,host_seeds", [(2, 0, False), (1, 0, True), (3, 0, False), (2, 1, True)])
-def test_plan_c1_epoch(H, c1, depth, flags, host_seeds):
+@pytest.mark.parametrize("depth,flags,host_seeds,staged", [(2, 0, False, False), (1, 0, True, False),
+                                                          (3, 0, False, False), (2, 1, True, False),
+                                                          (3, 0, False, True), (1, 1, True, True)])
+def test_plan_c1_epoch(H, c1, depth, flags, host_seeds, staged):
     cfg = c1.cfg
     Hr, S = workloads.tier_rows(cfg)
-    g, hot, c = build(H, c1, Hr, S, flags=H.HOST_ALIAS)
+    g, hot, c = build(H, c1, Hr, S, flags=H.HOST_ALIAS | (H.HOST_STAGED if staged else 0))
     dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S, host_slot_is_id=True)
     p = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=depth, flags=flags)
     keys = workloads.batch_keys(0, len(c1.batches))
