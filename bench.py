@@ -232,6 +232,7 @@ def main():
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no baseline, no parity")
     ap.add_argument("--depth", type=int, default=6, help="batches in flight (plan slots)")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly instead of CUDA graphs")
+    ap.add_argument("--serial-gather", type=int, default=0, help="1: gathers of successive batches run one at a time")
     ap.add_argument("--host-alias", action="store_true", help="host tier = canonical table by id (no packed copy)")
     ap.add_argument("--io-rings", type=int, default=8, help="SQ/CQ ring pairs = host IO worker threads")
     ap.add_argument("--host-staged", type=float, default=0.0,
@@ -370,7 +371,8 @@ def main():
     seed_of = {b: torch.as_tensor(inp.batches[b]).cuda() for b in sorted(set(seq))}
     stream = torch.cuda.current_stream()
     depth = args.depth
-    plan = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=depth, flags=H.PLAN_NO_GRAPH if args.no_graph else 0)
+    pflags = (H.PLAN_NO_GRAPH if args.no_graph else 0) | (H.PLAN_SERIAL_GATHER if args.serial_gather else 0)
+    plan = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=depth, flags=pflags)
 
     for i in range(args.warmup):
         H.helios_plan_submit(plan, i % depth, seed_of[seq[i]], keys[seq[i]], stream)
@@ -513,7 +515,7 @@ def main():
     dominant = max(terms.items(), key=lambda x: x[1])[0]
     value = world * steps / (max_ms / 1e3)
     e2e_val = world * steps / e2e_s
-    launches_per_step = 3 * L + 2 + 2 + (3 if c.info().file_rows > 0 else 0)
+    launches_per_step = 3 * L + 2 + 2 + (3 if c.info().file_rows > 0 else 0) + (1 if args.host_staged > 0 else 0)
     out = {
         "metric": "sampled+gathered mini-batches/sec (feature GB/s and tier-roofline fraction alongside)",
         "value": round(value, 3), "unit": "batches/s", "n_gpus": 1 if one_gpu else world, "steps": steps, "warmup": args.warmup,
@@ -529,7 +531,7 @@ def main():
                    "host_tier": ("alias of canonical table (by id)" if args.host_alias else "packed, hot-rank order")
                    + (f"; {args.host_staged:.0%} of host rows staged by {args.stage_workers} host threads"
                       if args.host_staged > 0 else "; GPU zero-copy reads"),
-                   "batches_in_flight": depth, "cuda_graphs": not args.no_graph,
+                   "batches_in_flight": depth, "cuda_graphs": not args.no_graph, "serial_gather": bool(args.serial_gather),
                    "l2": "inputs larger than L2 (CSR %.1f GB, feature table %.1f GB); no flush" % (
                        (inp.graph.E * 4 + cfg.V * 8) / 1e9, cfg.V * R / 1e9)},
         "feature_gbs": round(world * n_rows / steps * R * steps / (max_ms / 1e3) / 1e9, 2),

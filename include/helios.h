@@ -158,8 +158,8 @@ typedef struct {
   const uint64_t* hotness;    /* device uint64[V] (helios_presample output, already all-reduced) */
   const void* host_table;     /* host: canonical rows, row v at host_table + v*R (V*R bytes), or NULL;
                                  borrowed (registered + mapped unless TABLE_MAPPED); must outlive the cache */
-  const char* feature_path;   /* canonical feature file or NULL (required iff G*H + S < V and no
-                                 host_table covers the FILE rows... FILE-tier rows are ALWAYS read from it) */
+  const char* feature_path;   /* canonical feature file or NULL; required when G*H + S < V (FILE-tier rows
+                                 are always read from it) or when no host_table is given to fill the tiers */
   int64_t header_bytes;       /* file: byte offset of row 0                                      */
   int64_t file_stride;        /* file: bytes between rows (>= R; 512-multiple for O_DIRECT)      */
   int32_t io_rings;           /* number of SQ/CQ ring pairs = host IO worker threads (>= 1)      */
@@ -228,10 +228,13 @@ helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64
  *   desc.max_seeds   B: capacity of every slot (n_seeds <= B per submit).
  *   desc.L, fanouts  hops and fanouts (as helios_sample).
  *   desc.depth       number of slots, 1..8.
- *   desc.flags       HELIOS_PLAN_NO_GRAPH: launch the kernels directly on every submit.
+ *   desc.flags       HELIOS_PLAN_NO_GRAPH: launch the kernels directly on every submit;
+ *                    HELIOS_PLAN_SERIAL_GATHER: chain the gathers of successive submits.
  *   c                cache, or NULL for a sampling-only plan (no features / stats).
  * Blocking create/free. */
 #define HELIOS_PLAN_NO_GRAPH 0x1u
+#define HELIOS_PLAN_SERIAL_GATHER 0x2u  /* gathers of successive batches run one at a time (sampling
+                                           still overlaps): the link is not split between gathers */
 #define HELIOS_SUBMIT_SEEDS_HOST 0x1u  /* seeds pointer is host memory (copied with the parameters, H2D) */
 #define HELIOS_SUBMIT_TIMING 0x2u      /* record device timing events around the sample / gather phases */
 typedef struct helios_plan helios_plan;
@@ -243,6 +246,7 @@ typedef struct {
   uint32_t flags;
 } helios_plan_desc;
 helios_status helios_plan_create(helios_graph* g, helios_cache* c, const helios_plan_desc* desc, helios_plan** out);
+/* Free a plan before the cache and graph it was created on. */
 void helios_plan_free(helios_plan* p);
 /* Plan-owned DEVICE outputs of `slot` (valid until helios_plan_free): the slot's blocks, its
  * feature buffer [blocks->nodes_cap, row_bytes] (NULL without cache) and its gather stats. */

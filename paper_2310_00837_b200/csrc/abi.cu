@@ -375,6 +375,7 @@ helios_status helios_plan_create(helios_graph* g, helios_cache* c, const helios_
   p->c = c;
   p->d = *d;
   p->graphs = !(d->flags & HELIOS_PLAN_NO_GRAPH);
+  p->serial_gather = (d->flags & HELIOS_PLAN_SERIAL_GATHER) != 0;
   helios_status st = plan_create_impl(p);
   if (st != HELIOS_OK) {
     std::string keep = helios_last_error();

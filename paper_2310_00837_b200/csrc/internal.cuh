@@ -137,8 +137,6 @@ struct GatherWS {
   StageCtx* sctx = nullptr;
 };
 
-struct helios_graph_impl;
-
 }  // namespace helios
 
 struct helios_graph {
@@ -263,6 +261,9 @@ struct helios_plan {
   helios_plan_desc d{};
   int64_t maxn = 0;
   bool graphs = true;
+  bool serial_gather = false;
+  cudaEvent_t ev_gather_chain = nullptr;  // last gather submitted (HELIOS_PLAN_SERIAL_GATHER)
+  bool gather_chained = false;
   std::vector<helios::PlanSlot> slots;
 };
 

@@ -32,6 +32,8 @@ void plan_free_impl(helios_plan* p) {
     if (s.stream) cudaStreamDestroy(s.stream);
   }
   p->slots.clear();
+  if (p->ev_gather_chain) cudaEventDestroy(p->ev_gather_chain);
+  p->ev_gather_chain = nullptr;
 }
 
 template <typename F>
@@ -58,6 +60,7 @@ helios_status plan_create_impl(helios_plan* p) {
   helios_status s = sample_bounds(d.max_seeds, d.fanouts, d.L, g->V, g->E, &p->maxn, lvl, edg);
   if (s != HELIOS_OK) return s;
   p->slots.resize(d.depth);
+  HCUDA(cudaEventCreateWithFlags(&p->ev_gather_chain, cudaEventDisableTiming));
   for (int k = 0; k < d.depth; k++) {
     PlanSlot& sl = p->slots[k];
     // output blocks: one allocation
@@ -132,7 +135,8 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
   const bool timed = (flags & HELIOS_SUBMIT_TIMING) != 0;
   cudaEvent_t* ev = &sl.ring[3 * (sl.tcount % PlanSlot::kRing)];
   if (timed) HCUDA(cudaEventRecord(ev[0], sl.stream));
-  if (p->graphs && !timed) {
+  const bool chain = p->serial_gather && p->c;
+  if (p->graphs && !timed && !chain) {
     HCUDA(cudaGraphLaunch(sl.g_all, sl.stream));
   } else {
     if (p->graphs) {
@@ -141,6 +145,7 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
       s = sample_launch(p->g, sl.ws, p->d.max_seeds, p->d.fanouts, p->d.L, &sl.blocks, sl.stream);
       if (s != HELIOS_OK) return s;
     }
+    if (chain && p->gather_chained) HCUDA(cudaStreamWaitEvent(sl.stream, p->ev_gather_chain, 0));
     if (timed) HCUDA(cudaEventRecord(ev[1], sl.stream));
     if (p->c) {
       if (p->graphs) {
@@ -155,6 +160,10 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
   if (p->c) {
     s = io_launch(p->c, sl.gws, sl.feats, sl.stream);
     if (s != HELIOS_OK) return s;
+  }
+  if (chain) {
+    HCUDA(cudaEventRecord(p->ev_gather_chain, sl.stream));
+    p->gather_chained = true;
   }
   if (timed) {
     HCUDA(cudaEventRecord(ev[2], sl.stream));

@@ -140,14 +140,11 @@ __device__ __forceinline__ void dev_count_scan(const SampleCtx& c, int h) {
       bp[n] = (int32_t)(prefix + agg);
       c.edge_counts[h] = prefix + agg;
     }
-    if (h == 0) {
-#pragma unroll
-      for (int q = 0; q < kScanItems; q++) {
-        const int64_t i = base + threadIdx.x * kScanItems + q;
-        if (i < n) insert_seed(c, i, seeds);
-      }
-    }
     __syncthreads();
+  }
+  if (h == 0) {  // side job: N_0 = seeds into the table, spread over the whole grid
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+      insert_seed(c, i, seeds);
   }
   if (h > 0) {  // side job: hop h-1's local ids are final (its dedup_assign has completed)
     const int64_t ep = c.edge_counts[h - 1];
@@ -618,7 +615,8 @@ helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const i
     const int32_t f = fanouts[h];
     // persistent tile loops: a grid of at most one CTA per SM, tiles taken by ticket
     const int rt = (int)std::min<int64_t>(std::max<int64_t>(1, (lvl[h] + kScanTile - 1) / kScanTile), g->sms);
-    if (h == 0) k_count_scan<<<rt, kScanBlock, 0, st>>>(c, 0);
+    // hop 0: enough CTAs for one seed insert per thread (the scan itself uses ceil(B/tile) tiles)
+    if (h == 0) k_count_scan<<<std::max<int>(rt, (int)std::min<int64_t>((B_max + 255) / 256, g->sms)), kScanBlock, 0, st>>>(c, 0);
     else launch_pdl(k_count_scan, dim3(rt), dim3(kScanBlock), st, c, h);
     if (f < 0 || f > 16) launch_fill<32>(g, c, h, lvl[h], st);
     else if (f > 8) launch_fill<16>(g, c, h, lvl[h], st);

@@ -22,12 +22,15 @@
 
 namespace helios {
 
+// Chunk distribution word: (seq << 32) | (n_chunks << 16) | next.  A chunk (seq, c) is claimed by a
+// CAS that checks seq and next < n_chunks in the same word, so a worker holding a stale view can
+// never take (or lose) a chunk of another batch.  While a claimed chunk is outstanding the GPU is
+// waiting for it, so the mailbox (n_gpu, n_stage) cannot change under the worker.
 struct StageCtx {
   GatherWS* w = nullptr;
   std::mutex mu;
   uint32_t cur_seq = 0;
-  int64_t n_gpu = 0, n_stage = 0, n_chunks = 0;
-  std::atomic<uint64_t> next{0};  // (seq << 32) | next chunk of that sequence
+  std::atomic<uint64_t> word{0};
 };
 
 struct Stager {
@@ -48,26 +51,25 @@ static void stager_worker(Stager* S) {
       std::shared_lock<std::shared_mutex> lk(S->mu);
       for (StageCtx* x : S->ctxs) {
         GatherWS& w = *x->w;
-        const uint32_t seq = __atomic_load_n(&w.h_mail[0], __ATOMIC_ACQUIRE);
-        if (seq != x->cur_seq) {  // a new batch was published on this context
+        if (__atomic_load_n(&w.h_mail[0], __ATOMIC_ACQUIRE) != x->cur_seq) {  // a new batch was posted
           std::lock_guard<std::mutex> g(x->mu);
+          const uint32_t seq = __atomic_load_n(&w.h_mail[0], __ATOMIC_ACQUIRE);  // latest, re-read under lock
           if (seq != x->cur_seq) {
-            x->n_gpu = w.h_mail[2];
-            x->n_stage = w.h_mail[3];
-            x->n_chunks = (x->n_stage + kStageChunk - 1) / kStageChunk;
-            x->next.store(((uint64_t)seq << 32), std::memory_order_release);
+            const uint64_t n_chunks = (w.h_mail[3] + kStageChunk - 1) / kStageChunk;
+            x->word.store(((uint64_t)seq << 32) | (n_chunks << 16), std::memory_order_release);
             x->cur_seq = seq;
           }
         }
         for (;;) {
-          const uint64_t cur = x->next.load(std::memory_order_acquire);
-          if ((uint32_t)(cur >> 32) != seq || (int64_t)(cur & 0xFFFFFFFFu) >= x->n_chunks) break;
-          const uint64_t t = x->next.fetch_add(1, std::memory_order_acq_rel);
-          const uint32_t tseq = (uint32_t)(t >> 32);
-          const int64_t chunk = (int64_t)(t & 0xFFFFFFFFu);
-          if (tseq != seq || chunk >= x->n_chunks) break;
-          const int64_t j0 = chunk * kStageChunk, j1 = std::min<int64_t>(x->n_stage, j0 + kStageChunk);
-          const uint64_t* hw = w.h_host_w + x->n_gpu;
+          uint64_t cur = x->word.load(std::memory_order_acquire);
+          const uint32_t seq = (uint32_t)(cur >> 32);
+          const int64_t n_chunks = (int64_t)((cur >> 16) & 0xFFFF), chunk = (int64_t)(cur & 0xFFFF);
+          if (chunk >= n_chunks) break;
+          if (!x->word.compare_exchange_weak(cur, cur + 1, std::memory_order_acq_rel)) continue;
+          // (seq, chunk) is ours and outstanding: the mailbox of `seq` is stable
+          const int64_t n_gpu = w.h_mail[2], n_stage = w.h_mail[3];
+          const int64_t j0 = chunk * kStageChunk, j1 = std::min<int64_t>(n_stage, j0 + kStageChunk);
+          const uint64_t* hw = w.h_host_w + n_gpu;
           for (int64_t j = j0; j < j1; j++) {
             if (j + 4 < j1) {
               const char* p = S->host_tier + (int64_t)(hw[j + 4] & ((1ull << 56) - 1)) * S->R;
@@ -117,6 +119,7 @@ helios_status stager_register(helios_cache* c, GatherWS& w) {
   StageCtx* x = new StageCtx();
   x->w = &w;
   x->cur_seq = w.h_mail[0];
+  x->word.store((uint64_t)x->cur_seq << 32);
   {
     std::unique_lock<std::shared_mutex> lk(c->stager->mu);
     c->stager->ctxs.push_back(x);

@@ -102,3 +102,29 @@ def test_plan_sample_only_medium(H):
         H.helios_plan_submit(p, 0, torch.arange(2000, device="cuda"), 1)
     assert e.value.name == "E_CAPACITY"
     p.free()
+
+
+def test_staged_stress_many_batches(H):
+    """Staged host tier under sustained load: 4000 batches through a 6-slot plan (a few hundred
+    thousand chunk hand-offs between GPU stage warps and host stager threads) must finish without the
+    watchdog firing, and the final batches must stay bit-exact."""
+    cfg = workloads.Config("stress", 200_000, 3_000_000, 64, 1024, [15, 10, 5], 0.05, 0.95, train_pct=100)
+    inp = workloads.make_inputs(cfg, table=True)
+    Hr, S = int(0.05 * cfg.V), cfg.V - int(0.05 * cfg.V)
+    g, hot, c = build(H, inp, Hr, S, flags=H.HOST_STAGED)
+    dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S)
+    p = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=6)
+    keys = workloads.batch_keys(0, len(inp.batches))
+    seeds = [torch.as_tensor(b).cuda() for b in inp.batches[:64]]
+    n = 4000
+    for i in range(n):
+        H.helios_plan_submit(p, i % 6, seeds[i % 64], keys[i % 64])
+    for k in range(6):
+        H.helios_plan_wait(p, k)
+    H.helios_sync(c)
+    for k in range(6):
+        b = (n - 6 + k) % 64
+        check_slot(p, (n - 6 + k) % 6, inp, inp.batches[b], keys[b], dref)
+    assert c.info().host_rows == S
+    p.free()
+    c.free()

@@ -127,3 +127,16 @@ def test_presample_hotness(H, c1):
     H.helios_graph_sync(g)
     ref = oracle.presample(c1.graph.indptr, c1.graph.indices, c1.batches, keys, cfg.fanouts)
     assert np.array_equal(hot.cpu().numpy().astype(np.uint64), ref)
+
+
+def test_persistent_sampler_parity(H, medium, monkeypatch):
+    """The opt-in persistent cooperative sampler (one kernel per batch, grid barriers) is bit-exact too."""
+    monkeypatch.setenv("HELIOS_SAMPLE_PERSISTENT", "1")
+    g = H.helios_graph_load(medium.indptr, medium.indices)
+    rng = np.random.default_rng(7)
+    for B, fan in ((1024, [15, 10, 5]), (64, [40, 3]), (300, [-1])):
+        seeds = rng.choice(medium.V, B, replace=False)
+        gpu = run_gpu(H, g, seeds, fan, 991)
+        orc = oracle.sample(medium.indptr, medium.indices, seeds, fan, 991)
+        assert_same(gpu, orc, len(fan))
+    g.free()
