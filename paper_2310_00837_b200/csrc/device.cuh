@@ -58,16 +58,16 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
 }
 
 // Open-addressing (linear probing) insert-or-find of key u; returns the slot, *fresh = created here.
-__device__ __forceinline__ uint32_t table_insert(uint32_t* keys, uint32_t mask, uint32_t u, bool* fresh) {
+__device__ __forceinline__ uint32_t table_insert(TableSlot* tab, uint32_t mask, uint32_t u, bool* fresh) {
   uint32_t s = hash32(u) & mask;
   for (;;) {
-    uint32_t k = ld_volatile_u32(keys + s);
+    uint32_t k = ld_volatile_u32(&tab[s].key);
     if (k == u) {
       *fresh = false;
       return s;
     }
     if (k == kEmpty) {
-      uint32_t prev = atomicCAS(keys + s, kEmpty, u);
+      uint32_t prev = atomicCAS(&tab[s].key, kEmpty, u);
       if (prev == kEmpty) {
         *fresh = true;
         return s;

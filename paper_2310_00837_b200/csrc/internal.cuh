@@ -75,17 +75,24 @@ struct ScanState {
   unsigned int* counter;       // tile ticket (all-ones -> first ticket is 0)
 };
 
+// One slot of the per-batch open-addressing table (array of structs: an insert, its atomicMin and
+// the later local-id reads all touch one 16 B slot, i.e. one 32 B sector, not three arrays).
+struct alignas(16) TableSlot {
+  uint32_t key;     // vertex id, kEmpty = free
+  uint32_t minpos;  // first edge position of an id new at this hop (atomicMin)
+  uint32_t local;   // local id in N_L once assigned, kEmpty = not yet
+  uint32_t pad;
+};
+
 // Sampling workspace: one per sampling context (the graph's default context, and one per plan
 // slot so that consecutive batches can be in flight concurrently).
 struct SampleWS {
   int64_t cap_edges = 0, cap_tiles_rows = 0, cap_tiles_edges = 0, cap_seeds = 0;
   uint32_t table_size = 0;   // power of two
-  // reset region (one cudaMemsetAsync(0xFF) per batch): keys | minpos | local | scan status | counters
+  // one allocation: table | scan status | tile counters | barrier (table memset once, scan part per batch)
   char* reset_base = nullptr;
   size_t reset_bytes = 0;
-  uint32_t* keys = nullptr;
-  uint32_t* minpos = nullptr;
-  uint32_t* local = nullptr;
+  TableSlot* table = nullptr;
   ScanState row_scan[HELIOS_MAX_HOPS];
   ScanState edge_scan[HELIOS_MAX_HOPS];
   uint32_t* slot_of = nullptr;  // [cap_edges] hash slot of each sampled edge of the current hop

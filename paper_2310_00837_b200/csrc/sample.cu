@@ -54,9 +54,7 @@ struct SampleCtx {
   int64_t V;
   const int64_t* params;  // [0] key, [1] n_seeds, [2] seeds pointer (device)
   int* err;
-  uint32_t* keys;
-  uint32_t* minpos;
-  uint32_t* local;
+  TableSlot* tab;
   uint32_t mask;
   uint32_t* slot_of;
   uint32_t* node_slot;
@@ -83,13 +81,13 @@ __device__ __forceinline__ void insert_seed(const SampleCtx& c, int64_t i, const
     return;
   }
   bool fresh;
-  const uint32_t s = table_insert(c.keys, c.mask, (uint32_t)u, &fresh);
+  const uint32_t s = table_insert(c.tab, c.mask, (uint32_t)u, &fresh);
   c.node_slot[i] = s;
   if (!fresh) {
     latch(c.err, HELIOS_E_INVALID);
     return;
   }
-  c.local[s] = (uint32_t)i;
+  c.tab[s].local = (uint32_t)i;
 }
 
 // Hop h degree scan: k_i = min(deg(N_h[i]), f_h), block_indptr[h] = exclusive scan (persistent tile
@@ -150,15 +148,15 @@ __device__ __forceinline__ void dev_count_scan(const SampleCtx& c, int h) {
     const int64_t ep = c.edge_counts[h - 1];
     int32_t* __restrict__ prev = c.bi[h - 1];
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ep; e += (int64_t)gridDim.x * blockDim.x)
-      prev[e] = (int32_t)c.local[c.slot_of[e]];
+      prev[e] = (int32_t)c.tab[c.slot_of[e]].local;
   }
 }
 
 __device__ __forceinline__ void insert_edge(const SampleCtx& c, int64_t e, uint32_t u) {
   bool fresh;
-  const uint32_t s = table_insert(c.keys, c.mask, u, &fresh);
+  const uint32_t s = table_insert(c.tab, c.mask, u, &fresh);
   c.slot_of[e] = s;
-  if (fresh || ld_volatile_u32(c.local + s) == kEmpty) atomicMin(c.minpos + s, (uint32_t)e);
+  if (fresh || ld_volatile_u32(&c.tab[s].local) == kEmpty) atomicMin(&c.tab[s].minpos, (uint32_t)e);
 }
 
 // Hop h fill: one G-lane group per frontier row (G = power of two >= min(f, 32), >= 4).  Copy the
@@ -249,7 +247,7 @@ __device__ __forceinline__ void dev_assign(const SampleCtx& c, int h) {
       slot[q] = 0;
       if (e < eh) {
         slot[q] = c.slot_of[e];
-        flag[q] = (ld_volatile_u32(c.local + slot[q]) == kEmpty && c.minpos[slot[q]] == (uint32_t)e) ? 1 : 0;
+        flag[q] = (ld_volatile_u32(&c.tab[slot[q]].local) == kEmpty && c.tab[slot[q]].minpos == (uint32_t)e) ? 1 : 0;
       }
       sum += flag[q];
     }
@@ -261,9 +259,9 @@ __device__ __forceinline__ void dev_assign(const SampleCtx& c, int h) {
     for (int q = 0; q < kScanItems; q++) {
       if (flag[q]) {
         const int64_t id = nh + run;
-        c.nodes[id] = (int64_t)c.keys[slot[q]];
+        c.nodes[id] = (int64_t)c.tab[slot[q]].key;
         c.node_slot[id] = slot[q];
-        c.local[slot[q]] = (uint32_t)id;
+        c.tab[slot[q]].local = (uint32_t)id;
         run++;
       }
     }
@@ -277,7 +275,7 @@ __device__ __forceinline__ void dev_relabel(const SampleCtx& c, int h) {
   const int64_t eh = c.edge_counts[h];
   int32_t* __restrict__ bi = c.bi[h];
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < eh; e += (int64_t)gridDim.x * blockDim.x)
-    bi[e] = (int32_t)c.local[c.slot_of[e]];
+    bi[e] = (int32_t)c.tab[c.slot_of[e]].local;
 }
 
 // Returns the batch hash table to all-EMPTY by clearing exactly the slots of the batch's nodes
@@ -287,9 +285,7 @@ __device__ __forceinline__ void dev_table_clear(const SampleCtx& c) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t s = c.node_slot[i];
     if (s != kEmpty) {
-      c.keys[s] = kEmpty;
-      c.minpos[s] = kEmpty;
-      c.local[s] = kEmpty;
+      *reinterpret_cast<uint4*>(&c.tab[s]) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     }
   }
 }
@@ -480,10 +476,10 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
     return HELIOS_OK;
   HCUDA(cudaDeviceSynchronize());
   ws_free(w);
-  const size_t table_bytes = (size_t)T * 4;
+  const size_t table_bytes = (size_t)T * sizeof(TableSlot);
   const size_t status_bytes = (size_t)(tiles_r + tiles_e) * HELIOS_MAX_HOPS * 8;
   const size_t counter_bytes = (size_t)2 * HELIOS_MAX_HOPS * 4 + 8;
-  w.reset_bytes = 3 * table_bytes + status_bytes + counter_bytes;
+  w.reset_bytes = table_bytes + status_bytes + counter_bytes;
   HCUDA(cudaMalloc(&w.reset_base, w.reset_bytes));
   HCUDA(cudaMalloc(&w.slot_of, (size_t)max_e * 4));
   HCUDA(cudaMalloc(&w.node_slot, (size_t)max_nodes * 4));
@@ -497,11 +493,7 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
   w.cap_tiles_rows = tiles_r;
   w.cap_tiles_edges = tiles_e;
   char* p = w.reset_base;
-  w.keys = (uint32_t*)p;
-  p += table_bytes;
-  w.minpos = (uint32_t*)p;
-  p += table_bytes;
-  w.local = (uint32_t*)p;
+  w.table = (TableSlot*)p;
   p += table_bytes;
   w.scan_base = p;
   for (int h = 0; h < HELIOS_MAX_HOPS; h++) {
@@ -552,9 +544,7 @@ static SampleCtx make_ctx(const helios_graph* g, const SampleWS& w, const int32_
   c.V = g->V;
   c.params = w.d_params;
   c.err = g->d_err;
-  c.keys = w.keys;
-  c.minpos = w.minpos;
-  c.local = w.local;
+  c.tab = w.table;
   c.mask = w.table_size - 1;
   c.slot_of = w.slot_of;
   c.node_slot = w.node_slot;
