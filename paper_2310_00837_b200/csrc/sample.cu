@@ -469,7 +469,8 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
     tiles_r = std::max(tiles_r, (lvl[h] + kScanTile - 1) / kScanTile);
     tiles_e = std::max(tiles_e, (edg[h] + kScanTile - 1) / kScanTile);
   }
-  uint32_t T = pow2_at_least(2 * std::min<int64_t>(g->V, std::max<int64_t>(maxn, 1)));
+  // worst-case load <= 0.8 (n_L bound / table); the typical batch fills a few percent of it
+  uint32_t T = pow2_at_least(std::min<int64_t>(g->V, std::max<int64_t>(maxn, 1)) * 5 / 4);
   const int64_t max_nodes = std::max<int64_t>(maxn, 1);
   if (w.reset_base && T <= w.table_size && max_e <= w.cap_edges && tiles_r <= w.cap_tiles_rows &&
       tiles_e <= w.cap_tiles_edges && max_nodes <= w.cap_nodes && B <= w.cap_seeds)
