@@ -235,17 +235,28 @@ def main():
     ap.add_argument("--serial-gather", type=int, default=0, help="1: gathers of successive batches run one at a time")
     ap.add_argument("--host-alias", action="store_true", help="host tier = canonical table by id (no packed copy)")
     ap.add_argument("--io-rings", type=int, default=8, help="SQ/CQ ring pairs = host IO worker threads")
+    ap.add_argument("--topo-host", action="store_true",
+                    help="CSR in pinned host memory, sampled zero-copy (the paper's placement; SURVEY NEXT-2)")
+    ap.add_argument("--hbm-frac", type=float, default=-1.0, help="override the HBM-tier share of V (tier ablation)")
+    ap.add_argument("--host-frac", type=float, default=-1.0, help="override the host-tier share of V (tier ablation)")
     ap.add_argument("--host-staged", type=float, default=0.0,
                     help="share of host-tier rows copied by host stager threads (0 = pure zero-copy)")
     ap.add_argument("--stage-workers", type=int, default=8)
     ap.add_argument("--ring-depth", type=int, default=256)
     ap.add_argument("--io-ctas", type=int, default=32, help="CTA budget of each IO kernel (PAPER.md:244)")
+    ap.add_argument("--io-sync", action="store_true", help="ablation: GIDS-style coupled IO (one warp per request)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg0 = workloads.CONFIGS[args.config]
+    if args.hbm_frac >= 0 or args.host_frac >= 0:   # tier ablations
+        import dataclasses
+        cfg0 = dataclasses.replace(cfg0, hbm_frac=args.hbm_frac if args.hbm_frac >= 0 else cfg0.hbm_frac,
+                                   host_frac=args.host_frac if args.host_frac >= 0 else cfg0.host_frac,
+                                   name=f"{cfg0.name}-hbm{cfg0.hbm_frac if args.hbm_frac < 0 else args.hbm_frac:g}"
+                                        f"-host{cfg0.host_frac if args.host_frac < 0 else args.host_frac:g}")
     workdir = os.environ.get("HELIOS_BENCH_DIR", "/tmp")
     s = args.scale if args.scale > 0 else pick_scale(cfg0, world, workdir)
     cfg = workloads.scaled(cfg0, s)
@@ -317,7 +328,8 @@ def main():
     log(f"inputs {cfg.name}: V={cfg.V} E={inp.graph.E} dim={cfg.dim} gen {gen_s:.1f}s")
 
     t1 = time.time()
-    g = H.helios_graph_load(inp.graph.indptr, inp.graph.indices, device=local)
+    g = H.helios_graph_load(inp.graph.indptr, inp.graph.indices, device=local,
+                            flags=H.GRAPH_TOPO_HOST if args.topo_host else 0)
     full_batches = [b for b in inp.batches if len(b) == cfg.B]
     # presample: one epoch with presample keys, split over ranks, hotness all-reduced (NCCL)
     hot = torch.zeros(cfg.V, dtype=torch.int64, device="cuda")
@@ -338,7 +350,7 @@ def main():
                io_rings=args.io_rings, ring_depth=args.ring_depth, io_ctas=args.io_ctas) if file_cfg else {}
     if args.host_staged > 0:
         fkw.update(stage_workers=args.stage_workers, stage_frac=args.host_staged)
-    sflag = H.HOST_STAGED if args.host_staged > 0 else 0
+    sflag = (H.HOST_STAGED if args.host_staged > 0 else 0) | (H.IO_SYNC if args.io_sync else 0)
     if (args.host_alias and table is not None) or S == 0:
         c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
                                  flags=(H.HOST_ALIAS if S else 0) | sflag, **fkw)
@@ -515,7 +527,8 @@ def main():
     dominant = max(terms.items(), key=lambda x: x[1])[0]
     value = world * steps / (max_ms / 1e3)
     e2e_val = world * steps / e2e_s
-    launches_per_step = 3 * L + 2 + 2 + (3 if c.info().file_rows > 0 else 0) + (1 if args.host_staged > 0 else 0)
+    launches_per_step = (3 * L + 2 + 2 + ((2 if args.io_sync else 3) if c.info().file_rows > 0 else 0)
+                         + (1 if args.host_staged > 0 else 0))
     out = {
         "metric": "sampled+gathered mini-batches/sec (feature GB/s and tier-roofline fraction alongside)",
         "value": round(value, 3), "unit": "batches/s", "n_gpus": 1 if one_gpu else world, "steps": steps, "warmup": args.warmup,
@@ -524,7 +537,8 @@ def main():
         "data": "synthetic (seeded R-MAT-marginal power-law graph, synth_feature rows; no datasets)",
         "config": {"workload": cfg.name, "desc": cfg.note, "V": cfg.V, "E": int(inp.graph.E), "dim": cfg.dim,
                    "file_tier": {"rows": int(c.info().file_rows), "direct_io": bool(c.info().direct_io),
-                                 "io_rings": args.io_rings, "ring_depth": args.ring_depth, "io_ctas": args.io_ctas}
+                                 "io_rings": args.io_rings, "ring_depth": args.ring_depth, "io_ctas": args.io_ctas,
+                                 "io_mode": "sync (GIDS-style ablation)" if args.io_sync else "decoupled submit/complete"}
                    if file_cfg else None,
                    "batch_per_rank": cfg.B, "fanouts": cfg.fanouts, "hbm_rows_per_gpu": Hr, "host_rows": S,
                    "scale": s, "parallelism": f"dp{world} (seeds split per rank, HBM tier sharded)",
@@ -532,6 +546,8 @@ def main():
                    + (f"; {args.host_staged:.0%} of host rows staged by {args.stage_workers} host threads"
                       if args.host_staged > 0 else "; GPU zero-copy reads"),
                    "batches_in_flight": depth, "cuda_graphs": not args.no_graph, "serial_gather": bool(args.serial_gather),
+                   "topology": "pinned host, zero-copy (UVA)" if args.topo_host else "HBM",
+                   "tiers": {"hbm_frac": cfg.hbm_frac, "host_frac": cfg.host_frac},
                    "l2": "inputs larger than L2 (CSR %.1f GB, feature table %.1f GB); no flush" % (
                        (inp.graph.E * 4 + cfg.V * 8) / 1e9, cfg.V * R / 1e9)},
         "feature_gbs": round(world * n_rows / steps * R * steps / (max_ms / 1e3) / 1e9, 2),

@@ -66,9 +66,13 @@ const char* helios_last_error(void);
  *   V, E     vertex / edge counts; 1 <= V < 2^31, 0 <= E.
  *   indptr   host int64[V+1]: indptr[0] = 0, non-decreasing, indptr[V] = E  (else E_INVALID).
  *   indices  host int32[E]: neighbour ids, each in [0, V)  (else E_RANGE).  Copied.
- *   flags    reserved, pass 0.
+ *   flags    0: the CSR is copied into HBM (default);
+ *            HELIOS_GRAPH_TOPO_HOST: the CSR is copied into pinned, mapped host memory and the
+ *            sampling kernels read it zero-copy over PCIe ("the entire topology data in the CPU
+ *            cache", sampling via UVA: PAPER.md:206 §3.2.1, :215 §3.2.2).
  *   out      receives the handle (free with helios_graph_free).
  * Blocking.  Validation runs on the GPU after the copy. */
+#define HELIOS_GRAPH_TOPO_HOST 0x1u
 helios_status helios_graph_load(int device, int64_t V, int64_t E, const int64_t* indptr, const int32_t* indices,
                                 uint32_t flags, helios_graph** out);
 void helios_graph_free(helios_graph* g);
@@ -148,6 +152,8 @@ helios_status helios_presample(helios_graph* g, const int64_t* seeds, int64_t n_
 #define HELIOS_CACHE_HOST_TIER_MAPPED 0x10u /* caller-provided host_tier already registered + mapped */
 #define HELIOS_CACHE_HOST_STAGED 0x20u  /* split host-tier rows: a share is copied by host stager threads into
                                            a contiguous pinned staging buffer read sequentially by the GPU */
+#define HELIOS_CACHE_IO_SYNC 0x40u      /* ablation: GIDS/BaM-style coupled IO, one warp per request does
+                                           submit + completion poll + copy (§2.2)   */
 #define HELIOS_CACHE_IO_FAULT_AT 0x100u  /* test builds: IO workers fail the io_fault_at-th read  */
 
 typedef struct {

@@ -77,9 +77,9 @@ const char* helios_last_error(void) { return helios::g_last_error.c_str(); }
 helios_status helios_graph_load(int device, int64_t V, int64_t E, const int64_t* indptr, const int32_t* indices,
                                 uint32_t flags, helios_graph** out) {
   GUARD_BEGIN
-  (void)flags;
   HCHECK(out, HELIOS_E_INVALID, "out is NULL");
   *out = nullptr;
+  HCHECK((flags & ~HELIOS_GRAPH_TOPO_HOST) == 0, HELIOS_E_INVALID, "unknown graph flags 0x%x", flags);
   HCHECK(V >= 1 && V < (1ll << 31), HELIOS_E_INVALID, "V=%lld out of [1, 2^31)", (long long)V);
   HCHECK(E >= 0 && indptr && (E == 0 || indices), HELIOS_E_INVALID, "bad E / null arrays");
   HCHECK(indptr[0] == 0 && indptr[V] == E, HELIOS_E_INVALID, "indptr[0]=%lld indptr[V]=%lld E=%lld",
@@ -92,23 +92,45 @@ helios_status helios_graph_load(int device, int64_t V, int64_t E, const int64_t*
   g->device = device;
   g->V = V;
   g->E = E;
+  g->topo_host = (flags & HELIOS_GRAPH_TOPO_HOST) != 0;
   cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, device);
   auto cleanup = [&](helios_status st) {
-    if (g->indptr) cudaFree(g->indptr);
-    if (g->indices) cudaFree(g->indices);
+    if (g->topo_host) {
+      if (g->h_indptr) cudaFreeHost(g->h_indptr);
+      if (g->h_indices) cudaFreeHost(g->h_indices);
+    } else {
+      if (g->indptr) cudaFree(g->indptr);
+      if (g->indices) cudaFree(g->indices);
+    }
     if (g->d_err) cudaFree(g->d_err);
     delete g;
     return st;
   };
-  if (cudaMalloc(&g->indptr, (V + 1) * 8) != cudaSuccess || cudaMalloc(&g->indices, std::max<int64_t>(E, 1) * 4) != cudaSuccess ||
-      cudaMalloc(&g->d_err, sizeof(int)) != cudaSuccess) {
-    cudaGetLastError();
-    return cleanup(fail(HELIOS_E_NOMEM, "device allocation of the CSR (%lld B) failed", (long long)(V * 8 + E * 4)));
+  if (g->topo_host) {  // pinned, mapped host copy; kernels use the device aliases (zero-copy)
+    if (cudaHostAlloc(&g->h_indptr, (V + 1) * 8, cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostAlloc(&g->h_indices, std::max<int64_t>(E, 1) * 4, cudaHostAllocMapped) != cudaSuccess ||
+        cudaMalloc(&g->d_err, sizeof(int)) != cudaSuccess) {
+      cudaGetLastError();
+      return cleanup(fail(HELIOS_E_NOMEM, "pinned allocation of the CSR (%lld B) failed", (long long)(V * 8 + E * 4)));
+    }
+    memcpy(g->h_indptr, indptr, (V + 1) * 8);
+    if (E > 0) memcpy(g->h_indices, indices, E * 4);
+    if (cudaHostGetDevicePointer((void**)&g->indptr, g->h_indptr, 0) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&g->indices, g->h_indices, 0) != cudaSuccess ||
+        cudaMemset(g->d_err, 0, sizeof(int)) != cudaSuccess)
+      return cleanup(fail(HELIOS_E_CUDA, "mapping the host CSR failed: %s", cudaGetErrorString(cudaGetLastError())));
+  } else {
+    if (cudaMalloc(&g->indptr, (V + 1) * 8) != cudaSuccess ||
+        cudaMalloc(&g->indices, std::max<int64_t>(E, 1) * 4) != cudaSuccess ||
+        cudaMalloc(&g->d_err, sizeof(int)) != cudaSuccess) {
+      cudaGetLastError();
+      return cleanup(fail(HELIOS_E_NOMEM, "device allocation of the CSR (%lld B) failed", (long long)(V * 8 + E * 4)));
+    }
+    if (cudaMemcpy(g->indptr, indptr, (V + 1) * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+        (E > 0 && cudaMemcpy(g->indices, indices, E * 4, cudaMemcpyHostToDevice) != cudaSuccess) ||
+        cudaMemset(g->d_err, 0, sizeof(int)) != cudaSuccess)
+      return cleanup(fail(HELIOS_E_CUDA, "CSR upload failed: %s", cudaGetErrorString(cudaGetLastError())));
   }
-  if (cudaMemcpy(g->indptr, indptr, (V + 1) * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
-      (E > 0 && cudaMemcpy(g->indices, indices, E * 4, cudaMemcpyHostToDevice) != cudaSuccess) ||
-      cudaMemset(g->d_err, 0, sizeof(int)) != cudaSuccess)
-    return cleanup(fail(HELIOS_E_CUDA, "CSR upload failed: %s", cudaGetErrorString(cudaGetLastError())));
   helios_status st = validate_csr_device(g->indptr, g->indices, V, E, g->d_err, 0);
   if (st != HELIOS_OK) return cleanup(st);
   helios_status lat = HELIOS_OK;
@@ -126,8 +148,13 @@ void helios_graph_free(helios_graph* g) {
   if (!g) return;
   DeviceGuard dg(g->device);
   cudaDeviceSynchronize();
-  cudaFree(g->indptr);
-  cudaFree(g->indices);
+  if (g->topo_host) {
+    cudaFreeHost(g->h_indptr);
+    cudaFreeHost(g->h_indices);
+  } else {
+    cudaFree(g->indptr);
+    cudaFree(g->indices);
+  }
   cudaFree(g->d_err);
   ws_free(g->ws);
   if (g->pre_mem) cudaFree(g->pre_mem);

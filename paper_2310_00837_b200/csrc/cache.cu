@@ -235,6 +235,7 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
   c->stride = d->file_stride > 0 ? d->file_stride : c->R;
   c->io_ctas = d->io_ctas > 0 ? d->io_ctas : 32;
   c->staged = (d->flags & HELIOS_CACHE_HOST_STAGED) != 0;
+  c->io_sync = (d->flags & HELIOS_CACHE_IO_SYNC) != 0;
   c->stage_workers = d->stage_workers > 0 ? d->stage_workers : 8;
   c->stage_frac = d->stage_frac > 0.f ? std::min(d->stage_frac, 1.0f) : 0.6f;
   const int64_t V = c->V;

@@ -372,6 +372,69 @@ __global__ void __launch_bounds__(256) k_io_complete(IoArgs a) {
   }
 }
 
+// Ablation (HELIOS_CACHE_IO_SYNC): the synchronous IO stack the paper measures GIDS/BaM with
+// (§2.2, Fig. iostack_bam): each warp owns one request end to end — its leader
+// reserves a ring slot and submits, the warp then spins on the completion and finally copies the
+// row — so a warp is tied up for the whole IO latency and at most one request per warp is in
+// flight.  Same rings and host workers as the decoupled k_io_submit / k_io_complete pair.
+__global__ void __launch_bounds__(256) k_io_sync(IoArgs a) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long M = a.ctl[kListFile];
+  const int nvec = a.R >> 4;
+  const uint64_t t0 = globaltimer();
+  for (;;) {
+    unsigned long long m = 0;
+    if (lane == 0) m = atomicAdd(&a.ctl[kCtlSubmit], 1ull);
+    m = __shfl_sync(0xFFFFFFFFu, m, 0);
+    if (m >= M) break;
+    const int r = (int)(m % a.rings);
+    const uint32_t p = (uint32_t)(m / a.rings);
+    const uint32_t seq = a.base_seq[r] + p + 1u;
+    const uint32_t slot = (seq - 1u) & (uint32_t)(a.depth - 1);
+    const int64_t idx = (int64_t)r * a.depth + slot;
+    bool ok = true;
+    if (lane == 0) {
+      while ((int32_t)(seq - (uint32_t)a.depth - ld_acquire_gpu_u32(a.free_seq + idx)) > 0) {
+        if (globaltimer() - t0 > kWatchdogNs) {
+          ok = false;
+          break;
+        }
+        __nanosleep(256);
+      }
+      if (ok) {
+        SqEntry* e = a.sq + idx;
+        e->file_off = (uint64_t)(a.header + (int64_t)(a.miss_w[m] & ((1ull << 56) - 1)) * a.stride);
+        e->len = (uint32_t)a.len;
+        e->slot = (uint32_t)idx;
+        e->out_row = (uint64_t)a.miss_out[m];
+        __threadfence_system();
+        st_release_sys_u32(&e->seq, seq);
+      }
+    }
+    ok = __shfl_sync(0xFFFFFFFFu, ok, 0);
+    while (ok && ld_acquire_sys_u32(&a.cq[idx].seq) != seq) {
+      if (globaltimer() - t0 > kWatchdogNs) ok = false;
+      else __nanosleep(128);
+    }
+    if (!__all_sync(0xFFFFFFFFu, ok)) {
+      if (lane == 0) latch(a.err, HELIOS_E_TIMEOUT);
+      break;
+    }
+    if (*(volatile const int32_t*)&a.cq[idx].status != 0) {
+      if (lane == 0) latch(a.err, HELIOS_E_IO);
+    } else {
+      const int4* s = (const int4*)(a.staging + idx * a.slot_bytes);
+      int4* d = (int4*)(a.out + a.miss_out[m] * (int64_t)a.R);
+      for (int k = lane; k < nvec; k += 32) d[k] = ld_volatile_v4(s + k);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      st_release_gpu_u32(a.free_seq + idx, seq);
+    }
+  }
+}
+
 __global__ void k_io_finish(unsigned long long* ctl, uint32_t* base_seq, int rings) {
   const unsigned long long M = ctl[kListFile];
   for (int r = threadIdx.x; r < rings; r += blockDim.x)
@@ -385,6 +448,7 @@ helios_status io_preload_kernels() {
   HCUDA(cudaFuncGetAttributes(&fa, k_io_submit));
   HCUDA(cudaFuncGetAttributes(&fa, k_io_complete));
   HCUDA(cudaFuncGetAttributes(&fa, k_io_finish));
+  HCUDA(cudaFuncGetAttributes(&fa, k_io_sync));
   return HELIOS_OK;
 }
 
@@ -518,8 +582,12 @@ helios_status io_launch(helios_cache* c, GatherWS& w, void* out, cudaStream_t st
     HCUDA(cudaStreamWaitEvent(c->s_submit, c->ev_io_done, 0));
     HCUDA(cudaStreamWaitEvent(c->s_complete, c->ev_io_done, 0));
   }
-  k_io_complete<<<c->io_ctas, 256, 0, c->s_complete>>>(io);
-  k_io_submit<<<c->io_ctas, 256, 0, c->s_submit>>>(io);
+  if (c->io_sync) {
+    k_io_sync<<<c->io_ctas, 256, 0, c->s_complete>>>(io);
+  } else {
+    k_io_complete<<<c->io_ctas, 256, 0, c->s_complete>>>(io);
+    k_io_submit<<<c->io_ctas, 256, 0, c->s_submit>>>(io);
+  }
   HCUDA(cudaGetLastError());
   HCUDA(cudaEventRecord(c->ev_submit, c->s_submit));
   HCUDA(cudaEventRecord(c->ev_complete, c->s_complete));

@@ -150,8 +150,11 @@ struct helios_graph {
   int device = 0;
   int sms = 148;
   int64_t V = 0, E = 0;
-  int64_t* indptr = nullptr;   // device [V+1]
+  int64_t* indptr = nullptr;   // device [V+1] (device alias of pinned host memory with TOPO_HOST)
   int32_t* indices = nullptr;  // device [E]
+  bool topo_host = false;      // CSR lives in pinned host memory (h_indptr / h_indices)
+  int64_t* h_indptr = nullptr;
+  int32_t* h_indices = nullptr;
   int* d_err = nullptr;        // device latched error (0 = none)
   helios::SampleWS ws;
   // presample scratch (lazily allocated)
@@ -227,6 +230,7 @@ struct helios_cache {
   std::string path;
   int64_t header = 0, stride = 0;
   int io_ctas = 32;
+  bool io_sync = false;            // HELIOS_CACHE_IO_SYNC ablation
   helios::IoRings io;
   bool has_file = false;
   // host staging (HELIOS_CACHE_HOST_STAGED)

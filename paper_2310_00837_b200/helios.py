@@ -25,7 +25,7 @@ MAX_HOPS = 8
 MAX_RANKS = 64
 STATUS = ["OK", "E_INVALID", "E_RANGE", "E_CAPACITY", "E_NOMEM", "E_CUDA", "E_IO", "E_TIMEOUT", "E_STATE"]
 HOST_ALIAS, TABLE_MAPPED, NO_DIRECT_IO, IO_FAULT_AT = 0x1, 0x2, 0x4, 0x100
-HOST_FILL, HOST_TIER_MAPPED, HOST_STAGED = 0x8, 0x10, 0x20
+HOST_FILL, HOST_TIER_MAPPED, HOST_STAGED, IO_SYNC = 0x8, 0x10, 0x20, 0x40
 PLAN_NO_GRAPH, PLAN_SERIAL_GATHER = 0x1, 0x2
 SUBMIT_SEEDS_HOST, SUBMIT_TIMING = 0x1, 0x2
 
@@ -142,12 +142,15 @@ class Graph:
             pass
 
 
-def helios_graph_load(indptr: np.ndarray, indices: np.ndarray, device: int = 0) -> Graph:
+GRAPH_TOPO_HOST = 0x1
+
+
+def helios_graph_load(indptr: np.ndarray, indices: np.ndarray, device: int = 0, flags: int = 0) -> Graph:
     indptr = np.ascontiguousarray(indptr, dtype=np.int64)
     indices = np.ascontiguousarray(indices, dtype=np.int32)
     V, E = len(indptr) - 1, len(indices)
     h = vp()
-    _check(_lib.helios_graph_load(device, V, E, _ptr(indptr), _ptr(indices) if E else None, 0, ctypes.byref(h)),
+    _check(_lib.helios_graph_load(device, V, E, _ptr(indptr), _ptr(indices) if E else None, flags, ctypes.byref(h)),
            "helios_graph_load")
     return Graph(h.value, V, E, device)
 

@@ -105,18 +105,21 @@ def test_gather_row_sizes(H, tmp_path, dim):
     c.free()
 
 
-def test_io_ring_wraparound_and_fault(H, c1, c1_hot):
+@pytest.mark.parametrize("sync", [False, True])
+def test_io_ring_wraparound_and_fault(H, c1, c1_hot, sync):
     g, hot = c1_hot
     cfg = c1.cfg
+    sf = H.IO_SYNC if sync else 0
     c = H.helios_cache_build(g, hot, cfg.R, 0, 0, host_table=None, feature_path=c1.feature_path,
-                             header_bytes=c1.header, file_stride=c1.stride, ring_depth=2, io_rings=2, io_ctas=2)
+                             header_bytes=c1.header, file_stride=c1.stride, ring_depth=2, io_rings=2, io_ctas=2,
+                             flags=sf)
     nodes = np.random.default_rng(9).permutation(cfg.V)[:3000]
     gather_and_check(H, c, c1, nodes, np.array([0, 0, 0, 3000]))
     gather_and_check(H, c, c1, nodes[::-1].copy(), np.array([0, 0, 0, 3000]))   # sequences continue across batches
     c.free()
     c = H.helios_cache_build(g, hot, cfg.R, 0, 0, host_table=None, feature_path=c1.feature_path,
                              header_bytes=c1.header, file_stride=c1.stride, ring_depth=8, io_rings=2,
-                             flags=H.IO_FAULT_AT, io_fault_at=17)
+                             flags=H.IO_FAULT_AT | sf, io_fault_at=17)
     out = torch.empty((3000, cfg.R), dtype=torch.uint8, device="cuda")
     H.helios_gather(c, torch.as_tensor(nodes).cuda(), torch.tensor([3000], device="cuda"), out)
     with pytest.raises(H.HeliosError) as e:

@@ -140,3 +140,26 @@ def test_persistent_sampler_parity(H, medium, monkeypatch):
         orc = oracle.sample(medium.indptr, medium.indices, seeds, fan, 991)
         assert_same(gpu, orc, len(fan))
     g.free()
+
+
+def test_host_resident_topology(H, medium, c1):
+    """HELIOS_GRAPH_TOPO_HOST: the CSR in pinned host memory, sampled zero-copy over
+    PCIe — same bit-exact batches and presample hotness."""
+    g = H.helios_graph_load(medium.indptr, medium.indices, flags=H.GRAPH_TOPO_HOST)
+    rng = np.random.default_rng(11)
+    for B, fan in ((1024, [15, 10, 5]), (50, [-1, 3])):
+        seeds = rng.choice(medium.V, B, replace=False)
+        gpu = run_gpu(H, g, seeds, fan, 5)
+        assert_same(gpu, oracle.sample(medium.indptr, medium.indices, seeds, fan, 5), len(fan))
+    g.free()
+    cfg = c1.cfg
+    g = H.helios_graph_load(c1.graph.indptr, c1.graph.indices, flags=H.GRAPH_TOPO_HOST)
+    keys = workloads.presample_keys(len(c1.batches))
+    hot = torch.zeros(cfg.V, dtype=torch.int64, device="cuda")
+    H.helios_presample(g, torch.as_tensor(np.concatenate(c1.batches)).cuda(), cfg.B, cfg.fanouts, keys, hot)
+    H.helios_graph_sync(g)
+    ref = oracle.presample(c1.graph.indptr, c1.graph.indices, c1.batches, keys, cfg.fanouts)
+    assert np.array_equal(hot.cpu().numpy().astype(np.uint64), ref)
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_graph_load(c1.graph.indptr, c1.graph.indices, flags=0x80)
+    assert e.value.name == "E_INVALID"
