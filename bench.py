@@ -233,6 +233,7 @@ def main():
     ap.add_argument("--depth", type=int, default=6, help="batches in flight (plan slots)")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly instead of CUDA graphs")
     ap.add_argument("--serial-gather", type=int, default=0, help="1: gathers of successive batches run one at a time")
+    ap.add_argument("--intra", action="store_true", help="intra-batch pipeline: per-hop gather passes (NEXT-1)")
     ap.add_argument("--host-alias", action="store_true", help="host tier = canonical table by id (no packed copy)")
     ap.add_argument("--io-rings", type=int, default=8, help="SQ/CQ ring pairs = host IO worker threads")
     ap.add_argument("--topo-host", action="store_true",
@@ -383,7 +384,8 @@ def main():
     seed_of = {b: torch.as_tensor(inp.batches[b]).cuda() for b in sorted(set(seq))}
     stream = torch.cuda.current_stream()
     depth = args.depth
-    pflags = (H.PLAN_NO_GRAPH if args.no_graph else 0) | (H.PLAN_SERIAL_GATHER if args.serial_gather else 0)
+    pflags = ((H.PLAN_NO_GRAPH if args.no_graph else 0) | (H.PLAN_SERIAL_GATHER if args.serial_gather else 0)
+              | (H.PLAN_INTRA_BATCH if args.intra else 0))
     plan = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=depth, flags=pflags)
 
     for i in range(args.warmup):
@@ -546,6 +548,7 @@ def main():
                    + (f"; {args.host_staged:.0%} of host rows staged by {args.stage_workers} host threads"
                       if args.host_staged > 0 else "; GPU zero-copy reads"),
                    "batches_in_flight": depth, "cuda_graphs": not args.no_graph, "serial_gather": bool(args.serial_gather),
+                   "intra_batch_pipeline": bool(args.intra),
                    "topology": "pinned host, zero-copy (UVA)" if args.topo_host else "HBM",
                    "tiers": {"hbm_frac": cfg.hbm_frac, "host_frac": cfg.host_frac},
                    "l2": "inputs larger than L2 (CSR %.1f GB, feature table %.1f GB); no flush" % (

@@ -235,12 +235,17 @@ helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64
  *   desc.L, fanouts  hops and fanouts (as helios_sample).
  *   desc.depth       number of slots, 1..8.
  *   desc.flags       HELIOS_PLAN_NO_GRAPH: launch the kernels directly on every submit;
- *                    HELIOS_PLAN_SERIAL_GATHER: chain the gathers of successive submits.
+ *                    HELIOS_PLAN_SERIAL_GATHER: chain the gathers of successive submits;
+ *                    HELIOS_PLAN_INTRA_BATCH: per-hop gather passes overlapping the sampling.
  *   c                cache, or NULL for a sampling-only plan (no features / stats).
  * Blocking create/free. */
 #define HELIOS_PLAN_NO_GRAPH 0x1u
 #define HELIOS_PLAN_SERIAL_GATHER 0x2u  /* gathers of successive batches run one at a time (sampling
                                            still overlaps): the link is not split between gathers */
+#define HELIOS_PLAN_INTRA_BATCH 0x4u    /* intra-batch pipeline: a lookup + gather pass
+                                           per new node range (N_0, then N_{h+1} \ N_h) forks onto a
+                                           side stream while the next hop samples; timed submits then
+                                           report the whole batch as the sampling phase */
 #define HELIOS_SUBMIT_SEEDS_HOST 0x1u  /* seeds pointer is host memory (copied with the parameters, H2D) */
 #define HELIOS_SUBMIT_TIMING 0x2u      /* record device timing events around the sample / gather phases */
 typedef struct helios_plan helios_plan;

@@ -403,6 +403,8 @@ helios_status helios_plan_create(helios_graph* g, helios_cache* c, const helios_
   p->d = *d;
   p->graphs = !(d->flags & HELIOS_PLAN_NO_GRAPH);
   p->serial_gather = (d->flags & HELIOS_PLAN_SERIAL_GATHER) != 0;
+  p->intra = (d->flags & HELIOS_PLAN_INTRA_BATCH) != 0;
+  HCHECK(!p->intra || p->graphs, HELIOS_E_INVALID, "HELIOS_PLAN_INTRA_BATCH needs CUDA graphs");
   helios_status st = plan_create_impl(p);
   if (st != HELIOS_OK) {
     std::string keep = helios_last_error();

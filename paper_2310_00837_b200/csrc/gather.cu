@@ -33,18 +33,21 @@ struct ListPtrs {
 
 // K3: one thread per row of N_L: dir[v] -> tier list (local HBM / peer HBM / host / file), appended
 // with warp-aggregated atomics.  The list counts are the per-tier row counts.
-__global__ void __launch_bounds__(256) k_lookup(const int64_t* __restrict__ nodes, const int64_t* __restrict__ n_nodes,
+// Rows [*lo, *hi) of N_L (lo = NULL: from 0); the intra-batch pipeline runs one pass per node range.
+__global__ void __launch_bounds__(256) k_lookup(const int64_t* __restrict__ nodes, const int64_t* __restrict__ lo_ptr,
+                                                const int64_t* __restrict__ n_nodes,
                                                 const int64_t* __restrict__ dir, int32_t rank, ListPtrs L,
                                                 unsigned long long* ctl) {
   pdl_trigger();
   const int lane = threadIdx.x & 31;
-  const int64_t n = *n_nodes;
+  const int64_t lo = lo_ptr ? *lo_ptr : 0;
+  const int64_t n = *n_nodes - lo;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < n; base += stride) {
-    const int64_t i = base + lane;
+    const int64_t i = lo + base + lane;
     int t = -1;
     uint64_t w = 0;
-    if (i < n) {
+    if (base + lane < n) {
       w = (uint64_t)dir[nodes[i]];
       const uint32_t tier = (uint32_t)(w >> 62);
       t = tier == 0 ? ((int)((w >> 56) & 63) == rank ? kListLocal : kListPeer) : (tier == 1 ? kListHost : kListFile);
@@ -97,6 +100,7 @@ struct GatherArgs {
   ListPtrs L;
   const unsigned long long* ctl;
   bool staged;
+  bool accumulate;          // intra-batch passes: add this pass's row counts to stats
   const char* stage;        // device alias of the pinned staging rows
   const uint32_t* done;     // device alias of the per-chunk completion flags
   int* err;
@@ -176,10 +180,16 @@ __global__ void __launch_bounds__(256, 4) k_gather_lists(GatherArgs a) {
   const int64_t n_gpu = a.staged ? (int64_t)a.ctl[kCtlStageGpu] : n_host;
   const int64_t n_stage = n_host - n_gpu;
   if (a.stats && gw == 0 && lane == 0) {
-    a.stats->rows_hbm_local = n_local;
-    a.stats->rows_hbm_peer = n_peer;
-    a.stats->rows_host = n_host;
-    a.stats->rows_file = (int64_t)a.ctl[kListFile];
+    if (a.accumulate) {
+      a.stats->rows_hbm_local += n_local;
+      a.stats->rows_hbm_peer += n_peer;
+      a.stats->rows_host += n_host;
+    } else {
+      a.stats->rows_hbm_local = n_local;
+      a.stats->rows_hbm_peer = n_peer;
+      a.stats->rows_host = n_host;
+    }
+    a.stats->rows_file = (int64_t)a.ctl[kListFile];  // the file list accumulates over passes
   }
   // warp roles: r = gw % 8.  r == 0: zero-copy host rows [0, n_gpu); r == 1 (staged mode): stage
   // consumers for rows [n_gpu, n_host); other warps: peer then local HBM rows.
@@ -510,13 +520,14 @@ helios_status gws_ensure(helios_cache* c, GatherWS& w, int64_t max_nodes) {
   return HELIOS_OK;
 }
 
-helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes,
-                            void* out, helios_gather_stats* stats, cudaStream_t st) {
-  HCHECK(nodes && n_nodes && (out || max_nodes == 0), HELIOS_E_INVALID, "null gather argument");
-  HCHECK(c->G == 1 || c->peers_attached, HELIOS_E_STATE, "world_size %d but peers not attached", c->G);
-  HCHECK(w.d_ctl && max_nodes <= w.cap, HELIOS_E_CAPACITY, "max_nodes %lld > gather list cap %lld",
-         (long long)max_nodes, (long long)w.cap);
-  HCUDA(cudaMemsetAsync(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long), st));
+// One lookup + gather pass over rows [*lo, *n_nodes) (lo = NULL: all).  first: reset every count;
+// otherwise (later intra-batch passes) only the per-pass tier counts are reset, so the file list and
+// the stats accumulate over the passes of a batch.
+static helios_status gather_pass(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* lo,
+                                 const int64_t* n_nodes, int64_t max_rows, void* out, helios_gather_stats* stats,
+                                 bool first, bool accumulate, cudaStream_t st) {
+  if (first) HCUDA(cudaMemsetAsync(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long), st));
+  else HCUDA(cudaMemsetAsync(w.d_ctl, 0, kListFile * sizeof(unsigned long long), st));
   ListPtrs L;
   for (int q = 0; q < kLists; q++) {
     L.i[q] = w.d_list_i + q * w.cap;
@@ -527,8 +538,8 @@ helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, 
     L.i[kListHost] = w.d_host_i;
     L.w[kListHost] = w.d_host_w;
   }
-  const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_nodes + 255) / 256), (int64_t)c->sms * 2);
-  k_lookup<<<lg, 256, 0, st>>>(nodes, n_nodes, c->dir, c->rank, L, w.d_ctl);
+  const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_rows + 255) / 256), (int64_t)c->sms * 2);
+  k_lookup<<<lg, 256, 0, st>>>(nodes, lo, n_nodes, c->dir, c->rank, L, w.d_ctl);
   if (staged) launch_pdl(k_stage_publish, dim3(1), dim3(1), st, w.d_ctl, w.d_seq, w.d_mail, c->stage_frac, kStageCapRows);
   GatherArgs a;
   a.out = (char*)out;
@@ -536,6 +547,7 @@ helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, 
   a.L = L;
   a.ctl = w.d_ctl;
   a.staged = staged;
+  a.accumulate = accumulate;
   a.stage = w.d_stage;
   a.done = w.d_done;
   a.err = c->d_err;
@@ -550,6 +562,22 @@ helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, 
   else launch_gather<8, 1, 1>(a, c->sms, st);
   HCUDA(cudaGetLastError());
   return HELIOS_OK;
+}
+
+helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes,
+                            void* out, helios_gather_stats* stats, cudaStream_t st) {
+  HCHECK(nodes && n_nodes && (out || max_nodes == 0), HELIOS_E_INVALID, "null gather argument");
+  HCHECK(c->G == 1 || c->peers_attached, HELIOS_E_STATE, "world_size %d but peers not attached", c->G);
+  HCHECK(w.d_ctl && max_nodes <= w.cap, HELIOS_E_CAPACITY, "max_nodes %lld > gather list cap %lld",
+         (long long)max_nodes, (long long)w.cap);
+  return gather_pass(c, w, nodes, nullptr, n_nodes, max_nodes, out, stats, true, false, st);
+}
+
+helios_status gather_range_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* lo,
+                                  const int64_t* hi, int64_t max_rows, void* out, helios_gather_stats* stats, bool first,
+                                  cudaStream_t st) {
+  HCHECK(c->G == 1 || c->peers_attached, HELIOS_E_STATE, "world_size %d but peers not attached", c->G);
+  return gather_pass(c, w, nodes, lo, hi, max_rows, out, stats, first, true, st);
 }
 
 // K5 / K6 on the cache's IO streams for the misses recorded in w by the preceding gather_launch on

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <functional>
 #include <utility>
 #include <cstdint>
 #include <cstdio>
@@ -257,6 +258,9 @@ struct PlanSlot {
   cudaStream_t stream = nullptr;
   cudaGraphExec_t g_sample = nullptr, g_gather = nullptr, g_all = nullptr;
   cudaEvent_t ev_caller = nullptr, ev_end = nullptr;
+  cudaStream_t s_side = nullptr;                        // intra-batch gather passes
+  cudaEvent_t ev_fork[HELIOS_MAX_HOPS + 1] = {};
+  cudaEvent_t ev_join = nullptr;
   static constexpr int kRing = 256;
   std::vector<cudaEvent_t> ring;  // kRing x {start, mid, end} timing events (timed submits only)
   int64_t count = 0;              // batches submitted to this slot
@@ -273,6 +277,7 @@ struct helios_plan {
   int64_t maxn = 0;
   bool graphs = true;
   bool serial_gather = false;
+  bool intra = false;  // HELIOS_PLAN_INTRA_BATCH
   cudaEvent_t ev_gather_chain = nullptr;  // last gather submitted (HELIOS_PLAN_SERIAL_GATHER)
   bool gather_chained = false;
   std::vector<helios::PlanSlot> slots;
@@ -292,8 +297,11 @@ void ws_free(SampleWS& w);
 helios_status ws_upload_params(SampleWS& w, uint64_t key, int64_t B, const int64_t* seeds, bool seeds_host,
                                cudaStream_t st);
 // Enqueues the sampling kernels; they read key / n_seeds / seeds from w.d_params.  B_max sizes the grids.
+// stage_hook (optional, multi-kernel path): called after the stream position where N_0 (stage 0) or
+// N_{h+1} (stage h+1) is final, to fork per-range work (the intra-batch pipeline).
 helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const int32_t* fanouts, int32_t L,
-                            const helios_blocks* out, cudaStream_t st);
+                            const helios_blocks* out, cudaStream_t st,
+                            const std::function<helios_status(int)>* stage_hook = nullptr);
 helios_status hot_count_enqueue(const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, uint64_t* hot,
                                 int sms, cudaStream_t st);
 helios_status gws_ensure(helios_cache* c, GatherWS& w, int64_t max_nodes);
@@ -302,6 +310,11 @@ void gws_free(GatherWS& w);
 // file list for io_launch.
 helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes,
                             void* out, helios_gather_stats* stats, cudaStream_t st);
+// Intra-batch pipeline pass: lookup + gather of rows [*lo, *hi) (lo = NULL: from 0); stats
+// accumulate, the file list accumulates (first = true resets everything).
+helios_status gather_range_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* lo,
+                                  const int64_t* hi, int64_t max_rows, void* out, helios_gather_stats* stats, bool first,
+                                  cudaStream_t st);
 // IO rings for the misses of the last gather_launch on `st` (not capturable: cross-stream events).
 helios_status io_launch(helios_cache* c, GatherWS& w, void* out, cudaStream_t st);
 helios_status validate_csr_device(const int64_t* indptr, const int32_t* indices, int64_t V, int64_t E, int* d_flag,

@@ -29,6 +29,10 @@ void plan_free_impl(helios_plan* p) {
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : s.ring)
       if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : s.ev_fork)
+      if (e) cudaEventDestroy(e);
+    if (s.ev_join) cudaEventDestroy(s.ev_join);
+    if (s.s_side) cudaStreamDestroy(s.s_side);
     if (s.stream) cudaStreamDestroy(s.stream);
   }
   p->slots.clear();
@@ -110,10 +114,32 @@ helios_status plan_create_impl(helios_plan* p) {
         s = capture(sl.stream, &sl.g_gather, gather_ops);
         if (s != HELIOS_OK) return s;
       }
-      s = capture(sl.stream, &sl.g_all, [&]() {  // the whole batch in one graph (untimed submits)
-        helios_status r = sample_ops();
-        return (r == HELIOS_OK && p->c) ? gather_ops() : r;
-      });
+      if (p->intra && p->c) {
+        // intra-batch pipeline: a lookup+gather pass per new node range forks
+        // onto the side stream as soon as that range is final, while the next hop samples
+        HCUDA(cudaStreamCreateWithFlags(&sl.s_side, cudaStreamNonBlocking));
+        for (auto& e : sl.ev_fork) HCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        HCUDA(cudaEventCreateWithFlags(&sl.ev_join, cudaEventDisableTiming));
+        std::function<helios_status(int)> hook = [&](int stage) -> helios_status {
+          HCUDA(cudaEventRecord(sl.ev_fork[stage], sl.stream));
+          HCUDA(cudaStreamWaitEvent(sl.s_side, sl.ev_fork[stage], 0));
+          const int64_t* lo = stage == 0 ? nullptr : sl.blocks.level_counts + stage - 1;
+          return gather_range_launch(p->c, sl.gws, sl.blocks.nodes, lo, sl.blocks.level_counts + stage,
+                                     sl.blocks.nodes_cap, sl.feats, sl.stats, stage == 0, sl.s_side);
+        };
+        s = capture(sl.stream, &sl.g_all, [&]() -> helios_status {
+          HCUDA(cudaMemsetAsync(sl.stats, 0, sizeof(helios_gather_stats), sl.stream));
+          helios_status r = sample_launch(g, sl.ws, d.max_seeds, d.fanouts, d.L, &sl.blocks, sl.stream, &hook);
+          HCUDA(cudaEventRecord(sl.ev_join, sl.s_side));
+          HCUDA(cudaStreamWaitEvent(sl.stream, sl.ev_join, 0));
+          return r;
+        });
+      } else {
+        s = capture(sl.stream, &sl.g_all, [&]() {  // the whole batch in one graph (untimed submits)
+          helios_status r = sample_ops();
+          return (r == HELIOS_OK && p->c) ? gather_ops() : r;
+        });
+      }
       if (s != HELIOS_OK) return s;
     }
   }
@@ -135,8 +161,11 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
   const bool timed = (flags & HELIOS_SUBMIT_TIMING) != 0;
   cudaEvent_t* ev = &sl.ring[3 * (sl.tcount % PlanSlot::kRing)];
   if (timed) HCUDA(cudaEventRecord(ev[0], sl.stream));
-  const bool chain = p->serial_gather && p->c;
-  if (p->graphs && !timed && !chain) {
+  const bool chain = p->serial_gather && p->c && !p->intra;
+  if (p->graphs && p->intra && p->c) {  // one graph; timed submits time the whole overlapped batch
+    HCUDA(cudaGraphLaunch(sl.g_all, sl.stream));
+    if (timed) HCUDA(cudaEventRecord(ev[1], sl.stream));
+  } else if (p->graphs && !timed && !chain) {
     HCUDA(cudaGraphLaunch(sl.g_all, sl.stream));
   } else {
     if (p->graphs) {

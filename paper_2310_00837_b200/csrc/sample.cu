@@ -581,13 +581,13 @@ static int persistent_grid(int sms) {
 }
 
 helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const int32_t* fanouts, int32_t L,
-                            const helios_blocks* out, cudaStream_t st) {
+                            const helios_blocks* out, cudaStream_t st, const std::function<helios_status(int)>* hook) {
   int64_t maxn, lvl[HELIOS_MAX_HOPS + 1], edg[HELIOS_MAX_HOPS];
   helios_status s = sample_bounds(B_max, fanouts, L, g->V, g->E, &maxn, lvl, edg);
   if (s != HELIOS_OK) return s;
   const SampleCtx c = make_ctx(g, w, fanouts, L, out);
   HCUDA(cudaMemsetAsync(w.scan_base, 0xFF, w.scan_bytes, st));
-  if (w.persistent) {
+  if (w.persistent && !hook) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(persistent_grid(g->sms));
     cfg.blockDim = dim3(256);
@@ -607,14 +607,25 @@ helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const i
     // persistent tile loops: a grid of at most one CTA per SM, tiles taken by ticket
     const int rt = (int)std::min<int64_t>(std::max<int64_t>(1, (lvl[h] + kScanTile - 1) / kScanTile), g->sms);
     // hop 0: enough CTAs for one seed insert per thread (the scan itself uses ceil(B/tile) tiles)
-    if (h == 0) k_count_scan<<<std::max<int>(rt, (int)std::min<int64_t>((B_max + 255) / 256, g->sms)), kScanBlock, 0, st>>>(c, 0);
-    else launch_pdl(k_count_scan, dim3(rt), dim3(kScanBlock), st, c, h);
+    if (h == 0) {
+      k_count_scan<<<std::max<int>(rt, (int)std::min<int64_t>((B_max + 255) / 256, g->sms)), kScanBlock, 0, st>>>(c, 0);
+      if (hook) {
+        helios_status hs = (*hook)(0);
+        if (hs != HELIOS_OK) return hs;
+      }
+    } else {
+      launch_pdl(k_count_scan, dim3(rt), dim3(kScanBlock), st, c, h);
+    }
     if (f < 0 || f > 16) launch_fill<32>(g, c, h, lvl[h], st);
     else if (f > 8) launch_fill<16>(g, c, h, lvl[h], st);
     else if (f > 4) launch_fill<8>(g, c, h, lvl[h], st);
     else launch_fill<4>(g, c, h, lvl[h], st);
     const int et = (int)std::min<int64_t>(std::max<int64_t>(1, (edg[h] + kScanTile - 1) / kScanTile), g->sms);
     launch_pdl(k_dedup_assign, dim3(et), dim3(kScanBlock), st, c, h);
+    if (hook) {
+      helios_status hs = (*hook)(h + 1);
+      if (hs != HELIOS_OK) return hs;
+    }
   }
   if (L > 0) {
     const int ge = (int)std::min<int64_t>(std::max<int64_t>(1, (edg[L - 1] + 255) / 256), (int64_t)g->sms * 2);

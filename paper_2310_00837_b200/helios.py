@@ -26,7 +26,7 @@ MAX_RANKS = 64
 STATUS = ["OK", "E_INVALID", "E_RANGE", "E_CAPACITY", "E_NOMEM", "E_CUDA", "E_IO", "E_TIMEOUT", "E_STATE"]
 HOST_ALIAS, TABLE_MAPPED, NO_DIRECT_IO, IO_FAULT_AT = 0x1, 0x2, 0x4, 0x100
 HOST_FILL, HOST_TIER_MAPPED, HOST_STAGED, IO_SYNC = 0x8, 0x10, 0x20, 0x40
-PLAN_NO_GRAPH, PLAN_SERIAL_GATHER = 0x1, 0x2
+PLAN_NO_GRAPH, PLAN_SERIAL_GATHER, PLAN_INTRA_BATCH = 0x1, 0x2, 0x4
 SUBMIT_SEEDS_HOST, SUBMIT_TIMING = 0x1, 0x2
 
 i64, i32, u32, u64, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p

@@ -54,7 +54,9 @@ def check_slot(p, slot, inp, seeds, key, dref):
 
 @pytest.mark.parametrize("depth,flags,host_seeds,staged", [(2, 0, False, False), (1, 0, True, False),
                                                           (3, 0, False, False), (2, 1, True, False),
-                                                          (3, 0, False, True), (1, 1, True, True)])
+                                                          (3, 0, False, True), (1, 1, True, True),
+                                                          (1, 4, False, False), (3, 4, True, False),
+                                                          (2, 4, False, True), (2, 2, False, False)])
 def test_plan_c1_epoch(H, c1, depth, flags, host_seeds, staged):
     cfg = c1.cfg
     Hr, S = workloads.tier_rows(cfg)
