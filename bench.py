@@ -581,6 +581,8 @@ def main():
     }
     if rank == 0:
         print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()   # no rank frees its HBM shard while another may still read it over NVLink
     plan.free()
     c.free()
     g.free()

@@ -279,7 +279,8 @@ helios_status helios_plan_wait(helios_plan* p, int32_t slot, void* stream);
 helios_status helios_plan_timing(helios_plan* p, int32_t slot, int32_t back, float* sample_ms, float* gather_ms);
 
 /* Waits for `stream` and the cache's IO streams; returns and clears latched errors of the cache
- * and its graph (E_IO, E_TIMEOUT, E_INVALID, E_RANGE). */
+ * and its graph (E_IO, E_TIMEOUT, E_INVALID, E_RANGE).  After E_TIMEOUT the cache's ring state is
+ * inconsistent and every later gather returns E_STATE (rebuild the cache). */
 helios_status helios_sync(helios_cache* c, void* stream);
 
 #ifdef __cplusplus

@@ -471,6 +471,7 @@ helios_status helios_sync(helios_cache* c, void* stream) {
   st = read_latched(c->g->d_err, &b);
   if (st != HELIOS_OK) return st;
   int host = c->io.host_err.exchange(0);
+  if (a == HELIOS_E_TIMEOUT) c->broken = true;  // ring sequences / staging hand-offs are out of step
   if (a != HELIOS_OK) return fail(a, "latched cache error %d (IO failure or ring watchdog)", (int)a);
   if (host != 0) return fail((helios_status)host, "IO worker reported error %d", host);
   if (b != HELIOS_OK) return fail(b, "latched sampling error %d (seed out of range / duplicate seed)", (int)b);

@@ -526,6 +526,7 @@ helios_status gws_ensure(helios_cache* c, GatherWS& w, int64_t max_nodes) {
 static helios_status gather_pass(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* lo,
                                  const int64_t* n_nodes, int64_t max_rows, void* out, helios_gather_stats* stats,
                                  bool first, bool accumulate, cudaStream_t st) {
+  HCHECK(!c->broken, HELIOS_E_STATE, "cache unusable after an IO / staging watchdog timeout");
   if (first) HCUDA(cudaMemsetAsync(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long), st));
   else HCUDA(cudaMemsetAsync(w.d_ctl, 0, kListFile * sizeof(unsigned long long), st));
   ListPtrs L;

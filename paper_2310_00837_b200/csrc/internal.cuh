@@ -232,6 +232,7 @@ struct helios_cache {
   int64_t header = 0, stride = 0;
   int io_ctas = 32;
   bool io_sync = false;            // HELIOS_CACHE_IO_SYNC ablation
+  bool broken = false;             // a ring / staging watchdog fired: ring state is no longer consistent
   helios::IoRings io;
   bool has_file = false;
   // host staging (HELIOS_CACHE_HOST_STAGED)
