@@ -1,0 +1,47 @@
+"""CPU checks of bench.py: the --impl reference arm (the oracle on host cores) prints one JSON line
+with the driver contract's keys, and the capacity/tier helpers behave."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_json_contract():
+    out = subprocess.check_output([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config",
+                                   "C1", "--steps", "3", "--warmup", "1"], cwd=ROOT, text=True, timeout=300)
+    lines = [l for l in out.splitlines() if l.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["steps"] == 3 and d["warmup"] == 1 and d["value"] > 0
+    assert d["higher_is_better"] is True and d["scaling"] == "weak" and d["vs_baseline"] is None
+    assert d["config"]["workload"] == "C1"
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] == 1 and cb["value"] == d["value"] and cb["sample"]
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_capacity_and_tier_helpers():
+    sys.path.insert(0, ROOT)
+    import bench
+    import workloads
+    C = workloads.CONFIGS
+    assert not bench.has_file_tier(C["C2"]) and not bench.has_file_tier(C["C3"])
+    assert bench.has_file_tier(C["C1"]) and bench.has_file_tier(C["C4"])
+    assert bench.keeps_table(C["C1"]) and bench.keeps_table(C["C3"]) and not bench.keeps_table(C["C4"])
+    assert bench.pick_scale(C["C1"], 1) == 1.0
+    huge = workloads.Config("huge", 10**12, 10**13, 1024, 1024, [15], 0.1, 0.4)
+    s = bench.pick_scale(huge, 1)
+    assert 0.01 <= s < 1.0
+    sc = workloads.scaled(C["C4"], 0.1)
+    assert sc.V == C["C4"].V // 10 and sc.dim == 1024 and sc.fanouts == C["C4"].fanouts
+    H, S = workloads.tier_rows(C["C3"])
+    assert H == 11_100_000 and S == 99_900_000
+    H2, _ = workloads.tier_rows(C["C2"], world_size=3)
+    assert H2 * 3 >= C["C2"].V
