@@ -194,6 +194,22 @@ def file_peak(path: str, stride: int, header: int, threads: int, secs: float = 3
     return json.loads(out)
 
 
+def interval_union(iv) -> float:
+    """Total length of the union of [a, b) intervals (ms): the time during which at least one of
+    the overlapping launches was running."""
+    tot, cur_a, cur_b = 0.0, None, None
+    for a, b in sorted(iv):
+        if cur_b is None or a > cur_b:
+            if cur_b is not None:
+                tot += cur_b - cur_a
+            cur_a, cur_b = a, b
+        else:
+            cur_b = max(cur_b, b)
+    if cur_b is not None:
+        tot += cur_b - cur_a
+    return tot
+
+
 # ---------------------------------------------------------------------------------------------
 
 def run_oracle_baseline(inp, keys, budget_s: float, check=None, dir_=None) -> dict:
@@ -234,6 +250,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly instead of CUDA graphs")
     ap.add_argument("--serial-gather", type=int, default=0, help="1: gathers of successive batches run one at a time")
     ap.add_argument("--intra", action="store_true", help="intra-batch pipeline: per-hop gather passes (NEXT-1)")
+    ap.add_argument("--link-stream", action="store_true",
+                    help="ablation: host-tier rows of every batch on one high-priority link stream (HELIOS_PLAN_LINK_STREAM)")
     ap.add_argument("--host-alias", action="store_true", help="host tier = canonical table by id (no packed copy)")
     ap.add_argument("--io-rings", type=int, default=8, help="SQ/CQ ring pairs = host IO worker threads")
     ap.add_argument("--topo-host", action="store_true",
@@ -385,7 +403,7 @@ def main():
     stream = torch.cuda.current_stream()
     depth = args.depth
     pflags = ((H.PLAN_NO_GRAPH if args.no_graph else 0) | (H.PLAN_SERIAL_GATHER if args.serial_gather else 0)
-              | (H.PLAN_INTRA_BATCH if args.intra else 0))
+              | (H.PLAN_INTRA_BATCH if args.intra else 0) | (H.PLAN_LINK_STREAM if args.link_stream else 0))
     plan = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=depth, flags=pflags)
 
     for i in range(args.warmup):
@@ -402,9 +420,13 @@ def main():
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
         start.record(stream)
-        for i in range(args.steps):   # device timing events on every 4th batch (sampled stage times)
+        H.helios_plan_mark(plan, stream)
+        # device timing events on every batch of the last depth*1000 (all of them by default): the
+        # per-batch segments give the stage times and the union of the gather segments' intervals
+        timed_from = max(0, args.steps - depth * 1000)
+        for i in range(args.steps):
             b = seq[args.warmup + i]
-            H.helios_plan_submit(plan, i % depth, seed_of[b], keys[b], stream, timing=(i % 4 == 0))
+            H.helios_plan_submit(plan, i % depth, seed_of[b], keys[b], stream, timing=(i >= timed_from))
         for k in range(depth):
             H.helios_plan_wait(plan, k, stream)
         end.record(stream)
@@ -412,13 +434,18 @@ def main():
     torch.cuda.nvtx.range_pop()
     H.helios_sync(c)
     total_ms = start.elapsed_time(end)
-    sample_ms, gather_ms = [], []
+    sample_ms, gather_ms, link_ms, gather_iv, link_iv = [], [], [], [], []
     for k in range(depth):
-        n_k = sum(1 for i in range(k, args.steps, depth) if i % 4 == 0)
-        for back in range(min(n_k, 255)):
-            a, b_ = H.helios_plan_timing(plan, k, back)
-            sample_ms.append(a)
-            gather_ms.append(b_)
+        n_k = sum(1 for i in range(k, args.steps, depth) if i >= timed_from)
+        for back in range(n_k):
+            tb = H.helios_plan_timing(plan, k, back)
+            sample_ms.append(tb.sample_ms)
+            gather_ms.append(tb.gather_ms)
+            gather_iv.append((tb.t_gather, tb.t_end))
+            if tb.link_ms >= 0:
+                link_ms.append(tb.link_ms)
+    n_timed = len(gather_iv)
+    gather_busy_ms = interval_union(gather_iv)
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     allreduce(t, dist.ReduceOp.MAX)
     if world > 1:
@@ -524,13 +551,45 @@ def main():
              "storage": stor_bytes / bw_file}
     t_roof_ms = sum(terms.values()) / 1e6
     alg_bytes = hbm_bytes + pcie_bytes + nvl_bytes + stor_bytes
-    achieved = alg_bytes / (g_ms * 1e6)
-    peak_eff = alg_bytes / (t_roof_ms * 1e6)
     dominant = max(terms.items(), key=lambda x: x[1])[0]
+    if plan.link and link_ms and not file_cfg:
+        # dominant kernel = the host-row kernel on the link stream: its PCIe bytes per launch over
+        # its own launch time (events on the link stream, one batch at a time by construction)
+        l_ms = statistics.mean(link_ms)
+        achieved = R * n_host / (l_ms * 1e6)
+        roof = {"bound": "pcie", "kernel": "k_gather_lists<host part> (link stream)", "achieved": round(achieved, 2),
+                "peak": round(bw_pcie, 2), "unit": "GB/s", "frac": round(achieved / bw_pcie, 4),
+                "traffic": traffic_of(cfg.name + "/host"), "launch_ms": round(l_ms, 4),
+                "note": "achieved = R*host_rows per launch / mean launch time (CUDA events on the link stream over the "
+                        "timed region); peak = pinned H2D copy-engine bandwidth measured in this run; the platform's "
+                        "random 512 B zero-copy ceiling is lower (DESIGN.md §6); tier sum form: t_roof_ms, frac_throughput"}
+    else:
+        # gathers of the `depth` slots overlap, so one launch's duration is shared with the others:
+        # achieved = the timed launches' algorithmic bytes / the time at least one of them was running
+        achieved = alg_bytes * n_timed / (gather_busy_ms * 1e6)
+        peak = alg_bytes / (t_roof_ms * 1e6)
+        roof = {"bound": dominant, "kernel": "k_lookup + k_gather_lists (K3+K4)", "achieved": round(achieved, 2),
+                "peak": round(peak, 2), "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": traffic_of(cfg.name), "launch_ms": round(g_ms, 4),
+                "busy_ms": round(gather_busy_ms, 3), "launches_timed": n_timed,
+                "note": "achieved = algorithmic tier bytes (HBM tier read + output write + ids/dir, PCIe host rows, "
+                        "NVLink peer rows, storage) of the timed launches / union of their execution intervals "
+                        f"(CUDA events on the slot streams over the timed region; {depth} batches in flight, so "
+                        "launches overlap); peak = the same bytes / T_roof, the tier sum form "
+                        "sum(bytes_link / BW_link); frac_throughput = T_roof / ms_per_step"}
+    roof.update({
+        "peaks_used": {"hbm_gbs": bw_hbm, "hbm_src": "MEASURED_PEAKS.json" if pk else "fallback",
+                       "pcie_gbs": round(bw_pcie, 2), "pcie_src": "pinned H2D copy measured in this run",
+                       "nvlink_gbs": bw_nvl, "file_gbs": round(bw_file, 4) if fpk else None,
+                       "file_src": f"tools/filebench random {inp.stride} B O_DIRECT={fpk['direct']} x{args.io_rings} threads" if fpk else None},
+        "bytes_per_launch": {"hbm": round(hbm_bytes), "pcie": round(pcie_bytes), "nvlink": round(nvl_bytes),
+                             "storage": round(stor_bytes)},
+        "t_roof_ms": round(t_roof_ms, 4),
+        "frac_throughput": round(t_roof_ms / (max_ms / steps), 4)})
     value = world * steps / (max_ms / 1e3)
     e2e_val = world * steps / e2e_s
     launches_per_step = (3 * L + 2 + 2 + ((2 if args.io_sync else 3) if c.info().file_rows > 0 else 0)
-                         + (1 if args.host_staged > 0 else 0))
+                         + (1 if args.host_staged > 0 else 0) + (1 if plan.link else 0))
     out = {
         "metric": "sampled+gathered mini-batches/sec (feature GB/s and tier-roofline fraction alongside)",
         "value": round(value, 3), "unit": "batches/s", "n_gpus": 1 if one_gpu else world, "steps": steps, "warmup": args.warmup,
@@ -548,6 +607,7 @@ def main():
                    + (f"; {args.host_staged:.0%} of host rows staged by {args.stage_workers} host threads"
                       if args.host_staged > 0 else "; GPU zero-copy reads"),
                    "batches_in_flight": depth, "cuda_graphs": not args.no_graph, "serial_gather": bool(args.serial_gather),
+                   "link_stream": bool(plan.link),
                    "intra_batch_pipeline": bool(args.intra),
                    "topology": "pinned host, zero-copy (UVA)" if args.topo_host else "HBM",
                    "tiers": {"hbm_frac": cfg.hbm_frac, "host_frac": cfg.host_frac},
@@ -555,22 +615,11 @@ def main():
                        (inp.graph.E * 4 + cfg.V * 8) / 1e9, cfg.V * R / 1e9)},
         "feature_gbs": round(world * n_rows / steps * R * steps / (max_ms / 1e3) / 1e9, 2),
         "stage_ms": {"sample": round(statistics.mean(sample_ms), 4), "gather": round(g_ms, 4),
-                     "note": f"per batch, device events around the two graph segments on every 4th batch, {depth} batches in flight"},
+                     "link_host_kernel": round(statistics.mean(link_ms), 4) if link_ms else None,
+                     "note": f"mean per batch, device events around the two graph segments of every timed batch ({n_timed}), {depth} batches in flight"},
         "rows_per_batch": {"n_L": round(nL, 1), "hbm_local": round(n_local, 1), "hbm_peer": round(n_peer, 1),
                            "host": round(n_host, 1), "file": round(n_file, 1)},
-        "roofline": {"bound": dominant, "kernel": "k_lookup + k_gather_lists (K3+K4)", "achieved": round(achieved, 2),
-                     "peak": round(peak_eff, 2), "unit": "GB/s", "frac": round(t_roof_ms / g_ms, 4),
-                     "traffic": traffic_of(cfg.name),
-                     "peaks_used": {"hbm_gbs": bw_hbm, "hbm_src": "MEASURED_PEAKS.json" if pk else "fallback",
-                                    "pcie_gbs": round(bw_pcie, 2), "pcie_src": "pinned H2D copy measured in this run",
-                                    "nvlink_gbs": bw_nvl, "file_gbs": round(bw_file, 4) if fpk else None,
-                                    "file_src": f"tools/filebench random {inp.stride} B O_DIRECT={fpk['direct']} x{args.io_rings} threads" if fpk else None},
-                     "bytes_per_launch": {"hbm": round(hbm_bytes), "pcie": round(pcie_bytes), "nvlink": round(nvl_bytes),
-                                          "storage": round(stor_bytes)},
-                     "t_roof_ms": round(t_roof_ms, 4),
-                     "frac_throughput": round(t_roof_ms / (max_ms / steps), 4),
-                     "note": "frac = T_roof / mean per-launch gather time (CUDA events, batches overlapping); "
-                             "frac_throughput = T_roof / ms_per_step (whole-path throughput vs the tier roofline)"},
+        "roofline": roof,
         "e2e": {"value": round(e2e_val, 3), "unit": "batches/s", "h2d_bytes_per_step": cfg.B * 8,
                 "d2h_bytes_per_step": (L + 1 + 4) * 8},
         "gpu_launches": launches_per_step * steps,

@@ -236,8 +236,14 @@ helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64
  *   desc.depth       number of slots, 1..8.
  *   desc.flags       HELIOS_PLAN_NO_GRAPH: launch the kernels directly on every submit;
  *                    HELIOS_PLAN_SERIAL_GATHER: chain the gathers of successive submits;
- *                    HELIOS_PLAN_INTRA_BATCH: per-hop gather passes overlapping the sampling.
+ *                    HELIOS_PLAN_INTRA_BATCH: per-hop gather passes overlapping the sampling;
+ *                    HELIOS_PLAN_LINK_STREAM: host rows on a shared link stream (see below).
  *   c                cache, or NULL for a sampling-only plan (no features / stats).
+ * Link stream (HELIOS_PLAN_LINK_STREAM, when c has a host tier, without SERIAL_GATHER / INTRA_BATCH):
+ * the host-tier rows of every batch are copied by one kernel on a high-priority stream shared by all
+ * slots, in submission order, so the PCIe link serves one batch at a time with all of that batch's
+ * reads in flight (PCIe is the host tier's bottleneck); the lookup and HBM rows stay
+ * on the slot's stream.  An ablation: measured slower than the default.
  * Blocking create/free. */
 #define HELIOS_PLAN_NO_GRAPH 0x1u
 #define HELIOS_PLAN_SERIAL_GATHER 0x2u  /* gathers of successive batches run one at a time (sampling
@@ -246,6 +252,7 @@ helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64
                                            per new node range (N_0, then N_{h+1} \ N_h) forks onto a
                                            side stream while the next hop samples; timed submits then
                                            report the whole batch as the sampling phase */
+#define HELIOS_PLAN_LINK_STREAM 0x8u    /* ablation: host-tier rows of every batch on a shared link stream */
 #define HELIOS_SUBMIT_SEEDS_HOST 0x1u  /* seeds pointer is host memory (copied with the parameters, H2D) */
 #define HELIOS_SUBMIT_TIMING 0x2u      /* record device timing events around the sample / gather phases */
 typedef struct helios_plan helios_plan;
@@ -272,11 +279,24 @@ helios_status helios_plan_submit(helios_plan* p, int32_t slot, const int64_t* se
                                  uint32_t flags, void* stream);
 /* Makes `stream` wait for the last batch submitted to `slot`. */
 helios_status helios_plan_wait(helios_plan* p, int32_t slot, void* stream);
-/* Device time (ms) of the sampling and gather phases of a batch submitted to `slot` with
- * HELIOS_SUBMIT_TIMING: back = 0 is the slot's last timed batch, back = k the k-th before it
- * (k < 256; CUDA events recorded around the two graph segments, which are then launched as two
- * graphs instead of one).  Blocks until that batch is done; E_RANGE if it is not recorded. */
-helios_status helios_plan_timing(helios_plan* p, int32_t slot, int32_t back, float* sample_ms, float* gather_ms);
+/* Device timing of a batch submitted to `slot` with HELIOS_SUBMIT_TIMING: back = 0 is the slot's
+ * last timed batch, back = k the k-th before it (k < 1024; CUDA events recorded around the two graph
+ * segments, which are then launched as two graphs instead of one).  All values in ms:
+ *   sample_ms   start of sampling -> end of sampling (slot stream);
+ *   gather_ms   end of sampling -> end of the batch (lookup + gather + IO; in link mode including
+ *               the wait for the link stream);
+ *   link_ms     the batch's host-row kernel on the link stream, -1 without a link stream;
+ *   t_start, t_gather, t_end   the batch's start / end of sampling / end, relative to the last
+ *               helios_plan_mark (-1 if the plan was never marked), so a caller can form the union
+ *               of busy intervals of overlapping batches.
+ * Blocks until that batch is done; E_RANGE if it is not recorded. */
+typedef struct {
+  float sample_ms, gather_ms, link_ms;
+  float t_start, t_gather, t_end;
+} helios_batch_timing;
+helios_status helios_plan_timing(helios_plan* p, int32_t slot, int32_t back, helios_batch_timing* out);
+/* Records the plan's reference event on `stream` (the origin of helios_batch_timing's t_* values). */
+helios_status helios_plan_mark(helios_plan* p, void* stream);
 
 /* Waits for `stream` and the cache's IO streams; returns and clears latched errors of the cache
  * and its graph (E_IO, E_TIMEOUT, E_INVALID, E_RANGE).  After E_TIMEOUT the cache's ring state is

@@ -29,7 +29,8 @@ helios_status plan_create_impl(helios_plan* p);
 helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seeds, int64_t n, uint64_t key, uint32_t flags,
                                cudaStream_t caller);
 helios_status plan_wait_impl(helios_plan* p, int32_t slot, cudaStream_t st);
-helios_status plan_timing_impl(helios_plan* p, int32_t slot, int32_t back, float* sample_ms, float* gather_ms);
+helios_status plan_timing_impl(helios_plan* p, int32_t slot, int32_t back, helios_batch_timing* out);
+helios_status plan_mark_impl(helios_plan* p, cudaStream_t st);
 helios_status plan_outputs_impl(helios_plan* p, int32_t slot, helios_blocks* blocks, void** features,
                                 helios_gather_stats** stats);
 
@@ -404,6 +405,7 @@ helios_status helios_plan_create(helios_graph* g, helios_cache* c, const helios_
   p->graphs = !(d->flags & HELIOS_PLAN_NO_GRAPH);
   p->serial_gather = (d->flags & HELIOS_PLAN_SERIAL_GATHER) != 0;
   p->intra = (d->flags & HELIOS_PLAN_INTRA_BATCH) != 0;
+  p->link = c && c->S > 0 && !p->intra && !p->serial_gather && (d->flags & HELIOS_PLAN_LINK_STREAM);
   HCHECK(!p->intra || p->graphs, HELIOS_E_INVALID, "HELIOS_PLAN_INTRA_BATCH needs CUDA graphs");
   helios_status st = plan_create_impl(p);
   if (st != HELIOS_OK) {
@@ -450,11 +452,19 @@ helios_status helios_plan_wait(helios_plan* p, int32_t slot, void* stream) {
   GUARD_END
 }
 
-helios_status helios_plan_timing(helios_plan* p, int32_t slot, int32_t back, float* sample_ms, float* gather_ms) {
+helios_status helios_plan_timing(helios_plan* p, int32_t slot, int32_t back, helios_batch_timing* out) {
   GUARD_BEGIN
   HCHECK(p, HELIOS_E_INVALID, "null plan");
   DeviceGuard dg(p->g->device);
-  return plan_timing_impl(p, slot, back, sample_ms, gather_ms);
+  return plan_timing_impl(p, slot, back, out);
+  GUARD_END
+}
+
+helios_status helios_plan_mark(helios_plan* p, void* stream) {
+  GUARD_BEGIN
+  HCHECK(p, HELIOS_E_INVALID, "null plan");
+  DeviceGuard dg(p->g->device);
+  return plan_mark_impl(p, (cudaStream_t)stream);
   GUARD_END
 }
 

@@ -98,7 +98,8 @@ struct GatherArgs {
   char* out;
   int32_t R;
   ListPtrs L;
-  const unsigned long long* ctl;
+  unsigned long long* ctl;  // list counts, staging split, host / stage row tickets
+  int part;                 // kPartAll / kPartHbm / kPartHost
   bool staged;
   bool accumulate;          // intra-batch passes: add this pass's row counts to stats
   const char* stage;        // device alias of the pinned staging rows
@@ -149,9 +150,16 @@ __device__ __forceinline__ void copy_rows(const GatherArgs& a, int q, int64_t j0
   }
 }
 
-// K4: warp-specialised gather.  When the host list is non-empty, one warp in 8 serves host rows
-// (zero-copy over PCIe, UH rows in flight per warp, so every host read is outstanding at once
-// and the link streams) while the others copy peer (NVLink) then local HBM rows.
+// K4: warp-specialised gather.
+//   kPartAll (one kernel, every tier): when the host list is non-empty one warp in 8 serves host
+//     rows (zero-copy over PCIe; in staged mode a second warp in 8 consumes staged chunks) while the
+//     others copy peer (NVLink) then local HBM rows.
+//   kPartHbm: every warp copies peer then local rows (link mode, slot stream).
+//   kPartHost: every warp serves host rows (link mode: the plan's link stream; staged mode: odd
+//     warps consume staged chunks).
+// Host rows and staged chunks are taken by ticket (UH rows per grab), not by a static split: CTAs
+// that become resident late (SMs busy with other batches' sampling) then take less work instead of
+// stretching the tail of the link transfer.
 __device__ __forceinline__ uint32_t ld_acquire_sys_u32_(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -167,6 +175,54 @@ __device__ __forceinline__ int4 ld_volatile_v4_(const int4* p) {
 }
 constexpr uint64_t kStageWatchdogNs = 30ull * 1000000000ull;
 
+__device__ __forceinline__ int64_t warp_ticket(unsigned long long* ctr, int n, int lane) {
+  unsigned long long t = 0;
+  if (lane == 0) t = atomicAdd(ctr, (unsigned long long)n);
+  return (int64_t)__shfl_sync(0xFFFFFFFFu, t, 0);
+}
+
+// Zero-copy host rows [0, n_gpu), UH rows per ticket.
+template <int VPL, int UH>
+__device__ __forceinline__ void host_rows(const GatherArgs& a, int64_t n_gpu, int lane, int nvec) {
+  for (;;) {
+    const int64_t j0 = warp_ticket(&a.ctl[kCtlHostTicket], UH, lane);
+    if (j0 >= n_gpu) break;
+    copy_rows<VPL, UH>(a, kListHost, j0, n_gpu, lane, nvec);
+  }
+}
+
+// Staged host rows [n_gpu, n_host): one chunk per ticket, polled until its host stager published it.
+__device__ __forceinline__ bool staged_rows(const GatherArgs& a, int64_t n_gpu, int64_t n_stage, int lane, int nvec) {
+  const uint32_t seq = (uint32_t)a.ctl[kCtlStageSeq];
+  const int64_t n_chunks = (n_stage + kStageChunk - 1) / kStageChunk;
+  const uint64_t t0 = globaltimer();
+  for (;;) {
+    const int64_t ch = warp_ticket(&a.ctl[kCtlStageTicket], 1, lane);
+    if (ch >= n_chunks) break;
+    bool ok = true;
+    unsigned backoff = 128;  // each poll is a PCIe read that competes with the row reads: back off
+    while (ld_acquire_sys_u32_(&a.done[ch]) != seq) {  // every lane polls (one request)
+      if (globaltimer() - t0 > kStageWatchdogNs) {
+        ok = false;
+        break;
+      }
+      __nanosleep(backoff);
+      backoff = min(backoff * 2u, 2048u);
+    }
+    if (!__all_sync(0xFFFFFFFFu, ok)) {
+      if (lane == 0) latch(a.err, HELIOS_E_TIMEOUT);
+      return false;
+    }
+    const int64_t j1 = min(n_stage, (ch + 1) * kStageChunk);
+    for (int64_t j = ch * kStageChunk; j < j1; j++) {
+      const int4* src = (const int4*)(a.stage + j * a.R);
+      int4* dst = (int4*)(a.out + a.L.i[kListHost][n_gpu + j] * (int64_t)a.R);
+      for (int k = lane; k < nvec; k += 32) dst[k] = ld_volatile_v4_(src + k);
+    }
+  }
+  return true;
+}
+
 template <int VPL, int U, int UH>
 __global__ void __launch_bounds__(256, 4) k_gather_lists(GatherArgs a) {
   pdl_wait();
@@ -179,6 +235,11 @@ __global__ void __launch_bounds__(256, 4) k_gather_lists(GatherArgs a) {
                 n_host = (int64_t)a.ctl[kListHost];
   const int64_t n_gpu = a.staged ? (int64_t)a.ctl[kCtlStageGpu] : n_host;
   const int64_t n_stage = n_host - n_gpu;
+  if (a.part == kPartHost) {
+    if (a.staged && (gw & 1)) staged_rows(a, n_gpu, n_stage, lane, nvec);
+    else host_rows<VPL, UH>(a, n_gpu, lane, nvec);
+    return;
+  }
   if (a.stats && gw == 0 && lane == 0) {
     if (a.accumulate) {
       a.stats->rows_hbm_local += n_local;
@@ -191,39 +252,13 @@ __global__ void __launch_bounds__(256, 4) k_gather_lists(GatherArgs a) {
     }
     a.stats->rows_file = (int64_t)a.ctl[kListFile];  // the file list accumulates over passes
   }
-  // warp roles: r = gw % 8.  r == 0: zero-copy host rows [0, n_gpu); r == 1 (staged mode): stage
-  // consumers for rows [n_gpu, n_host); other warps: peer then local HBM rows.
-  const int nspecial = (n_host > 0) ? (a.staged ? 2 : 1) : 0;
+  // kPartAll warp roles: r = gw % 8.  r == 0: zero-copy host rows; r == 1 (staged mode): stage
+  // consumers; other warps: peer then local HBM rows.
+  const int nspecial = (a.part == kPartAll && n_host > 0) ? (a.staged ? 2 : 1) : 0;
   const int r = (int)(gw & 7);
   if (r < nspecial) {
-    const int64_t sw = gw >> 3, n_sw = nw >> 3;
-    if (r == 0) {
-      for (int64_t j0 = sw * UH; j0 < n_gpu; j0 += n_sw * UH) copy_rows<VPL, UH>(a, kListHost, j0, n_gpu, lane, nvec);
-    } else {
-      const uint32_t seq = (uint32_t)a.ctl[kCtlStageSeq];
-      const int64_t n_chunks = (n_stage + kStageChunk - 1) / kStageChunk;
-      const uint64_t t0 = globaltimer();
-      for (int64_t ch = sw; ch < n_chunks; ch += n_sw) {
-        bool ok = true;
-        while (ld_acquire_sys_u32_(&a.done[ch]) != seq) {  // every lane polls (one request)
-          if (globaltimer() - t0 > kStageWatchdogNs) {
-            ok = false;
-            break;
-          }
-          __nanosleep(200);
-        }
-        if (!__all_sync(0xFFFFFFFFu, ok)) {
-          if (lane == 0) latch(a.err, HELIOS_E_TIMEOUT);
-          return;
-        }
-        const int64_t j1 = min(n_stage, (ch + 1) * kStageChunk);
-        for (int64_t j = ch * kStageChunk; j < j1; j++) {
-          const int4* src = (const int4*)(a.stage + j * a.R);
-          int4* dst = (int4*)(a.out + a.L.i[kListHost][n_gpu + j] * (int64_t)a.R);
-          for (int k = lane; k < nvec; k += 32) dst[k] = ld_volatile_v4_(src + k);
-        }
-      }
-    }
+    if (r == 0) host_rows<VPL, UH>(a, n_gpu, lane, nvec);
+    else staged_rows(a, n_gpu, n_stage, lane, nvec);
     return;
   }
   const int64_t dw = (gw >> 3) * (8 - nspecial) + (r - nspecial);  // index among data warps
@@ -462,7 +497,9 @@ helios_status io_preload_kernels() {
   return HELIOS_OK;
 }
 
-// Persistent grid: exactly the resident CTAs, so every host-row warp is live from the start.
+// Persistent grid: exactly the resident CTAs, so every host-row warp is live from the start.  The
+// host-only part (link stream) uses one CTA per SM: 1184 warps keep the link saturated
+// (tools/hostorder.cu) and leave the rest of the SMs to the sampling of other batches.
 template <int VPL, int U, int UH>
 static void launch_gather(const GatherArgs& a, int sms, cudaStream_t st) {
   static int per_sm = 0;
@@ -470,7 +507,16 @@ static void launch_gather(const GatherArgs& a, int sms, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_lists<VPL, U, UH>, 256, 0);
     per_sm = std::max(per_sm, 1);
   }
-  launch_pdl(k_gather_lists<VPL, U, UH>, dim3(sms * per_sm), dim3(256), st, a);
+  const int grid = a.part == kPartHost ? sms : sms * per_sm;
+  launch_pdl(k_gather_lists<VPL, U, UH>, dim3(grid), dim3(256), st, a);
+}
+
+static void launch_gather_any(const GatherArgs& a, int sms, cudaStream_t st) {
+  const int nvec = a.R / 16;
+  if (nvec <= 32) launch_gather<1, 4, 8>(a, sms, st);
+  else if (nvec <= 64) launch_gather<2, 2, 4>(a, sms, st);
+  else if (nvec <= 128) launch_gather<4, 1, 2>(a, sms, st);
+  else launch_gather<8, 1, 1>(a, sms, st);
 }
 
 void gws_free(GatherWS& w) {
@@ -520,33 +566,22 @@ helios_status gws_ensure(helios_cache* c, GatherWS& w, int64_t max_nodes) {
   return HELIOS_OK;
 }
 
-// One lookup + gather pass over rows [*lo, *n_nodes) (lo = NULL: all).  first: reset every count;
-// otherwise (later intra-batch passes) only the per-pass tier counts are reset, so the file list and
-// the stats accumulate over the passes of a batch.
-static helios_status gather_pass(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* lo,
-                                 const int64_t* n_nodes, int64_t max_rows, void* out, helios_gather_stats* stats,
-                                 bool first, bool accumulate, cudaStream_t st) {
-  HCHECK(!c->broken, HELIOS_E_STATE, "cache unusable after an IO / staging watchdog timeout");
-  if (first) HCUDA(cudaMemsetAsync(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long), st));
-  else HCUDA(cudaMemsetAsync(w.d_ctl, 0, kListFile * sizeof(unsigned long long), st));
-  ListPtrs L;
+static GatherArgs make_args(helios_cache* c, GatherWS& w, void* out, helios_gather_stats* stats, bool accumulate,
+                            int part) {
+  GatherArgs a;
   for (int q = 0; q < kLists; q++) {
-    L.i[q] = w.d_list_i + q * w.cap;
-    L.w[q] = w.d_list_w + q * w.cap;
+    a.L.i[q] = w.d_list_i + q * w.cap;
+    a.L.w[q] = w.d_list_w + q * w.cap;
   }
   const bool staged = c->staged && w.d_host_i;
   if (staged) {
-    L.i[kListHost] = w.d_host_i;
-    L.w[kListHost] = w.d_host_w;
+    a.L.i[kListHost] = w.d_host_i;
+    a.L.w[kListHost] = w.d_host_w;
   }
-  const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_rows + 255) / 256), (int64_t)c->sms * 2);
-  k_lookup<<<lg, 256, 0, st>>>(nodes, lo, n_nodes, c->dir, c->rank, L, w.d_ctl);
-  if (staged) launch_pdl(k_stage_publish, dim3(1), dim3(1), st, w.d_ctl, w.d_seq, w.d_mail, c->stage_frac, kStageCapRows);
-  GatherArgs a;
   a.out = (char*)out;
   a.R = c->R;
-  a.L = L;
   a.ctl = w.d_ctl;
+  a.part = part;
   a.staged = staged;
   a.accumulate = accumulate;
   a.stage = w.d_stage;
@@ -556,11 +591,27 @@ static helios_status gather_pass(helios_cache* c, GatherWS& w, const int64_t* no
   a.peers = c->d_peers;
   a.host_dev = c->d_host_tier;
   a.stats = stats;
-  const int nvec = c->R / 16;
-  if (nvec <= 32) launch_gather<1, 4, 8>(a, c->sms, st);
-  else if (nvec <= 64) launch_gather<2, 2, 4>(a, c->sms, st);
-  else if (nvec <= 128) launch_gather<4, 1, 2>(a, c->sms, st);
-  else launch_gather<8, 1, 1>(a, c->sms, st);
+  return a;
+}
+
+// One lookup + gather pass over rows [*lo, *n_nodes) (lo = NULL: all).  first: reset every count;
+// otherwise (later intra-batch passes) only the per-pass tier counts and row tickets are reset, so
+// the file list and the stats accumulate over the passes of a batch.
+static helios_status gather_pass(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* lo,
+                                 const int64_t* n_nodes, int64_t max_rows, void* out, helios_gather_stats* stats,
+                                 bool first, bool accumulate, int part, cudaStream_t st) {
+  HCHECK(!c->broken, HELIOS_E_STATE, "cache unusable after an IO / staging watchdog timeout");
+  if (first) {
+    HCUDA(cudaMemsetAsync(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long), st));
+  } else {
+    HCUDA(cudaMemsetAsync(w.d_ctl, 0, kListFile * sizeof(unsigned long long), st));
+    HCUDA(cudaMemsetAsync(w.d_ctl + kCtlHostTicket, 0, 2 * sizeof(unsigned long long), st));
+  }
+  GatherArgs a = make_args(c, w, out, stats, accumulate, part);
+  const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_rows + 255) / 256), (int64_t)c->sms * 2);
+  k_lookup<<<lg, 256, 0, st>>>(nodes, lo, n_nodes, c->dir, c->rank, a.L, w.d_ctl);
+  if (a.staged) launch_pdl(k_stage_publish, dim3(1), dim3(1), st, w.d_ctl, w.d_seq, w.d_mail, c->stage_frac, kStageCapRows);
+  launch_gather_any(a, c->sms, st);
   HCUDA(cudaGetLastError());
   return HELIOS_OK;
 }
@@ -571,14 +622,31 @@ helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, 
   HCHECK(c->G == 1 || c->peers_attached, HELIOS_E_STATE, "world_size %d but peers not attached", c->G);
   HCHECK(w.d_ctl && max_nodes <= w.cap, HELIOS_E_CAPACITY, "max_nodes %lld > gather list cap %lld",
          (long long)max_nodes, (long long)w.cap);
-  return gather_pass(c, w, nodes, nullptr, n_nodes, max_nodes, out, stats, true, false, st);
+  return gather_pass(c, w, nodes, nullptr, n_nodes, max_nodes, out, stats, true, false, kPartAll, st);
+}
+
+helios_status gather_hbm_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* n_nodes,
+                                int64_t max_nodes, void* out, helios_gather_stats* stats, cudaStream_t st) {
+  HCHECK(nodes && n_nodes && (out || max_nodes == 0), HELIOS_E_INVALID, "null gather argument");
+  HCHECK(c->G == 1 || c->peers_attached, HELIOS_E_STATE, "world_size %d but peers not attached", c->G);
+  HCHECK(w.d_ctl && max_nodes <= w.cap, HELIOS_E_CAPACITY, "max_nodes %lld > gather list cap %lld",
+         (long long)max_nodes, (long long)w.cap);
+  return gather_pass(c, w, nodes, nullptr, n_nodes, max_nodes, out, stats, true, false, kPartHbm, st);
+}
+
+helios_status gather_host_launch(helios_cache* c, GatherWS& w, void* out, cudaStream_t st) {
+  HCHECK(!c->broken, HELIOS_E_STATE, "cache unusable after an IO / staging watchdog timeout");
+  const GatherArgs a = make_args(c, w, out, nullptr, false, kPartHost);
+  launch_gather_any(a, c->sms, st);
+  HCUDA(cudaGetLastError());
+  return HELIOS_OK;
 }
 
 helios_status gather_range_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* lo,
                                   const int64_t* hi, int64_t max_rows, void* out, helios_gather_stats* stats, bool first,
                                   cudaStream_t st) {
   HCHECK(c->G == 1 || c->peers_attached, HELIOS_E_STATE, "world_size %d but peers not attached", c->G);
-  return gather_pass(c, w, nodes, lo, hi, max_rows, out, stats, first, true, st);
+  return gather_pass(c, w, nodes, lo, hi, max_rows, out, stats, first, true, kPartAll, st);
 }
 
 // K5 / K6 on the cache's IO streams for the misses recorded in w by the preceding gather_launch on

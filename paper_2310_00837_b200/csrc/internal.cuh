@@ -118,7 +118,11 @@ struct SampleWS {
 // Per-gather bookkeeping (one per gather context): per-tier work lists written by the lookup
 // kernel, and the ticket / count words shared with the gather and IO kernels.
 enum : int { kListLocal = 0, kListPeer = 1, kListHost = 2, kListFile = 3, kLists = 4 };
-enum : int { kCtlSubmit = 4, kCtlComplete = 5, kCtlStageGpu = 6, kCtlStageSeq = 7, kCtlWords = 8 };
+enum : int { kCtlSubmit = 4, kCtlComplete = 5, kCtlStageGpu = 6, kCtlStageSeq = 7, kCtlHostTicket = 8,
+             kCtlStageTicket = 9, kCtlWords = 10 };
+// Which rows a k_gather_lists launch copies: every tier (one kernel), only the HBM tiers (local +
+// peer), or only the host tier (zero-copy + staged rows; the plan's link stream).
+enum : int { kPartAll = 0, kPartHbm = 1, kPartHost = 2 };
 constexpr int kStageChunk = 64;              // rows per staging chunk (one completion flag each)
 constexpr int64_t kStageCapRows = 1 << 16;   // staged rows per batch at most (the rest: zero-copy)
 struct StageCtx;
@@ -262,8 +266,11 @@ struct PlanSlot {
   cudaStream_t s_side = nullptr;                        // intra-batch gather passes
   cudaEvent_t ev_fork[HELIOS_MAX_HOPS + 1] = {};
   cudaEvent_t ev_join = nullptr;
-  static constexpr int kRing = 256;
-  std::vector<cudaEvent_t> ring;  // kRing x {start, mid, end} timing events (timed submits only)
+  cudaEvent_t ev_lk = nullptr, ev_host = nullptr;  // link mode: lookup done (slot) / host rows done (link)
+  static constexpr int kRing = 1024;
+  static constexpr int kEv = 5;   // per timed batch: {start, sampled, end} on the slot stream,
+                                  // {host start, host end} on the link stream
+  std::vector<cudaEvent_t> ring;  // kRing x kEv timing events (timed submits only)
   int64_t count = 0;              // batches submitted to this slot
   int64_t tcount = 0;             // timed batches submitted to this slot
   bool submitted = false;
@@ -279,7 +286,18 @@ struct helios_plan {
   bool graphs = true;
   bool serial_gather = false;
   bool intra = false;  // HELIOS_PLAN_INTRA_BATCH
+  // Link mode (HELIOS_PLAN_LINK_STREAM, opt-in ablation): the host-tier rows of every batch are
+  // copied by one k_gather_lists<kPartHost> launch on a high-priority stream shared by all slots, so
+  // the PCIe link serves one batch at a time; HBM rows stay on the slot stream.  Measured slower
+  // than letting each slot's gather kernel read its own host rows.
+  bool link = false;
+  static constexpr int kMaxLinks = 4;
+  int n_links = 1;                    // link streams used round-robin (HELIOS_PLAN_LINKS, 1..4)
+  int64_t link_count = 0;             // batches submitted to the link streams
+  cudaStream_t s_link[kMaxLinks] = {};
   cudaEvent_t ev_gather_chain = nullptr;  // last gather submitted (HELIOS_PLAN_SERIAL_GATHER)
+  cudaEvent_t ev_ref = nullptr;           // helios_plan_mark: origin of the t_* timings
+  bool marked = false;
   bool gather_chained = false;
   std::vector<helios::PlanSlot> slots;
 };
@@ -311,6 +329,11 @@ void gws_free(GatherWS& w);
 // file list for io_launch.
 helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes,
                             void* out, helios_gather_stats* stats, cudaStream_t st);
+// Link mode, first half (slot stream): K3 lookup + K4 over the HBM tiers only (stats written).
+helios_status gather_hbm_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* n_nodes,
+                                int64_t max_nodes, void* out, helios_gather_stats* stats, cudaStream_t st);
+// Link mode, second half (link stream, after the first half): K4 over the host tier only.
+helios_status gather_host_launch(helios_cache* c, GatherWS& w, void* out, cudaStream_t st);
 // Intra-batch pipeline pass: lookup + gather of rows [*lo, *hi) (lo = NULL: from 0); stats
 // accumulate, the file list accumulates (first = true resets everything).
 helios_status gather_range_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* lo,

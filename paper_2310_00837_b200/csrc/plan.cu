@@ -8,6 +8,7 @@
 // sampling of batch i+1 overlaps the gather of batch i (the inter-mini-batch pipeline).  File-tier
 // IO operators (K5/K6) are launched per batch behind the graphs (they wait on cross-stream events).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -32,10 +33,18 @@ void plan_free_impl(helios_plan* p) {
     for (cudaEvent_t e : s.ev_fork)
       if (e) cudaEventDestroy(e);
     if (s.ev_join) cudaEventDestroy(s.ev_join);
+    if (s.ev_lk) cudaEventDestroy(s.ev_lk);
+    if (s.ev_host) cudaEventDestroy(s.ev_host);
     if (s.s_side) cudaStreamDestroy(s.s_side);
     if (s.stream) cudaStreamDestroy(s.stream);
   }
   p->slots.clear();
+  for (auto& l : p->s_link) {
+    if (l) cudaStreamDestroy(l);
+    l = nullptr;
+  }
+  if (p->ev_ref) cudaEventDestroy(p->ev_ref);
+  p->ev_ref = nullptr;
   if (p->ev_gather_chain) cudaEventDestroy(p->ev_gather_chain);
   p->ev_gather_chain = nullptr;
 }
@@ -65,6 +74,13 @@ helios_status plan_create_impl(helios_plan* p) {
   if (s != HELIOS_OK) return s;
   p->slots.resize(d.depth);
   HCUDA(cudaEventCreateWithFlags(&p->ev_gather_chain, cudaEventDisableTiming));
+  HCUDA(cudaEventCreate(&p->ev_ref));
+  if (p->link) {
+    int least = 0, greatest = 0;
+    HCUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    if (const char* e = getenv("HELIOS_PLAN_LINKS")) p->n_links = std::max(1, std::min(atoi(e), helios_plan::kMaxLinks));
+    for (int i = 0; i < p->n_links; i++) HCUDA(cudaStreamCreateWithPriority(&p->s_link[i], cudaStreamNonBlocking, greatest));
+  }
   for (int k = 0; k < d.depth; k++) {
     PlanSlot& sl = p->slots[k];
     // output blocks: one allocation
@@ -100,13 +116,17 @@ helios_status plan_create_impl(helios_plan* p) {
     HCUDA(cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking));
     HCUDA(cudaEventCreateWithFlags(&sl.ev_caller, cudaEventDisableTiming));
     HCUDA(cudaEventCreateWithFlags(&sl.ev_end, cudaEventDisableTiming));
-    sl.ring.assign(3 * PlanSlot::kRing, nullptr);
+    sl.ring.assign(PlanSlot::kEv * PlanSlot::kRing, nullptr);
     for (auto& e : sl.ring) HCUDA(cudaEventCreate(&e));
+    if (p->link) {
+      HCUDA(cudaEventCreateWithFlags(&sl.ev_lk, cudaEventDisableTiming));
+      HCUDA(cudaEventCreateWithFlags(&sl.ev_host, cudaEventDisableTiming));
+    }
     if (p->graphs) {
       auto sample_ops = [&]() { return sample_launch(g, sl.ws, d.max_seeds, d.fanouts, d.L, &sl.blocks, sl.stream); };
-      auto gather_ops = [&]() {
-        return gather_launch(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + d.L, sl.blocks.nodes_cap,
-                             sl.feats, sl.stats, sl.stream);
+      auto gather_ops = [&]() {  // link mode: lookup + HBM rows only (host rows: link stream)
+        return (p->link ? gather_hbm_launch : gather_launch)(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + d.L,
+                                                             sl.blocks.nodes_cap, sl.feats, sl.stats, sl.stream);
       };
       s = capture(sl.stream, &sl.g_sample, sample_ops);
       if (s != HELIOS_OK) return s;
@@ -159,7 +179,7 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
   helios_status s = ws_upload_params(sl.ws, key, n, seeds, (flags & HELIOS_SUBMIT_SEEDS_HOST) != 0, sl.stream);
   if (s != HELIOS_OK) return s;
   const bool timed = (flags & HELIOS_SUBMIT_TIMING) != 0;
-  cudaEvent_t* ev = &sl.ring[3 * (sl.tcount % PlanSlot::kRing)];
+  cudaEvent_t* ev = &sl.ring[PlanSlot::kEv * (sl.tcount % PlanSlot::kRing)];
   if (timed) HCUDA(cudaEventRecord(ev[0], sl.stream));
   const bool chain = p->serial_gather && p->c && !p->intra;
   if (p->graphs && p->intra && p->c) {  // one graph; timed submits time the whole overlapped batch
@@ -180,11 +200,22 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
       if (p->graphs) {
         HCUDA(cudaGraphLaunch(sl.g_gather, sl.stream));
       } else {
-        s = gather_launch(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + p->d.L, sl.blocks.nodes_cap,
-                          sl.feats, sl.stats, sl.stream);
+        s = (p->link ? gather_hbm_launch : gather_launch)(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + p->d.L,
+                                                          sl.blocks.nodes_cap, sl.feats, sl.stats, sl.stream);
         if (s != HELIOS_OK) return s;
       }
     }
+  }
+  if (p->link) {  // host rows on the link stream, one batch at a time, in submission order
+    HCUDA(cudaEventRecord(sl.ev_lk, sl.stream));
+    cudaStream_t ls = p->s_link[p->link_count++ % p->n_links];
+    HCUDA(cudaStreamWaitEvent(ls, sl.ev_lk, 0));
+    if (timed) HCUDA(cudaEventRecord(ev[3], ls));
+    s = gather_host_launch(p->c, sl.gws, sl.feats, ls);
+    if (s != HELIOS_OK) return s;
+    if (timed) HCUDA(cudaEventRecord(ev[4], ls));
+    HCUDA(cudaEventRecord(sl.ev_host, ls));
+    HCUDA(cudaStreamWaitEvent(sl.stream, sl.ev_host, 0));
   }
   if (p->c) {
     s = io_launch(p->c, sl.gws, sl.feats, sl.stream);
@@ -212,18 +243,30 @@ helios_status plan_wait_impl(helios_plan* p, int32_t slot, cudaStream_t st) {
   return HELIOS_OK;
 }
 
-helios_status plan_timing_impl(helios_plan* p, int32_t slot, int32_t back, float* sample_ms, float* gather_ms) {
+helios_status plan_timing_impl(helios_plan* p, int32_t slot, int32_t back, helios_batch_timing* out) {
   HCHECK(slot >= 0 && slot < (int32_t)p->slots.size(), HELIOS_E_INVALID, "slot %d of %zu", slot, p->slots.size());
+  HCHECK(out, HELIOS_E_INVALID, "null timing output");
   PlanSlot& sl = p->slots[slot];
   HCHECK(back >= 0 && back < PlanSlot::kRing && back < sl.tcount, HELIOS_E_RANGE,
          "slot %d: timed batch -%d not recorded", slot, back);
-  cudaEvent_t* ev = &sl.ring[3 * ((sl.tcount - 1 - back) % PlanSlot::kRing)];
+  cudaEvent_t* ev = &sl.ring[PlanSlot::kEv * ((sl.tcount - 1 - back) % PlanSlot::kRing)];
   HCUDA(cudaEventSynchronize(ev[2]));
-  float a = 0, b = 0;
-  HCUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
-  HCUDA(cudaEventElapsedTime(&b, ev[1], ev[2]));
-  if (sample_ms) *sample_ms = a;
-  if (gather_ms) *gather_ms = b;
+  helios_batch_timing t{0, 0, -1.0f, -1.0f, -1.0f, -1.0f};
+  HCUDA(cudaEventElapsedTime(&t.sample_ms, ev[0], ev[1]));
+  HCUDA(cudaEventElapsedTime(&t.gather_ms, ev[1], ev[2]));
+  if (p->link) HCUDA(cudaEventElapsedTime(&t.link_ms, ev[3], ev[4]));
+  if (p->marked) {
+    HCUDA(cudaEventElapsedTime(&t.t_start, p->ev_ref, ev[0]));
+    HCUDA(cudaEventElapsedTime(&t.t_gather, p->ev_ref, ev[1]));
+    HCUDA(cudaEventElapsedTime(&t.t_end, p->ev_ref, ev[2]));
+  }
+  *out = t;
+  return HELIOS_OK;
+}
+
+helios_status plan_mark_impl(helios_plan* p, cudaStream_t st) {
+  HCUDA(cudaEventRecord(p->ev_ref, st));
+  p->marked = true;
   return HELIOS_OK;
 }
 

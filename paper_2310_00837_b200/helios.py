@@ -26,7 +26,7 @@ MAX_RANKS = 64
 STATUS = ["OK", "E_INVALID", "E_RANGE", "E_CAPACITY", "E_NOMEM", "E_CUDA", "E_IO", "E_TIMEOUT", "E_STATE"]
 HOST_ALIAS, TABLE_MAPPED, NO_DIRECT_IO, IO_FAULT_AT = 0x1, 0x2, 0x4, 0x100
 HOST_FILL, HOST_TIER_MAPPED, HOST_STAGED, IO_SYNC = 0x8, 0x10, 0x20, 0x40
-PLAN_NO_GRAPH, PLAN_SERIAL_GATHER, PLAN_INTRA_BATCH = 0x1, 0x2, 0x4
+PLAN_NO_GRAPH, PLAN_SERIAL_GATHER, PLAN_INTRA_BATCH, PLAN_LINK_STREAM = 0x1, 0x2, 0x4, 0x8
 SUBMIT_SEEDS_HOST, SUBMIT_TIMING = 0x1, 0x2
 
 i64, i32, u32, u64, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p
@@ -48,6 +48,11 @@ class helios_cache_desc(ctypes.Structure):
 
 class helios_plan_desc(ctypes.Structure):
     _fields_ = [("max_seeds", i64), ("L", i32), ("fanouts", i32 * MAX_HOPS), ("depth", i32), ("flags", u32)]
+
+
+class helios_batch_timing(ctypes.Structure):
+    _fields_ = [("sample_ms", ctypes.c_float), ("gather_ms", ctypes.c_float), ("link_ms", ctypes.c_float),
+                ("t_start", ctypes.c_float), ("t_gather", ctypes.c_float), ("t_end", ctypes.c_float)]
 
 
 class helios_cache_info(ctypes.Structure):
@@ -81,7 +86,8 @@ _sig = {
                                            ctypes.POINTER(vp)]),
     "helios_plan_submit": (ctypes.c_int, [vp, i32, vp, i64, u64, u32, vp]),
     "helios_plan_wait": (ctypes.c_int, [vp, i32, vp]),
-    "helios_plan_timing": (ctypes.c_int, [vp, i32, i32, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
+    "helios_plan_timing": (ctypes.c_int, [vp, i32, i32, ctypes.POINTER(helios_batch_timing)]),
+    "helios_plan_mark": (ctypes.c_int, [vp, vp]),
 }
 for _n, (_r, _a) in _sig.items():
     _f = getattr(_lib, _n)
@@ -378,7 +384,11 @@ def helios_plan_create(g: Graph, c: Cache | None, B: int, fanouts, depth: int = 
     h = vp()
     _check(_lib.helios_plan_create(g.handle, c.handle if c is not None else None, ctypes.byref(d), ctypes.byref(h)),
            "helios_plan_create")
-    return Plan(h.value, g, c, B, fanouts, depth)
+    p = Plan(h.value, g, c, B, fanouts, depth)
+    # host rows go through the plan's link stream (see helios.h, HELIOS_PLAN_LINK_STREAM)
+    p.link = (c is not None and c.info().host_rows > 0 and bool(flags & PLAN_LINK_STREAM)
+              and not flags & (PLAN_SERIAL_GATHER | PLAN_INTRA_BATCH))
+    return p
 
 
 def helios_plan_submit(p: Plan, slot: int, seeds, key: int, stream=None, timing: bool = False) -> None:
@@ -397,8 +407,14 @@ def helios_plan_wait(p: Plan, slot: int, stream=None) -> None:
     _check(_lib.helios_plan_wait(p.handle, slot, _stream(stream)), "helios_plan_wait")
 
 
-def helios_plan_timing(p: Plan, slot: int, back: int = 0) -> tuple[float, float]:
-    """(sample_ms, gather_ms) of slot's batch `back` submissions ago (0 = last)."""
-    a, b = ctypes.c_float(), ctypes.c_float()
-    _check(_lib.helios_plan_timing(p.handle, slot, back, ctypes.byref(a), ctypes.byref(b)), "helios_plan_timing")
-    return a.value, b.value
+def helios_plan_timing(p: Plan, slot: int, back: int = 0) -> helios_batch_timing:
+    """Device timing of slot's timed batch `back` timed submissions ago (0 = last): sample_ms,
+    gather_ms, link_ms (-1 without a link stream) and t_start / t_gather / t_end in ms since the last
+    helios_plan_mark (-1 if never marked)."""
+    t = helios_batch_timing()
+    _check(_lib.helios_plan_timing(p.handle, slot, back, ctypes.byref(t)), "helios_plan_timing")
+    return t
+
+
+def helios_plan_mark(p: Plan, stream=None) -> None:
+    _check(_lib.helios_plan_mark(p.handle, _stream(stream)), "helios_plan_mark")

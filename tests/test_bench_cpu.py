@@ -45,3 +45,22 @@ def test_capacity_and_tier_helpers():
     assert H == 11_100_000 and S == 99_900_000
     H2, _ = workloads.tier_rows(C["C2"], world_size=3)
     assert H2 * 3 >= C["C2"].V
+
+
+def test_interval_union():
+    """The busy time of overlapping launches (roofline denominator) against brute force on a grid."""
+    sys.path.insert(0, ROOT)
+    import random
+
+    import bench
+    assert bench.interval_union([]) == 0.0
+    assert bench.interval_union([(0, 1), (2, 3)]) == 2.0
+    assert bench.interval_union([(0, 2), (1, 3), (5, 6), (5.5, 5.7)]) == 4.0
+    rng = random.Random(5)
+    for _ in range(50):
+        iv = []
+        for _ in range(rng.randint(1, 12)):
+            a = rng.randint(0, 40)
+            iv.append((a, a + rng.randint(0, 10)))
+        covered = sum(1 for t in range(60) if any(a <= t < b for a, b in iv))
+        assert bench.interval_union(iv) == covered

@@ -56,7 +56,10 @@ def check_slot(p, slot, inp, seeds, key, dref):
                                                           (3, 0, False, False), (2, 1, True, False),
                                                           (3, 0, False, True), (1, 1, True, True),
                                                           (1, 4, False, False), (3, 4, True, False),
-                                                          (2, 4, False, True), (2, 2, False, False)])
+                                                          (2, 4, False, True), (2, 2, False, False),
+                                                          (3, 8, False, False), (2, 8, True, True),
+                                                          (6, 0, False, False), (6, 1, False, True),
+                                                          (6, 8, False, False), (4, 9, True, False)])
 def test_plan_c1_epoch(H, c1, depth, flags, host_seeds, staged):
     cfg = c1.cfg
     Hr, S = workloads.tier_rows(cfg)
@@ -77,8 +80,10 @@ def test_plan_c1_epoch(H, c1, depth, flags, host_seeds, staged):
         for k, b in enumerate(idx):
             check_slot(p, k, c1, c1.batches[b], keys[b], dref)
         if depth > 1 or start % 2 == 0:
-            s_ms, g_ms = H.helios_plan_timing(p, 0)
-            assert s_ms > 0 and g_ms > 0
+            t = H.helios_plan_timing(p, 0)
+            assert t.sample_ms > 0 and t.gather_ms > 0
+            assert (t.link_ms > 0) == p.link
+            assert t.t_start == -1.0   # never marked
     p.free()
     c.free()
 
