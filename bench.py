@@ -246,7 +246,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--parity-batches", type=int, default=2)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no baseline, no parity")
-    ap.add_argument("--depth", type=int, default=6, help="batches in flight (plan slots)")
+    ap.add_argument("--depth", type=int, default=8, help="batches in flight (plan slots)")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly instead of CUDA graphs")
     ap.add_argument("--serial-gather", type=int, default=0, help="1: gathers of successive batches run one at a time")
     ap.add_argument("--intra", action="store_true", help="intra-batch pipeline: per-hop gather passes (NEXT-1)")
@@ -532,6 +532,13 @@ def main():
                    "feature_gbs": round(r["gbs"], 3)}
 
     # ---- roofline of the dominant kernel (lookup+gather, K3/K4) ----
+    probe = None
+    if S > 0 and not args.profile:   # the host link's random-row ceiling for K4 (fresh uniform rows, alone)
+        n_probe, reps = 1 << 18, 8
+        p_ms = H.helios_cache_probe_host(c, n_probe, seed=7, reps=reps)
+        probe = {"Mrows_s": round(n_probe / p_ms / 1e3, 2), "gbs": round(n_probe * cfg.R / p_ms / 1e6, 2),
+                 "how": f"helios_cache_probe_host: K4 host part alone, {n_probe} uniformly random host-tier rows per "
+                        f"launch, fresh rows each of {reps} launches (no L2 reuse)"}
     pk = measured_peaks()
     bw_hbm = float(pk.get("hbm_gbs", HBM_PEAK_FALLBACK))
     bw_pcie = pcie_h2d_peak(torch) if rank == 0 else 0.0
@@ -586,6 +593,12 @@ def main():
                              "storage": round(stor_bytes)},
         "t_roof_ms": round(t_roof_ms, 4),
         "frac_throughput": round(t_roof_ms / (max_ms / steps), 4)})
+    if probe is not None and n_host > 0:
+        got = n_host * (world * steps / (max_ms / 1e3)) / world / 1e6
+        roof["host_link"] = {"achieved_Mrows_s": round(got, 2), "random_row_ceiling": probe,
+                             "frac_of_ceiling": round(got / probe["Mrows_s"], 4),
+                             "note": "host-tier rows per second of the whole timed run vs the measured ceiling of "
+                                     "random zero-copy rows on this platform (DESIGN.md §6)"}
     value = world * steps / (max_ms / 1e3)
     e2e_val = world * steps / e2e_s
     launches_per_step = (3 * L + 2 + 2 + ((2 if args.io_sync else 3) if c.info().file_rows > 0 else 0)

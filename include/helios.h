@@ -214,6 +214,12 @@ helios_status helios_cache_attach_peers(helios_cache* c, const void* blobs, size
 typedef struct {
   int64_t rows_hbm_local, rows_hbm_peer, rows_host, rows_file;
 } helios_gather_stats;
+/* Measurement aid (blocking): the host-link ceiling K4 sees for random host-tier rows.  Runs K4's
+ * host-row part `reps` times, each over n_rows rows drawn uniformly from the host tier's address
+ * range (fresh rows every rep, so no L2 reuse), into a scratch buffer; *ms = mean device time per
+ * rep (CUDA events around the kernel).  E_INVALID for n_rows <= 0 or reps <= 0, E_STATE without a
+ * host tier.  Library-owned scratch is freed before return. */
+helios_status helios_cache_probe_host(helios_cache* c, int64_t n_rows, uint64_t seed, int32_t reps, float* ms);
 helios_status helios_gather(helios_cache* c, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, void* out,
                             helios_gather_stats* stats, void* stream);
 
@@ -233,7 +239,7 @@ helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64
  * batches is serialised on the cache's IO streams.
  *   desc.max_seeds   B: capacity of every slot (n_seeds <= B per submit).
  *   desc.L, fanouts  hops and fanouts (as helios_sample).
- *   desc.depth       number of slots, 1..8.
+ *   desc.depth       number of slots, 1..16.
  *   desc.flags       HELIOS_PLAN_NO_GRAPH: launch the kernels directly on every submit;
  *                    HELIOS_PLAN_SERIAL_GATHER: chain the gathers of successive submits;
  *                    HELIOS_PLAN_INTRA_BATCH: per-hop gather passes overlapping the sampling;

@@ -12,6 +12,14 @@ static thread_local std::string g_last_error;
 
 void set_error(const std::string& s) { g_last_error = s; }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HELIOS_NO_PDL");
+    return !(e && atoi(e) != 0);
+  }();
+  return on;
+}
+
 helios_status fail(helios_status st, const char* fmt, ...) {
   char buf[1024];
   va_list ap;
@@ -372,6 +380,14 @@ helios_status helios_gather(helios_cache* c, const int64_t* nodes, const int64_t
   GUARD_END
 }
 
+helios_status helios_cache_probe_host(helios_cache* c, int64_t n_rows, uint64_t seed, int32_t reps, float* ms) {
+  GUARD_BEGIN
+  HCHECK(c, HELIOS_E_INVALID, "null cache");
+  DeviceGuard dg(c->device);
+  return probe_host_impl(c, n_rows, seed, reps, ms);
+  GUARD_END
+}
+
 helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64_t* seeds, int64_t n_seeds,
                                    const int32_t* fanouts, int32_t L, uint64_t key, const helios_blocks* out,
                                    void* features, helios_gather_stats* stats, void* stream) {
@@ -395,7 +411,7 @@ helios_status helios_plan_create(helios_graph* g, helios_cache* c, const helios_
   HCHECK(g && d && out, HELIOS_E_INVALID, "null argument");
   *out = nullptr;
   HCHECK(!c || c->g == g, HELIOS_E_INVALID, "cache was built on another graph");
-  HCHECK(d->depth >= 1 && d->depth <= 8, HELIOS_E_INVALID, "plan depth %d not in [1,8]", d->depth);
+  HCHECK(d->depth >= 1 && d->depth <= 16, HELIOS_E_INVALID, "plan depth %d not in [1,16]", d->depth);
   HCHECK(d->max_seeds >= 0, HELIOS_E_INVALID, "max_seeds < 0");
   DeviceGuard dg(g->device);
   helios_plan* p = new helios_plan();

@@ -649,6 +649,75 @@ helios_status gather_range_launch(helios_cache* c, GatherWS& w, const int64_t* n
   return gather_pass(c, w, nodes, lo, hi, max_rows, out, stats, first, true, kPartAll, st);
 }
 
+// ---- host-link probe (measurement) --------------------------------------------------------------
+// Fills a host list with n uniformly random rows of the host tier's address range (fresh per rep,
+// SplitMix64 of (seed, rep, i)) and the ctl words the host part of K4 reads.
+__global__ void k_probe_list(int64_t* li, uint64_t* lw, unsigned long long* ctl, int64_t n, int64_t range, uint64_t seed) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = t; i < n; i += nt) {
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * (uint64_t)(i + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    li[i] = i;
+    lw[i] = (1ull << 62) | (uint64_t)__umul64hi(z, (uint64_t)range);
+  }
+  if (t == 0) {
+    for (int q = 0; q < kCtlWords; q++) ctl[q] = 0;
+    ctl[kListHost] = (unsigned long long)n;
+  }
+}
+
+helios_status probe_host_impl(helios_cache* c, int64_t n, uint64_t seed, int32_t reps, float* ms) {
+  HCHECK(n > 0 && reps > 0 && ms, HELIOS_E_INVALID, "probe: n_rows %lld, reps %d", (long long)n, reps);
+  HCHECK(c->S > 0 && c->d_host_tier, HELIOS_E_STATE, "probe: the cache has no host tier");
+  const int64_t range = (c->flags & HELIOS_CACHE_HOST_ALIAS) ? c->V : c->S;
+  GatherWS w;
+  HCUDA(cudaMalloc(&w.d_list_i, kLists * n * 8));
+  HCUDA(cudaMalloc(&w.d_list_w, kLists * n * 8));
+  HCUDA(cudaMalloc(&w.d_ctl, kCtlWords * sizeof(unsigned long long)));
+  w.cap = n;
+  char* out = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaStream_t st = nullptr;
+  helios_status s = HELIOS_OK;
+  float tot = 0;
+  auto run = [&]() -> helios_status {
+    HCUDA(cudaMalloc(&out, n * (int64_t)c->R));
+    HCUDA(cudaEventCreate(&e0));
+    HCUDA(cudaEventCreate(&e1));
+    HCUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    GatherArgs a = make_args(c, w, out, nullptr, false, kPartHost);
+    a.staged = false;
+    a.L.i[kListHost] = w.d_list_i + kListHost * n;
+    a.L.w[kListHost] = w.d_list_w + kListHost * n;
+    for (int r = 0; r < reps; r++) {
+      k_probe_list<<<c->sms * 4, 256, 0, st>>>(a.L.i[kListHost], a.L.w[kListHost], w.d_ctl, n, range,
+                                                seed ^ (0x5851F42D4C957F2Dull * (uint64_t)(r + 1)));
+      HCUDA(cudaEventRecord(e0, st));
+      launch_gather_any(a, c->sms, st);
+      HCUDA(cudaEventRecord(e1, st));
+      HCUDA(cudaEventSynchronize(e1));
+      float t = 0;
+      HCUDA(cudaEventElapsedTime(&t, e0, e1));
+      tot += t;
+    }
+    return HELIOS_OK;
+  };
+  s = run();
+  if (st) cudaStreamSynchronize(st);
+  if (out) cudaFree(out);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (st) cudaStreamDestroy(st);
+  cudaFree(w.d_list_i);
+  cudaFree(w.d_list_w);
+  cudaFree(w.d_ctl);
+  w = GatherWS{};
+  if (s == HELIOS_OK) *ms = tot / reps;
+  return s;
+}
+
 // K5 / K6 on the cache's IO streams for the misses recorded in w by the preceding gather_launch on
 // `st`.  IO batches are serialised across gather contexts through ev_io_done (ring sequence
 // numbers advance per batch in k_io_finish).

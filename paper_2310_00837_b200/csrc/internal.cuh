@@ -50,6 +50,8 @@ struct DeviceGuard {
 // Programmatic dependent launch (sm_90+): the kernel may start launching while its predecessor in
 // the stream drains; it must execute griddepcontrol.wait (pdl_wait) before touching the
 // predecessor's results.  Captured into CUDA graphs as programmatic edges.
+// HELIOS_NO_PDL=1 (read once): plain stream-ordered launches instead (ablation).
+bool pdl_enabled();
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
@@ -61,7 +63,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, c
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -339,6 +341,8 @@ helios_status gather_host_launch(helios_cache* c, GatherWS& w, void* out, cudaSt
 helios_status gather_range_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* lo,
                                   const int64_t* hi, int64_t max_rows, void* out, helios_gather_stats* stats, bool first,
                                   cudaStream_t st);
+// Host-link probe: mean device time (ms) of K4's host part over n uniformly random host-tier rows.
+helios_status probe_host_impl(helios_cache* c, int64_t n, uint64_t seed, int32_t reps, float* ms);
 // IO rings for the misses of the last gather_launch on `st` (not capturable: cross-stream events).
 helios_status io_launch(helios_cache* c, GatherWS& w, void* out, cudaStream_t st);
 helios_status validate_csr_device(const int64_t* indptr, const int32_t* indices, int64_t V, int64_t E, int* d_flag,

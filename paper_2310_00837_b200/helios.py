@@ -78,6 +78,7 @@ _sig = {
     "helios_cache_export": (ctypes.c_int, [vp, vp, ctypes.POINTER(ctypes.c_size_t)]),
     "helios_cache_attach_peers": (ctypes.c_int, [vp, vp, ctypes.c_size_t]),
     "helios_gather": (ctypes.c_int, [vp, vp, vp, i64, vp, vp, vp]),
+    "helios_cache_probe_host": (ctypes.c_int, [vp, i64, u64, i32, ctypes.POINTER(ctypes.c_float)]),
     "helios_batch_prepare": (ctypes.c_int, [vp, vp, vp, i64, vp, i32, u64, ctypes.POINTER(helios_blocks), vp, vp, vp]),
     "helios_sync": (ctypes.c_int, [vp, vp]),
     "helios_plan_create": (ctypes.c_int, [vp, vp, ctypes.POINTER(helios_plan_desc), ctypes.POINTER(vp)]),
@@ -314,6 +315,14 @@ def helios_batch_prepare(g: Graph, c: Cache, seeds: torch.Tensor, fanouts, key: 
     _check(_lib.helios_batch_prepare(g.handle, c.handle, _ptr(seeds), seeds.numel(), _ptr(fan), len(fan),
                                      key & (2**64 - 1), ctypes.byref(s), _ptr(features), _ptr(stats),
                                      _stream(stream)), "helios_batch_prepare")
+
+
+def helios_cache_probe_host(c: Cache, n_rows: int, seed: int = 1, reps: int = 5) -> float:
+    """Mean ms of K4's host part over n_rows uniformly random host-tier rows (fresh each rep)."""
+    ms = ctypes.c_float()
+    _check(_lib.helios_cache_probe_host(c.handle, n_rows, seed & (2**64 - 1), reps, ctypes.byref(ms)),
+           "helios_cache_probe_host")
+    return ms.value
 
 
 def helios_sync(c: Cache, stream=None) -> None:

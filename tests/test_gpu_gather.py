@@ -153,3 +153,28 @@ def test_batch_prepare_c1_epoch(H, c1, c1_hot):
         assert np.array_equal(feats[:n].cpu().numpy(), ref)
         assert stats.cpu().numpy().tolist() == oracle.lookup_counts(dref, orc.nodes).tolist()
     c.free()
+
+
+@pytest.mark.parametrize("alias", [False, True])
+def test_probe_host(H, c1, c1_hot, alias):
+    """helios_cache_probe_host: runs K4's host part on random host-tier rows and reports a time;
+    argument and state errors are synchronous; the cache stays usable (a gather afterwards is exact)."""
+    g, hot = c1_hot
+    Hr, S = workloads.tier_rows(c1.cfg)
+    c = H.helios_cache_build(g, hot, c1.cfg.R, Hr, S, host_table=c1.table, feature_path=c1.feature_path,
+                             header_bytes=c1.header, file_stride=c1.stride, flags=H.HOST_ALIAS if alias else 0)
+    ms = H.helios_cache_probe_host(c, 50_000, seed=3, reps=3)
+    assert 0 < ms < 1000
+    for n, reps in ((0, 1), (10, 0)):
+        with pytest.raises(H.HeliosError) as e:
+            H.helios_cache_probe_host(c, n, reps=reps)
+        assert e.value.name == "E_INVALID"
+    dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S, host_slot_is_id=alias)
+    nodes = np.arange(c1.cfg.V, dtype=np.int64)
+    gather_and_check(H, c, c1, nodes, oracle.lookup_counts(dref, nodes))
+    c.free()
+    c0 = H.helios_cache_build(g, hot, c1.cfg.R, c1.cfg.V, 0, host_table=c1.table)
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_cache_probe_host(c0, 100)
+    assert e.value.name == "E_STATE"
+    c0.free()

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <unistd.h>
 #define CK(x) do{cudaError_t e=(x); if(e!=cudaSuccess){fprintf(stderr,"%s:%d %s\n",__FILE__,__LINE__,cudaGetErrorString(e)); exit(1);} }while(0)
 
 __device__ __forceinline__ int4 ld_nc(const int4* p) {
@@ -64,6 +65,18 @@ __global__ void burst(const int* __restrict__ big, int64_t n, unsigned* sink, in
     acc += big[x % n];
   }
   if (acc == 0xFFFFFFFFu) sink[0] = acc;
+}
+
+// Compute-only spin for `ns` nanoseconds (between batches: SM activity without memory traffic).
+__global__ void spin(int64_t ns, unsigned* sink) {
+  const uint64_t t0 = clock64();
+  uint64_t x = threadIdx.x;
+  while ((int64_t)(clock64() - t0) < ns * 2) x = x * 6364136223846793005ull + 1;  // ~2 GHz
+  if (x == 42) sink[0] = (unsigned)x;
+}
+// Streaming writes of `n` ints (between batches: write-only HBM traffic).
+__global__ void wburst(int* big, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) big[i] = (int)i;
 }
 
 // mode 1: random 4 B reads over 7.5 GB + random atomics over 32 MB
@@ -143,11 +156,14 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&tickets, nb * 8 * 8));
   CK(cudaFuncGetAttributes(&fa, gather_dyn<8>));
   CK(cudaFuncGetAttributes(&fa, burst));
+  CK(cudaFuncGetAttributes(&fa, spin));
+  CK(cudaFuncGetAttributes(&fa, wburst));
   // cases: {noise mode, noise CTAs (0 = none), between-batch burst (0 none, 1 over 7.5 GB, 2 over 64 MB)}
   struct Case { const char* name; int mode, ctas, burst_kind; };
   Case cases[] = {{"none", 0, 0, 0}, {"concurrent rand7.5GB x148", 2, 148, 0}, {"concurrent rand7.5GB x16", 2, 16, 0},
                   {"concurrent stream7.5GB x148", 5, 148, 0}, {"burst rand7.5GB between batches", 0, 0, 1},
-                  {"burst rand64MB between batches", 0, 0, 2}};
+                  {"burst rand64MB between batches", 0, 0, 2}, {"spin 20us between batches", 0, 0, 3},
+                  {"write 64MB between batches", 0, 0, 4}, {"host sleep 50us between batches", 0, 0, 5}};
   for (const Case& cs : cases) {
     for (int dyn = 0; dyn < 2; dyn++) {
       if (cs.mode) {
@@ -160,7 +176,11 @@ int main(int argc, char** argv) {
         CK(cudaMemsetAsync(tickets, 0, nb * 8 * 8, sg));
         float tot = 0;
         for (int i = 0; i < nb; i++) {
-          if (cs.burst_kind) burst<<<148 * 4, 256, 0, sg>>>(big, cs.burst_kind == 1 ? nbig : (16 << 20), tab, 32);
+          if (cs.burst_kind == 1 || cs.burst_kind == 2)
+            burst<<<148 * 4, 256, 0, sg>>>(big, cs.burst_kind == 1 ? nbig : (16 << 20), tab, 32);
+          else if (cs.burst_kind == 3) spin<<<148 * 4, 256, 0, sg>>>(20000, tab);
+          else if (cs.burst_kind == 4) wburst<<<148 * 4, 256, 0, sg>>>(big, 16 << 20);
+          else if (cs.burst_kind == 5) usleep(50);
           cudaEventRecord(e0, sg);
           if (dyn) gather_dyn<8><<<148, 256, 0, sg>>>(hd, di + offs[i], out, offs[i + 1] - offs[i], R, tickets + 8 * i);
           else gather<8, false><<<148, 256, 0, sg>>>(hd, di + offs[i], out, offs[i + 1] - offs[i], R);
