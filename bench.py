@@ -194,6 +194,25 @@ def file_peak(path: str, stride: int, header: int, threads: int, secs: float = 3
     return json.loads(out)
 
 
+def sampling_accesses(batch: dict, indptr: np.ndarray, fanouts) -> dict:
+    """Minimum DRAM work of one batch's sampling + lookup at sector granularity:
+    per hop, one 32 B sector per frontier row for its indptr pair and at least ceil(4k/32) sectors for
+    the k sampled positions of its adjacency; one sector per node for its directory word.  Streaming
+    bytes: block CSR writes (4 per edge and per indptr entry) and the node list (8 per node)."""
+    nodes, lc = batch["nodes"], batch["level_counts"]
+    sectors = stream = 0
+    for h, f in enumerate(fanouts):
+        nh = nodes[: lc[h]]
+        d = indptr[nh + 1] - indptr[nh]
+        k = d if f < 0 else np.minimum(d, f)
+        sectors += len(nh) + int(((4 * k + 31) // 32).sum())
+        stream += 4 * int(k.sum()) + 4 * (len(nh) + 1)
+    n_l = int(lc[len(fanouts)])
+    sectors += n_l
+    stream += 8 * n_l
+    return {"sectors": sectors, "stream_bytes": stream}
+
+
 def interval_union(iv) -> float:
     """Total length of the union of [a, b) intervals (ms): the time during which at least one of
     the overlapping launches was running."""
@@ -458,6 +477,7 @@ def main():
     st = [0, 0, 0, 0]
     n_rows = 0
     blk0, _, stats0 = plan.outputs[0]
+    acc = []   # sampling access counts of the first batches (end-to-end sector-granular roofline)
     for i in range(args.steps):
         b = seq[args.warmup + i]
         H.helios_plan_submit(plan, 0, seed_of[b], keys[b], stream)
@@ -465,6 +485,8 @@ def main():
         stream.synchronize()
         st = [x + int(y) for x, y in zip(st, stats0.cpu().tolist())]
         n_rows += int(blk0.level_counts[L].item())
+        if i < 16:
+            acc.append(sampling_accesses(blk0.to_host(), inp.graph.indptr, cfg.fanouts))
     H.helios_sync(c)
 
     # ---- e2e: through the public API with host buffers (pinned seeds in, counts out) ----
@@ -593,6 +615,22 @@ def main():
                              "storage": round(stor_bytes)},
         "t_roof_ms": round(t_roof_ms, 4),
         "frac_throughput": round(t_roof_ms / (max_ms / steps), 4)})
+    # end-to-end (sampling + lookup + gather) bound: streaming bytes at the HBM copy peak plus random
+    # 32 B sectors at the random-sector rate measured live over this graph's CSR, plus the host link
+    n_rs = 1 << 24
+    sec_rate = n_rs / (H.helios_graph_probe_random(g, n_rs, reps=5) * 1e6) if not args.topo_host else None  # sectors/ns
+    if acc and sec_rate:
+        a_sec = statistics.mean(x["sectors"] for x in acc)
+        a_str = statistics.mean(x["stream_bytes"] for x in acc) + hbm_bytes
+        t_e2e = (a_str / bw_hbm + a_sec / sec_rate + pcie_bytes / max(bw_pcie, 1e-9) + nvl_bytes / bw_nvl
+                 + stor_bytes / bw_file) / 1e6
+        roof["end_to_end"] = {"random_sectors_per_batch": round(a_sec), "stream_bytes_per_batch": round(a_str),
+                              "sector_rate_G_s": round(sec_rate, 2), "t_roof_ms": round(t_e2e, 4),
+                              "frac": round(t_e2e / (max_ms / steps), 4),
+                              "note": "whole step vs stream/BW_hbm + sectors/sector_rate + tier-link terms; sectors = "
+                                      "per hop one per frontier row (indptr) + ceil(4k/32) per row (sampled positions) + "
+                                      "one per node (directory), averaged over the first 16 timed batches; sector_rate = "
+                                      "helios_graph_probe_random (uniform 4 B loads over the CSR indices)"}
     if probe is not None and n_host > 0:
         got = n_host * (world * steps / (max_ms / 1e3)) / world / 1e6
         roof["host_link"] = {"achieved_Mrows_s": round(got, 2), "random_row_ceiling": probe,

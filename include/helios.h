@@ -126,6 +126,11 @@ helios_status helios_sample(helios_graph* g, const int64_t* seeds, int64_t n_see
 
 /* Waits for `stream`, then returns and clears the graph's latched device error (HELIOS_OK if none). */
 helios_status helios_graph_sync(helios_graph* g, void* stream);
+/* Measurement aid (blocking): the random-sector ceiling the sampler sees.  `reps` launches of n_reads
+ * independent uniformly random 4 B loads over the graph's CSR indices array (each touches one 32 B
+ * sector; fresh positions every launch); *ms = mean device time per launch.  E_INVALID for
+ * n_reads <= 0 or reps <= 0. */
+helios_status helios_graph_probe_random(helios_graph* g, int64_t n_reads, int32_t reps, float* ms);
 
 /* helios_presample: one pass of pre-sampling that "collects all vertices' hotness" (PAPER.md:212
  * §3.2.2 Cache Initialization; reading 8).  Seeds are split into consecutive batches of `batch`

@@ -201,6 +201,14 @@ helios_status helios_sample(helios_graph* g, const int64_t* seeds, int64_t n_see
   GUARD_END
 }
 
+helios_status helios_graph_probe_random(helios_graph* g, int64_t n_reads, int32_t reps, float* ms) {
+  GUARD_BEGIN
+  HCHECK(g, HELIOS_E_INVALID, "null graph");
+  DeviceGuard dg(g->device);
+  return probe_random_impl(g, n_reads, reps, ms);
+  GUARD_END
+}
+
 helios_status helios_graph_sync(helios_graph* g, void* stream) {
   GUARD_BEGIN
   HCHECK(g, HELIOS_E_INVALID, "null graph");

@@ -341,6 +341,8 @@ helios_status gather_host_launch(helios_cache* c, GatherWS& w, void* out, cudaSt
 helios_status gather_range_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* lo,
                                   const int64_t* hi, int64_t max_rows, void* out, helios_gather_stats* stats, bool first,
                                   cudaStream_t st);
+// Random-sector probe: mean device time (ms) of n uniformly random 4 B loads over the CSR indices.
+helios_status probe_random_impl(helios_graph* g, int64_t n, int32_t reps, float* ms);
 // Host-link probe: mean device time (ms) of K4's host part over n uniformly random host-tier rows.
 helios_status probe_host_impl(helios_cache* c, int64_t n, uint64_t seed, int32_t reps, float* ms);
 // IO rings for the misses of the last gather_launch on `st` (not capturable: cross-stream events).

@@ -403,6 +403,51 @@ helios_status hot_count_enqueue(const int64_t* nodes, const int64_t* n_nodes, in
   return HELIOS_OK;
 }
 
+// ---- random-sector probe (measurement) --------------------------------------------------------
+// Every thread issues `per` independent loads at SplitMix64-random positions of indices[E].
+__global__ void k_probe_random(const int32_t* __restrict__ a, int64_t E, int per, uint64_t seed, int* sink) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  int acc = 0;
+  for (int k = 0; k < per; k++) {
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * (t * (uint64_t)per + k + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    acc += __ldcg(a + (int64_t)__umul64hi(z, (uint64_t)E));
+  }
+  if (acc == 0x7FFFFFFF) *sink = acc;
+}
+
+helios_status probe_random_impl(helios_graph* g, int64_t n, int32_t reps, float* ms) {
+  HCHECK(n > 0 && reps > 0 && ms, HELIOS_E_INVALID, "probe: n_reads %lld, reps %d", (long long)n, reps);
+  HCHECK(g->E > 0 && !g->topo_host, HELIOS_E_STATE, "probe: no HBM-resident CSR indices");
+  const int per = 16;
+  const int64_t threads = (n + per - 1) / per;
+  const int grid = (int)std::max<int64_t>(1, (threads + 255) / 256);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int* sink = nullptr;
+  HCUDA(cudaMalloc(&sink, sizeof(int)));
+  HCUDA(cudaEventCreate(&e0));
+  HCUDA(cudaEventCreate(&e1));
+  float tot = 0;
+  cudaError_t err = cudaSuccess;
+  for (int r = 0; r < reps && err == cudaSuccess; r++) {
+    cudaEventRecord(e0, 0);
+    k_probe_random<<<grid, 256>>>(g->indices, g->E, per, 0xA5A5A5A5ull * (uint64_t)(r + 1), sink);
+    cudaEventRecord(e1, 0);
+    err = cudaEventSynchronize(e1);
+    float t = 0;
+    if (err == cudaSuccess) err = cudaEventElapsedTime(&t, e0, e1);
+    tot += t;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  if (err != cudaSuccess) return fail(HELIOS_E_CUDA, "probe_random: %s", cudaGetErrorString(err));
+  *ms = tot / reps * (float)n / (float)(threads * per);  // per n reads
+  return HELIOS_OK;
+}
+
 // ---- host side --------------------------------------------------------------------------------
 
 helios_status sample_bounds(int64_t n_seeds, const int32_t* fanouts, int32_t L, int64_t V, int64_t E, int64_t* max_nodes,

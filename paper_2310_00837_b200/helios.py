@@ -70,6 +70,7 @@ _sig = {
     "helios_graph_device_csr": (ctypes.c_int, [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]),
     "helios_sample_bounds": (ctypes.c_int, [i64, vp, i32, i64, i64, ctypes.POINTER(i64), vp, vp]),
     "helios_sample": (ctypes.c_int, [vp, vp, i64, vp, i32, u64, ctypes.POINTER(helios_blocks), vp]),
+    "helios_graph_probe_random": (ctypes.c_int, [vp, i64, i32, ctypes.POINTER(ctypes.c_float)]),
     "helios_graph_sync": (ctypes.c_int, [vp, vp]),
     "helios_presample": (ctypes.c_int, [vp, vp, i64, i32, vp, i32, vp, vp, vp]),
     "helios_cache_build": (ctypes.c_int, [vp, ctypes.POINTER(helios_cache_desc), ctypes.POINTER(vp)]),
@@ -229,6 +230,13 @@ def helios_sample(g: Graph, seeds: torch.Tensor, fanouts, key: int, out: Blocks,
     s = out.struct()
     _check(_lib.helios_sample(g.handle, _ptr(seeds), seeds.numel(), _ptr(fan), len(fan), key & (2**64 - 1),
                               ctypes.byref(s), _stream(stream)), "helios_sample")
+
+
+def helios_graph_probe_random(g: Graph, n_reads: int, reps: int = 5) -> float:
+    """Mean ms of n_reads uniformly random 4 B loads over the CSR indices (random-sector ceiling)."""
+    ms = ctypes.c_float()
+    _check(_lib.helios_graph_probe_random(g.handle, n_reads, reps, ctypes.byref(ms)), "helios_graph_probe_random")
+    return ms.value
 
 
 def helios_graph_sync(g: Graph, stream=None) -> None:

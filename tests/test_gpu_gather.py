@@ -165,6 +165,10 @@ def test_probe_host(H, c1, c1_hot, alias):
                              header_bytes=c1.header, file_stride=c1.stride, flags=H.HOST_ALIAS if alias else 0)
     ms = H.helios_cache_probe_host(c, 50_000, seed=3, reps=3)
     assert 0 < ms < 1000
+    assert 0 < H.helios_graph_probe_random(g, 1 << 20, reps=2) < 1000
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_graph_probe_random(g, 0)
+    assert e.value.name == "E_INVALID"
     for n, reps in ((0, 1), (10, 0)):
         with pytest.raises(H.HeliosError) as e:
             H.helios_cache_probe_host(c, n, reps=reps)
