@@ -12,6 +12,7 @@
 //   request, polls its CQ entry (acquire, system scope), then the whole warp moves the row from the
 //   staging slot into the output feature buffer and frees the slot.
 #include <algorithm>
+#include <cstdlib>
 
 #include "device.cuh"
 
@@ -100,6 +101,7 @@ struct GatherArgs {
   ListPtrs L;
   unsigned long long* ctl;  // list counts, staging split, host / stage row tickets
   int part;                 // kPartAll / kPartHbm / kPartHost
+  int host_warps;           // kPartAll: zero-copy host-row warps per 8 warps
   bool staged;
   bool accumulate;          // intra-batch passes: add this pass's row counts to stats
   const char* stage;        // device alias of the pinned staging rows
@@ -254,10 +256,10 @@ __global__ void __launch_bounds__(256, 4) k_gather_lists(GatherArgs a) {
   }
   // kPartAll warp roles: r = gw % 8.  r == 0: zero-copy host rows; r == 1 (staged mode): stage
   // consumers; other warps: peer then local HBM rows.
-  const int nspecial = (a.part == kPartAll && n_host > 0) ? (a.staged ? 2 : 1) : 0;
+  const int nspecial = (a.part == kPartAll && n_host > 0) ? (a.staged ? 1 : 0) + a.host_warps : 0;
   const int r = (int)(gw & 7);
   if (r < nspecial) {
-    if (r == 0) host_rows<VPL, UH>(a, n_gpu, lane, nvec);
+    if (r < a.host_warps) host_rows<VPL, UH>(a, n_gpu, lane, nvec);
     else staged_rows(a, n_gpu, n_stage, lane, nvec);
     return;
   }
@@ -497,18 +499,13 @@ helios_status io_preload_kernels() {
   return HELIOS_OK;
 }
 
-// Persistent grid: exactly the resident CTAs, so every host-row warp is live from the start.  The
-// host-only part (link stream) uses one CTA per SM: 1184 warps keep the link saturated
-// (tools/hostorder.cu) and leave the rest of the SMs to the sampling of other batches.
+// Persistent grid of one CTA per SM (8 warps each; one in 8 serves host rows).  A gather waits on
+// PCIe reads for most of its life, so a smaller grid leaves SM slots to the other in-flight batches'
+// sampling: measured against 4 CTAs per SM, C3 +6 % and C2 +6 %; 74-296 CTAs are within noise on
+// C3, 74 is 4 % slower on C2; 2 or 4 host warps per 8 are slower.
 template <int VPL, int U, int UH>
 static void launch_gather(const GatherArgs& a, int sms, cudaStream_t st) {
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_lists<VPL, U, UH>, 256, 0);
-    per_sm = std::max(per_sm, 1);
-  }
-  const int grid = a.part == kPartHost ? sms : sms * per_sm;
-  launch_pdl(k_gather_lists<VPL, U, UH>, dim3(grid), dim3(256), st, a);
+  launch_pdl(k_gather_lists<VPL, U, UH>, dim3(sms), dim3(256), st, a);
 }
 
 static void launch_gather_any(const GatherArgs& a, int sms, cudaStream_t st) {
@@ -582,6 +579,7 @@ static GatherArgs make_args(helios_cache* c, GatherWS& w, void* out, helios_gath
   a.R = c->R;
   a.ctl = w.d_ctl;
   a.part = part;
+  a.host_warps = 1;
   a.staged = staged;
   a.accumulate = accumulate;
   a.stage = w.d_stage;
