@@ -489,29 +489,21 @@ def main():
             acc.append(sampling_accesses(blk0.to_host(), inp.graph.indptr, cfg.fanouts))
     H.helios_sync(c)
 
-    # ---- e2e: through the public API with host buffers (pinned seeds in, counts out) ----
+    # ---- e2e: through the public API with host buffers (host seeds in, counts + tier stats out) ----
     host_seeds = {b: np.ascontiguousarray(inp.batches[b]) for b in sorted(set(seq))}
-    out_host = torch.empty(depth, L + 1 + 4, dtype=torch.int64).pin_memory()
+    out_host = np.empty((depth, L + 1 + 4), dtype=np.int64)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-
-    def consume(k):
-        blk, _, sts = plan.outputs[k]
-        H.helios_plan_wait(plan, k, stream)
-        out_host[k, : L + 1].copy_(blk.level_counts, non_blocking=True)
-        out_host[k, L + 1:].copy_(sts, non_blocking=True)
-
     t_e2e = time.perf_counter()
     for i in range(args.steps):
         b = seq[args.warmup + i]
-        H.helios_plan_submit(plan, i % depth, host_seeds[b], keys[b], stream)
-        if i >= depth - 1:
-            consume((i - depth + 1) % depth)
-            stream.synchronize()
-    for i in range(max(0, args.steps - depth + 1), args.steps):
-        consume(i % depth)
-    stream.synchronize()
+        k = i % depth
+        if i >= depth:   # the slot's previous batch: its result must be on the host before reuse
+            H.helios_plan_readback(plan, k, out_host[k])
+        H.helios_plan_submit(plan, k, host_seeds[b], keys[b], stream, readback=True)
+    for i in range(max(0, args.steps - depth), args.steps):
+        H.helios_plan_readback(plan, i % depth, out_host[i % depth])
     e2e_s = time.perf_counter() - t_e2e
     H.helios_sync(c)
     e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")

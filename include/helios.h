@@ -266,6 +266,8 @@ helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64
 #define HELIOS_PLAN_LINK_STREAM 0x8u    /* ablation: host-tier rows of every batch on a shared link stream */
 #define HELIOS_SUBMIT_SEEDS_HOST 0x1u  /* seeds pointer is host memory (copied with the parameters, H2D) */
 #define HELIOS_SUBMIT_TIMING 0x2u      /* record device timing events around the sample / gather phases */
+#define HELIOS_SUBMIT_READBACK 0x4u    /* copy the batch's level counts and tier stats to plan-owned pinned
+                                          host memory at its end (read with helios_plan_readback) */
 typedef struct helios_plan helios_plan;
 typedef struct {
   int64_t max_seeds;
@@ -288,6 +290,11 @@ helios_status helios_plan_outputs(helios_plan* p, int32_t slot, helios_blocks* b
  * alive until the batch completes).  n_seeds <= desc.max_seeds (else E_CAPACITY). */
 helios_status helios_plan_submit(helios_plan* p, int32_t slot, const int64_t* seeds, int64_t n_seeds, uint64_t key,
                                  uint32_t flags, void* stream);
+/* Blocks until the last batch submitted to `slot` (with HELIOS_SUBMIT_READBACK) is done, then writes
+ * its level counts and tier stats to host `out`: int64[L + 1 + 4] = n_0..n_L, rows_hbm_local,
+ * rows_hbm_peer, rows_host, rows_file (stats 0 for a sample-only plan).  E_STATE if that batch was
+ * not submitted with HELIOS_SUBMIT_READBACK. */
+helios_status helios_plan_readback(helios_plan* p, int32_t slot, int64_t* out);
 /* Makes `stream` wait for the last batch submitted to `slot`. */
 helios_status helios_plan_wait(helios_plan* p, int32_t slot, void* stream);
 /* Device timing of a batch submitted to `slot` with HELIOS_SUBMIT_TIMING: back = 0 is the slot's

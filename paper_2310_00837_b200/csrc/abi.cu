@@ -39,6 +39,7 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
 helios_status plan_wait_impl(helios_plan* p, int32_t slot, cudaStream_t st);
 helios_status plan_timing_impl(helios_plan* p, int32_t slot, int32_t back, helios_batch_timing* out);
 helios_status plan_mark_impl(helios_plan* p, cudaStream_t st);
+helios_status plan_readback_impl(helios_plan* p, int32_t slot, int64_t* out);
 helios_status plan_outputs_impl(helios_plan* p, int32_t slot, helios_blocks* blocks, void** features,
                                 helios_gather_stats** stats);
 
@@ -481,6 +482,14 @@ helios_status helios_plan_timing(helios_plan* p, int32_t slot, int32_t back, hel
   HCHECK(p, HELIOS_E_INVALID, "null plan");
   DeviceGuard dg(p->g->device);
   return plan_timing_impl(p, slot, back, out);
+  GUARD_END
+}
+
+helios_status helios_plan_readback(helios_plan* p, int32_t slot, int64_t* out) {
+  GUARD_BEGIN
+  HCHECK(p, HELIOS_E_INVALID, "null plan");
+  DeviceGuard dg(p->g->device);
+  return plan_readback_impl(p, slot, out);
   GUARD_END
 }
 

@@ -273,6 +273,8 @@ struct PlanSlot {
   static constexpr int kEv = 5;   // per timed batch: {start, sampled, end} on the slot stream,
                                   // {host start, host end} on the link stream
   std::vector<cudaEvent_t> ring;  // kRing x kEv timing events (timed submits only)
+  int64_t* h_rb = nullptr;        // pinned readback {level_counts[L+1], stats[4]} (HELIOS_SUBMIT_READBACK)
+  bool rb_valid = false;          // the last submit requested a readback
   int64_t count = 0;              // batches submitted to this slot
   int64_t tcount = 0;             // timed batches submitted to this slot
   bool submitted = false;

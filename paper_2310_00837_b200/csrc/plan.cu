@@ -22,6 +22,7 @@ void plan_free_impl(helios_plan* p) {
     ws_free(s.ws);
     gws_free(s.gws);
     if (s.mem) cudaFree(s.mem);
+    if (s.h_rb) cudaFreeHost(s.h_rb);
     if (s.feats) cudaFree(s.feats);
     if (s.g_sample) cudaGraphExecDestroy(s.g_sample);
     if (s.g_gather) cudaGraphExecDestroy(s.g_gather);
@@ -114,6 +115,7 @@ helios_status plan_create_impl(helios_plan* p) {
     s = ws_ensure(g, sl.ws, d.max_seeds, d.fanouts, d.L);
     if (s != HELIOS_OK) return s;
     HCUDA(cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking));
+    HCUDA(cudaHostAlloc(&sl.h_rb, (HELIOS_MAX_HOPS + 1 + 4) * sizeof(int64_t), cudaHostAllocDefault));
     HCUDA(cudaEventCreateWithFlags(&sl.ev_caller, cudaEventDisableTiming));
     HCUDA(cudaEventCreateWithFlags(&sl.ev_end, cudaEventDisableTiming));
     sl.ring.assign(PlanSlot::kEv * PlanSlot::kRing, nullptr);
@@ -229,6 +231,12 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
     HCUDA(cudaEventRecord(ev[2], sl.stream));
     sl.tcount++;
   }
+  sl.rb_valid = (flags & HELIOS_SUBMIT_READBACK) != 0;
+  if (sl.rb_valid) {
+    const int L = p->d.L;
+    HCUDA(cudaMemcpyAsync(sl.h_rb, sl.blocks.level_counts, (L + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, sl.stream));
+    if (p->c) HCUDA(cudaMemcpyAsync(sl.h_rb + L + 1, sl.stats, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, sl.stream));
+  }
   HCUDA(cudaEventRecord(sl.ev_end, sl.stream));
   sl.count++;
   sl.submitted = true;
@@ -240,6 +248,18 @@ helios_status plan_wait_impl(helios_plan* p, int32_t slot, cudaStream_t st) {
   PlanSlot& sl = p->slots[slot];
   if (!sl.submitted) return HELIOS_OK;
   HCUDA(cudaStreamWaitEvent(st, sl.ev_end, 0));
+  return HELIOS_OK;
+}
+
+helios_status plan_readback_impl(helios_plan* p, int32_t slot, int64_t* out) {
+  HCHECK(slot >= 0 && slot < (int32_t)p->slots.size(), HELIOS_E_INVALID, "slot %d of %zu", slot, p->slots.size());
+  HCHECK(out, HELIOS_E_INVALID, "null readback output");
+  PlanSlot& sl = p->slots[slot];
+  HCHECK(sl.submitted && sl.rb_valid, HELIOS_E_STATE, "slot %d: last batch not submitted with HELIOS_SUBMIT_READBACK", slot);
+  HCUDA(cudaEventSynchronize(sl.ev_end));
+  const int L = p->d.L;
+  memcpy(out, sl.h_rb, (L + 1) * sizeof(int64_t));
+  for (int q = 0; q < 4; q++) out[L + 1 + q] = p->c ? sl.h_rb[L + 1 + q] : 0;
   return HELIOS_OK;
 }
 

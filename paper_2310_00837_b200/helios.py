@@ -27,7 +27,7 @@ STATUS = ["OK", "E_INVALID", "E_RANGE", "E_CAPACITY", "E_NOMEM", "E_CUDA", "E_IO
 HOST_ALIAS, TABLE_MAPPED, NO_DIRECT_IO, IO_FAULT_AT = 0x1, 0x2, 0x4, 0x100
 HOST_FILL, HOST_TIER_MAPPED, HOST_STAGED, IO_SYNC = 0x8, 0x10, 0x20, 0x40
 PLAN_NO_GRAPH, PLAN_SERIAL_GATHER, PLAN_INTRA_BATCH, PLAN_LINK_STREAM = 0x1, 0x2, 0x4, 0x8
-SUBMIT_SEEDS_HOST, SUBMIT_TIMING = 0x1, 0x2
+SUBMIT_SEEDS_HOST, SUBMIT_TIMING, SUBMIT_READBACK = 0x1, 0x2, 0x4
 
 i64, i32, u32, u64, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p
 
@@ -87,6 +87,7 @@ _sig = {
     "helios_plan_outputs": (ctypes.c_int, [vp, i32, ctypes.POINTER(helios_blocks), ctypes.POINTER(vp),
                                            ctypes.POINTER(vp)]),
     "helios_plan_submit": (ctypes.c_int, [vp, i32, vp, i64, u64, u32, vp]),
+    "helios_plan_readback": (ctypes.c_int, [vp, i32, vp]),
     "helios_plan_wait": (ctypes.c_int, [vp, i32, vp]),
     "helios_plan_timing": (ctypes.c_int, [vp, i32, i32, ctypes.POINTER(helios_batch_timing)]),
     "helios_plan_mark": (ctypes.c_int, [vp, vp]),
@@ -408,7 +409,8 @@ def helios_plan_create(g: Graph, c: Cache | None, B: int, fanouts, depth: int = 
     return p
 
 
-def helios_plan_submit(p: Plan, slot: int, seeds, key: int, stream=None, timing: bool = False) -> None:
+def helios_plan_submit(p: Plan, slot: int, seeds, key: int, stream=None, timing: bool = False,
+                       readback: bool = False) -> None:
     if isinstance(seeds, torch.Tensor) and seeds.is_cuda:
         ptr, n, fl = seeds.data_ptr(), seeds.numel(), 0
     else:
@@ -416,8 +418,19 @@ def helios_plan_submit(p: Plan, slot: int, seeds, key: int, stream=None, timing:
         ptr, n, fl = _ptr(arr), len(arr), SUBMIT_SEEDS_HOST
     if timing:
         fl |= SUBMIT_TIMING
+    if readback:
+        fl |= SUBMIT_READBACK
     _check(_lib.helios_plan_submit(p.handle, slot, ptr, n, key & (2**64 - 1), fl, _stream(stream)),
            "helios_plan_submit")
+
+
+def helios_plan_readback(p: Plan, slot: int, out: np.ndarray | None = None) -> np.ndarray:
+    """Blocks for slot's last batch (submitted with readback=True): int64[L + 1 + 4] = level counts,
+    then rows_hbm_local, rows_hbm_peer, rows_host, rows_file."""
+    if out is None:
+        out = np.empty(len(p.fanouts) + 5, dtype=np.int64)
+    _check(_lib.helios_plan_readback(p.handle, slot, _ptr(out)), "helios_plan_readback")
+    return out
 
 
 def helios_plan_wait(p: Plan, slot: int, stream=None) -> None:

@@ -135,3 +135,29 @@ def test_staged_stress_many_batches(H):
     assert c.info().host_rows == S
     p.free()
     c.free()
+
+
+def test_plan_readback(H, c1):
+    """HELIOS_SUBMIT_READBACK / helios_plan_readback: the host copy equals the slot's device level
+    counts and tier stats (= the oracle's); E_STATE for a batch submitted without it."""
+    cfg = c1.cfg
+    Hr, S = workloads.tier_rows(cfg)
+    g, hot, c = build(H, c1, Hr, S)
+    dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S)
+    p = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=3)
+    keys = workloads.batch_keys(0, len(c1.batches))
+    for b in range(6):
+        k = b % 3
+        if b >= 3:
+            got = H.helios_plan_readback(p, k)
+            ob = oracle.sample(c1.graph.indptr, c1.graph.indices, c1.batches[b - 3], cfg.fanouts, keys[b - 3])
+            assert got[: len(cfg.fanouts) + 1].tolist() == ob.level_counts.tolist()
+            assert got[len(cfg.fanouts) + 1:].tolist() == oracle.lookup_counts(dref, ob.nodes).tolist()
+        H.helios_plan_submit(p, k, c1.batches[b], keys[b], readback=True)
+    H.helios_plan_submit(p, 0, c1.batches[0], keys[0])
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_plan_readback(p, 0)
+    assert e.value.name == "E_STATE"
+    H.helios_sync(c)
+    p.free()
+    c.free()
