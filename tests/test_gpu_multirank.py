@@ -72,7 +72,8 @@ def _worker(rank, world, port, tag, q):
         ok, peer_rows = True, 0
         for j, b in enumerate(mine):
             k = j % 2
-            H.helios_plan_submit(p, k, torch.as_tensor(inp.batches[b]).cuda(), keys[b])
+            sd = torch.as_tensor(inp.batches[b]).cuda()   # alive until the batch completes
+            H.helios_plan_submit(p, k, sd, keys[b])
             H.helios_plan_wait(p, k)
             H.helios_sync(c)
             blocks, feats, stats = p.outputs[k]

@@ -71,8 +71,10 @@ def test_plan_c1_epoch(H, c1, depth, flags, host_seeds, staged):
     nb = len(c1.batches)
     for start in range(0, nb, depth):
         idx = list(range(start, min(nb, start + depth)))
+        live = []   # device seeds must stay allocated until their batch completes (helios.h)
         for k, b in enumerate(idx):
             seeds = c1.batches[b] if host_seeds else torch.as_tensor(c1.batches[b]).cuda()
+            live.append(seeds)
             H.helios_plan_submit(p, k, seeds, keys[b], stream, timing=(b % 2 == 0))
         for k, b in enumerate(idx):
             H.helios_plan_wait(p, k, stream)
@@ -98,8 +100,9 @@ def test_plan_sample_only_medium(H):
     for it in range(3):
         seeds = [rng.choice(gr.V, 1024 - 100 * k, replace=False) for k in range(2)]
         keys = [it * 7 + 1, it * 7 + 2]
+        dev = [torch.as_tensor(x).cuda() for x in seeds]   # alive until the batches complete
         for k in range(2):
-            H.helios_plan_submit(p, k, torch.as_tensor(seeds[k]).cuda(), keys[k])
+            H.helios_plan_submit(p, k, dev[k], keys[k])
         torch.cuda.synchronize()
         for k in range(2):
             H.helios_plan_wait(p, k)
