@@ -195,17 +195,33 @@ def file_peak(path: str, stride: int, header: int, threads: int, secs: float = 3
 
 
 def sampling_accesses(batch: dict, indptr: np.ndarray, fanouts) -> dict:
-    """Minimum DRAM work of one batch's sampling + lookup at sector granularity:
-    per hop, one 32 B sector per frontier row for its indptr pair and at least ceil(4k/32) sectors for
-    the k sampled positions of its adjacency; one sector per node for its directory word.  Streaming
-    bytes: block CSR writes (4 per edge and per indptr entry) and the node list (8 per node)."""
+    """Minimum DRAM work of one batch's sampling + lookup at 32 B sector granularity.
+    Per hop and frontier row v (degree d, k = min(d, f) sampled positions): one sector for its indptr
+    pair, and the sectors of indices[indptr[v] : indptr[v] + d] that hold a sampled position -- all
+    S sectors of the row's span when k == d, else the expectation S * (1 - C(d - 8, k) / C(d, k)) for k
+    positions drawn uniformly without replacement (8 positions per sector); one sector per node for its
+    directory word.  Streaming bytes: block CSR writes (4 per edge and per indptr entry) and the node
+    list (8 per node)."""
     nodes, lc = batch["nodes"], batch["level_counts"]
-    sectors = stream = 0
+    sectors = stream = 0.0
     for h, f in enumerate(fanouts):
         nh = nodes[: lc[h]]
-        d = indptr[nh + 1] - indptr[nh]
+        base = indptr[nh]
+        d = indptr[nh + 1] - base
         k = d if f < 0 else np.minimum(d, f)
-        sectors += len(nh) + int(((4 * k + 31) // 32).sum())
+        span = np.where(d > 0, (base + d - 1) // 8 - base // 8 + 1, 0)
+        # P(no sampled position among m given positions) = C(d - m, k) / C(d, k), m = 0..8
+        p_none = np.ones((9, len(nh)))
+        for i in range(8):
+            p_none[i + 1] = p_none[i] * np.clip((d - k - i) / np.maximum(d - i, 1), 0.0, 1.0)
+        cols = np.arange(len(nh))
+        m_first = np.minimum(d, 8 - base % 8)
+        m_last = np.where(span > 1, base + d - 8 * ((base + d - 1) // 8), 0)
+        interior = np.maximum(span - 2, 0)
+        touched = ((1.0 - p_none[m_first, cols]) + np.where(span > 1, 1.0 - p_none[m_last, cols], 0.0)
+                   + interior * (1.0 - p_none[8]))
+        touched = np.where(k == d, span, np.where(k > 0, touched, 0.0))
+        sectors += len(nh) + float(touched.sum())
         stream += 4 * int(k.sum()) + 4 * (len(nh) + 1)
     n_l = int(lc[len(fanouts)])
     sectors += n_l
@@ -620,9 +636,10 @@ def main():
                               "sector_rate_G_s": round(sec_rate, 2), "t_roof_ms": round(t_e2e, 4),
                               "frac": round(t_e2e / (max_ms / steps), 4),
                               "note": "whole step vs stream/BW_hbm + sectors/sector_rate + tier-link terms; sectors = "
-                                      "per hop one per frontier row (indptr) + ceil(4k/32) per row (sampled positions) + "
-                                      "one per node (directory), averaged over the first 16 timed batches; sector_rate = "
-                                      "helios_graph_probe_random (uniform 4 B loads over the CSR indices)"}
+                                      "per hop one per frontier row (indptr) + the expected distinct sectors holding its k "
+                                      "sampled positions + one per node (directory), averaged over the first 16 timed "
+                                      "batches (bench.sampling_accesses); sector_rate = helios_graph_probe_random "
+                                      "(uniform 4 B loads over the CSR indices)"}
     if probe is not None and n_host > 0:
         got = n_host * (world * steps / (max_ms / 1e3)) / world / 1e6
         roof["host_link"] = {"achieved_Mrows_s": round(got, 2), "random_row_ceiling": probe,

@@ -64,3 +64,27 @@ def test_interval_union():
             iv.append((a, a + rng.randint(0, 10)))
         covered = sum(1 for t in range(60) if any(a <= t < b for a, b in iv))
         assert bench.interval_union(iv) == covered
+
+
+def test_sampling_sector_count():
+    """bench.sampling_accesses: exact on full rows; the k < d expectation matches a Monte-Carlo draw."""
+    sys.path.insert(0, ROOT)
+    import numpy as np
+
+    import bench
+    # one hop, rows: v0 d=3 (k=d, one sector), v1 d=20 starting at 3 (k=d: sectors 0..2), v2 d=400, f=5
+    indptr = np.array([0, 3, 23, 423], dtype=np.int64)
+    batch = {"nodes": np.array([0, 1, 2]), "level_counts": np.array([3, 3])}
+    got = bench.sampling_accesses(batch, indptr, [5])
+    # v0: k=3=d -> span 1; v1: k=5<d=20 -> expectation; v2: k=5<400 -> expectation
+    rng = np.random.default_rng(0)
+    mc = 0.0
+    for base, d in ((3, 20), (23, 400)):
+        t = 0
+        for _ in range(4000):
+            pos = base + rng.choice(d, 5, replace=False)
+            t += len(np.unique(pos // 8))
+        mc += t / 4000
+    expect_sectors = 3 + 1 + mc + 3          # indptr per row + v0's sector + sampled + directory
+    assert abs(got["sectors"] - expect_sectors) < 0.25
+    assert got["stream_bytes"] == 4 * (3 + 5 + 5) + 4 * 4 + 8 * 3
