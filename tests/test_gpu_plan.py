@@ -164,3 +164,34 @@ def test_plan_readback(H, c1):
     H.helios_sync(c)
     p.free()
     c.free()
+
+
+def test_plan_timing_marked(H, c1):
+    """helios_plan_mark + HELIOS_SUBMIT_TIMING: per-batch offsets are ordered (start <= end of sampling
+    <= end) and consistent with the durations; batches of different slots share the origin."""
+    cfg = c1.cfg
+    Hr, S = workloads.tier_rows(cfg)
+    g, hot, c = build(H, c1, Hr, S)
+    p = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=2)
+    keys = workloads.batch_keys(0, len(c1.batches))
+    stream = torch.cuda.current_stream()
+    H.helios_plan_mark(p, stream)
+    for b in range(4):
+        H.helios_plan_submit(p, b % 2, c1.batches[b], keys[b], stream, timing=True)
+    for k in range(2):
+        H.helios_plan_wait(p, k, stream)
+    H.helios_sync(c)
+    ends = []
+    for k in range(2):
+        for back in range(2):
+            t = H.helios_plan_timing(p, k, back)
+            assert 0 <= t.t_start <= t.t_gather <= t.t_end
+            assert abs((t.t_gather - t.t_start) - t.sample_ms) < 1e-2
+            assert abs((t.t_end - t.t_gather) - t.gather_ms) < 1e-2
+            ends.append(t.t_end)
+    assert max(ends) < 10_000
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_plan_timing(p, 0, 2)
+    assert e.value.name == "E_RANGE"
+    p.free()
+    c.free()
