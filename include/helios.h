@@ -264,6 +264,8 @@ helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64
                                            side stream while the next hop samples; timed submits then
                                            report the whole batch as the sampling phase */
 #define HELIOS_PLAN_LINK_STREAM 0x8u    /* ablation: host-tier rows of every batch on a shared link stream */
+#define HELIOS_PLAN_TRACE 0x10u         /* per-kernel device timeline of every batch (helios_plan_trace);
+                                           only in the traced build libhelios_trace.so, else E_INVALID */
 #define HELIOS_SUBMIT_SEEDS_HOST 0x1u  /* seeds pointer is host memory (copied with the parameters, H2D) */
 #define HELIOS_SUBMIT_TIMING 0x2u      /* record device timing events around the sample / gather phases */
 #define HELIOS_SUBMIT_READBACK 0x4u    /* copy the batch's level counts and tier stats to plan-owned pinned
@@ -313,6 +315,15 @@ typedef struct {
   float t_start, t_gather, t_end;
 } helios_batch_timing;
 helios_status helios_plan_timing(helios_plan* p, int32_t slot, int32_t back, helios_batch_timing* out);
+/* Device timeline of a batch of a plan created with HELIOS_PLAN_TRACE (tracing subsystem; nsys-free):
+ * back = 0 is the slot's last batch, back = k the k-th before it (k < 256).  Blocks until the slot's
+ * last batch is done.  out[2k], out[2k+1] = %globaltimer ns of the earliest warp start (after its
+ * programmatic-dependency wait) and the latest warp end of kernel position k, 0 if it did not run:
+ * k = 3h + {0, 1, 2} = count scan / fill / dedup-assign of hop h, 3L relabel, 3L+1 table clear,
+ * 3L+2 lookup (K3), 3L+3 gather (K4).  *n_kernels = 3L + 4; E_CAPACITY if cap < 2 * (3L + 4),
+ * E_STATE without HELIOS_PLAN_TRACE, E_RANGE if the batch is not in the ring. */
+helios_status helios_plan_trace(helios_plan* p, int32_t slot, int32_t back, uint64_t* out, int32_t cap,
+                                int32_t* n_kernels);
 /* Records the plan's reference event on `stream` (the origin of helios_batch_timing's t_* values). */
 helios_status helios_plan_mark(helios_plan* p, void* stream);
 

@@ -9,6 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libhelios.so")
+SO_TRACE = os.path.join(HERE, "libhelios_trace.so")  # -DHELIOS_TRACE: device pipeline timeline (tools)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -21,15 +22,24 @@ def deps() -> list[str]:
     return sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(HERE, "..", "include", "helios.h")]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(SO) and all(os.path.getmtime(SO) >= os.path.getmtime(d) for d in deps()):
-        return SO
+def _build_one(so: str, defines: list[str], force: bool, verbose: bool) -> str:
+    if not force and os.path.exists(so) and all(os.path.getmtime(so) >= os.path.getmtime(d) for d in deps()):
+        return so
     cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-shared", "-Xcompiler", "-fPIC", "-cudart", "static",
-           "-Xcompiler", "-pthread", "--expt-relaxed-constexpr", "-o", SO, *sources()]
+           "-Xcompiler", "-pthread", "--expt-relaxed-constexpr", *defines, "-o", so, *sources()]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
+    return so
+
+
+def build(force: bool = False, verbose: bool = False, trace: bool = True) -> str:
+    """libhelios.so (the product) and, unless trace=False, libhelios_trace.so (same sources with the
+    device pipeline tracer compiled in)."""
+    _build_one(SO, [], force, verbose)
+    if trace:
+        _build_one(SO_TRACE, ["-DHELIOS_TRACE"], force, verbose)
     return SO
 
 

@@ -39,6 +39,7 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
 helios_status plan_wait_impl(helios_plan* p, int32_t slot, cudaStream_t st);
 helios_status plan_timing_impl(helios_plan* p, int32_t slot, int32_t back, helios_batch_timing* out);
 helios_status plan_mark_impl(helios_plan* p, cudaStream_t st);
+helios_status plan_trace_impl(helios_plan* p, int32_t slot, int32_t back, uint64_t* out, int32_t cap, int32_t* n_out);
 helios_status plan_readback_impl(helios_plan* p, int32_t slot, int64_t* out);
 helios_status plan_outputs_impl(helios_plan* p, int32_t slot, helios_blocks* blocks, void** features,
                                 helios_gather_stats** stats);
@@ -430,6 +431,13 @@ helios_status helios_plan_create(helios_graph* g, helios_cache* c, const helios_
   p->graphs = !(d->flags & HELIOS_PLAN_NO_GRAPH);
   p->serial_gather = (d->flags & HELIOS_PLAN_SERIAL_GATHER) != 0;
   p->intra = (d->flags & HELIOS_PLAN_INTRA_BATCH) != 0;
+  p->trace = (d->flags & HELIOS_PLAN_TRACE) != 0;
+#ifndef HELIOS_TRACE
+  if (p->trace) {
+    delete p;
+    return fail(HELIOS_E_INVALID, "HELIOS_PLAN_TRACE needs the traced build (libhelios_trace.so, HELIOS_LIB=trace)");
+  }
+#endif
   p->link = c && c->S > 0 && !p->intra && !p->serial_gather && (d->flags & HELIOS_PLAN_LINK_STREAM);
   HCHECK(!p->intra || p->graphs, HELIOS_E_INVALID, "HELIOS_PLAN_INTRA_BATCH needs CUDA graphs");
   helios_status st = plan_create_impl(p);
@@ -490,6 +498,15 @@ helios_status helios_plan_readback(helios_plan* p, int32_t slot, int64_t* out) {
   HCHECK(p, HELIOS_E_INVALID, "null plan");
   DeviceGuard dg(p->g->device);
   return plan_readback_impl(p, slot, out);
+  GUARD_END
+}
+
+helios_status helios_plan_trace(helios_plan* p, int32_t slot, int32_t back, uint64_t* out, int32_t cap,
+                                int32_t* n_kernels) {
+  GUARD_BEGIN
+  HCHECK(p, HELIOS_E_INVALID, "null plan");
+  DeviceGuard dg(p->g->device);
+  return plan_trace_impl(p, slot, back, out, cap, n_kernels);
   GUARD_END
 }
 

@@ -46,6 +46,35 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+// Pipeline trace (HELIOS_PLAN_TRACE): params[3] of a batch points at its row of TraceRec, one per
+// kernel position (3h + {0,1,2} = count scan / fill / assign of hop h, 3L relabel, 3L+1 table clear,
+// 3L+2 lookup, 3L+3 gather).  The row is preset to all-ones; every warp records, after its PDL wait,
+// the earliest start (atomicMin) and, when it leaves the kernel, the latest end (atomicMin of ~t).
+struct TraceRec {
+  unsigned long long start, end_inv;
+};
+#ifdef HELIOS_TRACE
+struct TraceScope {
+  TraceRec* r = nullptr;
+  __device__ __forceinline__ TraceScope(const int64_t* params, int idx) {
+    TraceRec* row = params ? reinterpret_cast<TraceRec*>(params[3]) : nullptr;
+    if (row) {
+      r = row + idx;
+      if ((threadIdx.x & 31) == 0) atomicMin(&r->start, (unsigned long long)globaltimer());
+    }
+  }
+  __device__ __forceinline__ ~TraceScope() {
+    if (r && (threadIdx.x & 31) == 0) atomicMin(&r->end_inv, ~(unsigned long long)globaltimer());
+  }
+};
+#else
+// Default build: no tracing code in the kernels (even a disabled scope cost C2 13 %); the traced
+// build is libhelios_trace.so (-DHELIOS_TRACE), loaded with HELIOS_LIB=trace.
+struct TraceScope {
+  __device__ __forceinline__ TraceScope(const int64_t*, int) {}
+};
+#endif
+
 __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));

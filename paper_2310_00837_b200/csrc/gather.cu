@@ -38,8 +38,10 @@ struct ListPtrs {
 __global__ void __launch_bounds__(256) k_lookup(const int64_t* __restrict__ nodes, const int64_t* __restrict__ lo_ptr,
                                                 const int64_t* __restrict__ n_nodes,
                                                 const int64_t* __restrict__ dir, int32_t rank, ListPtrs L,
-                                                unsigned long long* ctl) {
+                                                unsigned long long* ctl, const int64_t* trace_params, int trace_idx) {
+  pdl_wait();  // N_L is final once the sampling chain's last kernel has completed
   pdl_trigger();
+  TraceScope ts(trace_params, trace_idx);
   const int lane = threadIdx.x & 31;
   const int64_t lo = lo_ptr ? *lo_ptr : 0;
   const int64_t n = *n_nodes - lo;
@@ -111,6 +113,8 @@ struct GatherArgs {
   char* const* peers;       // device [G]
   const char* host_dev;     // device alias of the host tier
   helios_gather_stats* stats;
+  const int64_t* trace_params;  // HELIOS_PLAN_TRACE (nullptr: off)
+  int trace_idx;
 };
 
 // Copies rows [j0, j0+U) of list q (warp-cooperative, VPL 16 B vectors per lane per row, all loads
@@ -229,6 +233,7 @@ template <int VPL, int U, int UH>
 __global__ void __launch_bounds__(256, 4) k_gather_lists(GatherArgs a) {
   pdl_wait();
   pdl_trigger();
+  TraceScope ts(a.part == kPartHost ? nullptr : a.trace_params, a.trace_idx);
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -589,6 +594,8 @@ static GatherArgs make_args(helios_cache* c, GatherWS& w, void* out, helios_gath
   a.peers = c->d_peers;
   a.host_dev = c->d_host_tier;
   a.stats = stats;
+  a.trace_params = w.trace_params;
+  a.trace_idx = w.trace_idx + 1;
   return a;
 }
 
@@ -600,14 +607,15 @@ static helios_status gather_pass(helios_cache* c, GatherWS& w, const int64_t* no
                                  bool first, bool accumulate, int part, cudaStream_t st) {
   HCHECK(!c->broken, HELIOS_E_STATE, "cache unusable after an IO / staging watchdog timeout");
   if (first) {
-    HCUDA(cudaMemsetAsync(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long), st));
+    if (!w.ctl_preset) HCUDA(cudaMemsetAsync(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long), st));
   } else {
     HCUDA(cudaMemsetAsync(w.d_ctl, 0, kListFile * sizeof(unsigned long long), st));
     HCUDA(cudaMemsetAsync(w.d_ctl + kCtlHostTicket, 0, 2 * sizeof(unsigned long long), st));
   }
   GatherArgs a = make_args(c, w, out, stats, accumulate, part);
   const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_rows + 255) / 256), (int64_t)c->sms * 2);
-  k_lookup<<<lg, 256, 0, st>>>(nodes, lo, n_nodes, c->dir, c->rank, a.L, w.d_ctl);
+  launch_pdl(k_lookup, dim3(lg), dim3(256), st, nodes, lo, n_nodes, (const int64_t*)c->dir, c->rank, a.L, w.d_ctl,
+             w.trace_params, w.trace_idx);
   if (a.staged) launch_pdl(k_stage_publish, dim3(1), dim3(1), st, w.d_ctl, w.d_seq, w.d_mail, c->stage_frac, kStageCapRows);
   launch_gather_any(a, c->sms, st);
   HCUDA(cudaGetLastError());

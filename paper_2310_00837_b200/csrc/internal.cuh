@@ -148,6 +148,9 @@ struct GatherWS {
   uint32_t* h_mail = nullptr;           // pinned {seq, n_host, n_gpu, n_stage}, published by the GPU
   uint32_t* d_mail = nullptr;
   uint32_t* d_seq = nullptr;            // device batch counter of this context
+  bool ctl_preset = false;              // the plan zeroes d_ctl at the batch start (off the K2 -> K3 edge)
+  const int64_t* trace_params = nullptr;  // HELIOS_PLAN_TRACE: the slot's parameter block (params[3] = trace row)
+  int trace_idx = 0;                    // kernel position of K3 in the trace row (K4: +1)
   StageCtx* sctx = nullptr;
 };
 
@@ -274,6 +277,8 @@ struct PlanSlot {
                                   // {host start, host end} on the link stream
   std::vector<cudaEvent_t> ring;  // kRing x kEv timing events (timed submits only)
   int64_t* h_rb = nullptr;        // pinned readback {level_counts[L+1], stats[4]} (HELIOS_SUBMIT_READBACK)
+  static constexpr int kTraceRing = 256;
+  void* d_trace = nullptr;        // HELIOS_PLAN_TRACE: kTraceRing rows of (3L+4) TraceRec
   bool rb_valid = false;          // the last submit requested a readback
   int64_t count = 0;              // batches submitted to this slot
   int64_t tcount = 0;             // timed batches submitted to this slot
@@ -294,6 +299,7 @@ struct helios_plan {
   // copied by one k_gather_lists<kPartHost> launch on a high-priority stream shared by all slots, so
   // the PCIe link serves one batch at a time; HBM rows stay on the slot stream.  Measured slower
   // than letting each slot's gather kernel read its own host rows.
+  bool trace = false;  // HELIOS_PLAN_TRACE
   bool link = false;
   static constexpr int kMaxLinks = 4;
   int n_links = 1;                    // link streams used round-robin (HELIOS_PLAN_LINKS, 1..4)
@@ -318,7 +324,7 @@ void ws_free(SampleWS& w);
 // Uploads (key, n_seeds, seeds) into w.d_params on `st` with ONE copy (not capturable; done before
 // a graph replay).  seeds_host: copy the seeds inline (host memory), else pass the device pointer.
 helios_status ws_upload_params(SampleWS& w, uint64_t key, int64_t B, const int64_t* seeds, bool seeds_host,
-                               cudaStream_t st);
+                               cudaStream_t st, void* trace_row = nullptr);
 // Enqueues the sampling kernels; they read key / n_seeds / seeds from w.d_params.  B_max sizes the grids.
 // stage_hook (optional, multi-kernel path): called after the stream position where N_0 (stage 0) or
 // N_{h+1} (stage h+1) is final, to fork per-range work (the intra-batch pipeline).

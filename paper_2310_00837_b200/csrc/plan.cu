@@ -23,6 +23,7 @@ void plan_free_impl(helios_plan* p) {
     gws_free(s.gws);
     if (s.mem) cudaFree(s.mem);
     if (s.h_rb) cudaFreeHost(s.h_rb);
+    if (s.d_trace) cudaFree(s.d_trace);
     if (s.feats) cudaFree(s.feats);
     if (s.g_sample) cudaGraphExecDestroy(s.g_sample);
     if (s.g_gather) cudaGraphExecDestroy(s.g_gather);
@@ -111,11 +112,19 @@ helios_status plan_create_impl(helios_plan* p) {
       HCUDA(cudaMemset(sl.stats, 0, sizeof(helios_gather_stats)));
       s = gws_ensure(p->c, sl.gws, sl.blocks.nodes_cap);
       if (s != HELIOS_OK) return s;
+      sl.gws.ctl_preset = !p->intra;
     }
     s = ws_ensure(g, sl.ws, d.max_seeds, d.fanouts, d.L);
     if (s != HELIOS_OK) return s;
     HCUDA(cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking));
     HCUDA(cudaHostAlloc(&sl.h_rb, (HELIOS_MAX_HOPS + 1 + 4) * sizeof(int64_t), cudaHostAllocDefault));
+    if (p->trace) {
+      const size_t row = (size_t)(3 * d.L + 4) * 16;
+      HCUDA(cudaMalloc(&sl.d_trace, PlanSlot::kTraceRing * row));
+      HCUDA(cudaMemset(sl.d_trace, 0xFF, PlanSlot::kTraceRing * row));
+      sl.gws.trace_params = sl.ws.d_params;  // before capture: the gather kernels take it by value
+      sl.gws.trace_idx = 3 * d.L + 2;
+    }
     HCUDA(cudaEventCreateWithFlags(&sl.ev_caller, cudaEventDisableTiming));
     HCUDA(cudaEventCreateWithFlags(&sl.ev_end, cudaEventDisableTiming));
     sl.ring.assign(PlanSlot::kEv * PlanSlot::kRing, nullptr);
@@ -125,7 +134,11 @@ helios_status plan_create_impl(helios_plan* p) {
       HCUDA(cudaEventCreateWithFlags(&sl.ev_host, cudaEventDisableTiming));
     }
     if (p->graphs) {
-      auto sample_ops = [&]() { return sample_launch(g, sl.ws, d.max_seeds, d.fanouts, d.L, &sl.blocks, sl.stream); };
+      auto sample_ops = [&]() -> helios_status {
+        // the gather's control words are zeroed at the batch start, off the sampling -> lookup edge
+        if (sl.gws.ctl_preset) HCUDA(cudaMemsetAsync(sl.gws.d_ctl, 0, kCtlWords * sizeof(unsigned long long), sl.stream));
+        return sample_launch(g, sl.ws, d.max_seeds, d.fanouts, d.L, &sl.blocks, sl.stream);
+      };
       auto gather_ops = [&]() {  // link mode: lookup + HBM rows only (host rows: link stream)
         return (p->link ? gather_hbm_launch : gather_launch)(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + d.L,
                                                              sl.blocks.nodes_cap, sl.feats, sl.stats, sl.stream);
@@ -178,7 +191,14 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
   PlanSlot& sl = p->slots[slot];
   HCUDA(cudaEventRecord(sl.ev_caller, caller));
   HCUDA(cudaStreamWaitEvent(sl.stream, sl.ev_caller, 0));
-  helios_status s = ws_upload_params(sl.ws, key, n, seeds, (flags & HELIOS_SUBMIT_SEEDS_HOST) != 0, sl.stream);
+  void* trace_row = nullptr;
+  if (p->trace) {
+    const size_t row = (size_t)(3 * p->d.L + 4) * 16;
+    trace_row = (char*)sl.d_trace + (sl.count % PlanSlot::kTraceRing) * row;
+    HCUDA(cudaMemsetAsync(trace_row, 0xFF, row, sl.stream));
+  }
+  helios_status s = ws_upload_params(sl.ws, key, n, seeds, (flags & HELIOS_SUBMIT_SEEDS_HOST) != 0, sl.stream,
+                                     trace_row);
   if (s != HELIOS_OK) return s;
   const bool timed = (flags & HELIOS_SUBMIT_TIMING) != 0;
   cudaEvent_t* ev = &sl.ring[PlanSlot::kEv * (sl.tcount % PlanSlot::kRing)];
@@ -193,6 +213,7 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
     if (p->graphs) {
       HCUDA(cudaGraphLaunch(sl.g_sample, sl.stream));
     } else {
+      if (sl.gws.ctl_preset) HCUDA(cudaMemsetAsync(sl.gws.d_ctl, 0, kCtlWords * sizeof(unsigned long long), sl.stream));
       s = sample_launch(p->g, sl.ws, p->d.max_seeds, p->d.fanouts, p->d.L, &sl.blocks, sl.stream);
       if (s != HELIOS_OK) return s;
     }
@@ -281,6 +302,28 @@ helios_status plan_timing_impl(helios_plan* p, int32_t slot, int32_t back, helio
     HCUDA(cudaEventElapsedTime(&t.t_end, p->ev_ref, ev[2]));
   }
   *out = t;
+  return HELIOS_OK;
+}
+
+helios_status plan_trace_impl(helios_plan* p, int32_t slot, int32_t back, uint64_t* out, int32_t cap,
+                              int32_t* n_out) {
+  HCHECK(slot >= 0 && slot < (int32_t)p->slots.size(), HELIOS_E_INVALID, "slot %d of %zu", slot, p->slots.size());
+  HCHECK(p->trace, HELIOS_E_STATE, "plan created without HELIOS_PLAN_TRACE");
+  PlanSlot& sl = p->slots[slot];
+  HCHECK(back >= 0 && back < PlanSlot::kTraceRing && back < sl.count, HELIOS_E_RANGE, "slot %d: batch -%d not traced",
+         slot, back);
+  const int K = 3 * p->d.L + 4;
+  HCHECK(out && cap >= 2 * K, HELIOS_E_CAPACITY, "trace output needs %d words", 2 * K);
+  HCUDA(cudaEventSynchronize(sl.ev_end));
+  std::vector<uint64_t> row(2 * K);
+  HCUDA(cudaMemcpy(row.data(), (char*)sl.d_trace + ((sl.count - 1 - back) % PlanSlot::kTraceRing) * (size_t)K * 16,
+                   (size_t)K * 16, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < K; k++) {
+    const bool ran = row[2 * k] != ~0ull;
+    out[2 * k] = ran ? row[2 * k] : 0;
+    out[2 * k + 1] = ran ? ~row[2 * k + 1] : 0;
+  }
+  if (n_out) *n_out = K;
   return HELIOS_OK;
 }
 

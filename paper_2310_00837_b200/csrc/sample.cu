@@ -302,27 +302,32 @@ __device__ __forceinline__ void dev_insert_seeds(const SampleCtx& c) {  // L = 0
 __global__ void __launch_bounds__(kScanBlock) k_count_scan(SampleCtx c, int h) {
   if (h > 0) pdl_wait();
   pdl_trigger();
+  TraceScope ts(c.params, 3 * h);
   dev_count_scan(c, h);
 }
 template <int G>
 __global__ void __launch_bounds__(256) k_fill_insert(SampleCtx c, int h) {
   pdl_wait();
   pdl_trigger();
+  TraceScope ts(c.params, 3 * h + 1);
   dev_fill_insert<G>(c, h);
 }
 __global__ void __launch_bounds__(kScanBlock) k_dedup_assign(SampleCtx c, int h) {
   pdl_wait();
   pdl_trigger();
+  TraceScope ts(c.params, 3 * h + 2);
   dev_assign(c, h);
 }
 __global__ void __launch_bounds__(256) k_relabel(SampleCtx c, int h) {
   pdl_wait();
   pdl_trigger();
+  TraceScope ts(c.params, 3 * c.L);
   dev_relabel(c, h);
 }
 __global__ void __launch_bounds__(256) k_table_clear(SampleCtx c) {
   pdl_wait();
   pdl_trigger();
+  TraceScope ts(c.params, 3 * c.L + 1);
   dev_table_clear(c);
 }
 __global__ void __launch_bounds__(256) k_insert_seeds(SampleCtx c) { dev_insert_seeds(c); }
@@ -563,12 +568,13 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
 }
 
 helios_status ws_upload_params(SampleWS& w, uint64_t key, int64_t B, const int64_t* seeds, bool seeds_host,
-                               cudaStream_t st) {
+                               cudaStream_t st, void* trace_row) {
   HCHECK(B <= w.cap_seeds, HELIOS_E_CAPACITY, "n_seeds %lld > workspace capacity %lld", (long long)B,
          (long long)w.cap_seeds);
   HCUDA(cudaEventSynchronize(w.params_ev));  // the previous upload has been consumed
   w.h_params[0] = (int64_t)key;
   w.h_params[1] = B;
+  w.h_params[3] = (int64_t)(uintptr_t)trace_row;  // HELIOS_PLAN_TRACE row of this batch, or 0
   size_t bytes = 4 * sizeof(int64_t);
   if (seeds_host) {
     if (B > 0) memcpy(w.h_params + 4, seeds, B * sizeof(int64_t));

@@ -15,7 +15,8 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libhelios.so")
+# HELIOS_LIB=trace loads the traced build (device pipeline timeline, tools/trace_pipeline.py)
+SO_PATH = os.path.join(_HERE, "libhelios_trace.so" if os.environ.get("HELIOS_LIB") == "trace" else "libhelios.so")
 if not os.path.exists(SO_PATH):
     raise ImportError(f"{SO_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
                       "(nvcc, sm_100a). There is no CPU fallback.")
@@ -26,7 +27,7 @@ MAX_RANKS = 64
 STATUS = ["OK", "E_INVALID", "E_RANGE", "E_CAPACITY", "E_NOMEM", "E_CUDA", "E_IO", "E_TIMEOUT", "E_STATE"]
 HOST_ALIAS, TABLE_MAPPED, NO_DIRECT_IO, IO_FAULT_AT = 0x1, 0x2, 0x4, 0x100
 HOST_FILL, HOST_TIER_MAPPED, HOST_STAGED, IO_SYNC = 0x8, 0x10, 0x20, 0x40
-PLAN_NO_GRAPH, PLAN_SERIAL_GATHER, PLAN_INTRA_BATCH, PLAN_LINK_STREAM = 0x1, 0x2, 0x4, 0x8
+PLAN_NO_GRAPH, PLAN_SERIAL_GATHER, PLAN_INTRA_BATCH, PLAN_LINK_STREAM, PLAN_TRACE = 0x1, 0x2, 0x4, 0x8, 0x10
 SUBMIT_SEEDS_HOST, SUBMIT_TIMING, SUBMIT_READBACK = 0x1, 0x2, 0x4
 
 i64, i32, u32, u64, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p
@@ -91,6 +92,7 @@ _sig = {
     "helios_plan_wait": (ctypes.c_int, [vp, i32, vp]),
     "helios_plan_timing": (ctypes.c_int, [vp, i32, i32, ctypes.POINTER(helios_batch_timing)]),
     "helios_plan_mark": (ctypes.c_int, [vp, vp]),
+    "helios_plan_trace": (ctypes.c_int, [vp, i32, i32, vp, i32, ctypes.POINTER(i32)]),
 }
 for _n, (_r, _a) in _sig.items():
     _f = getattr(_lib, _n)
@@ -444,6 +446,17 @@ def helios_plan_timing(p: Plan, slot: int, back: int = 0) -> helios_batch_timing
     t = helios_batch_timing()
     _check(_lib.helios_plan_timing(p.handle, slot, back, ctypes.byref(t)), "helios_plan_timing")
     return t
+
+
+def helios_plan_trace(p: Plan, slot: int, back: int = 0) -> np.ndarray:
+    """Per-kernel device timeline (ns, %globaltimer) of a traced batch: uint64[3L + 4, 2] of
+    (first warp start, last warp end); rows 3h..3h+2 = count scan / fill / assign of hop h, then
+    relabel, table clear, lookup, gather (0 = did not run).  Plan created with PLAN_TRACE."""
+    K = 3 * len(p.fanouts) + 4
+    out = np.zeros(2 * K, dtype=np.uint64)
+    n = i32()
+    _check(_lib.helios_plan_trace(p.handle, slot, back, _ptr(out), 2 * K, ctypes.byref(n)), "helios_plan_trace")
+    return out.reshape(K, 2)
 
 
 def helios_plan_mark(p: Plan, stream=None) -> None:

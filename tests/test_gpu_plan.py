@@ -195,3 +195,67 @@ def test_plan_timing_marked(H, c1):
     assert e.value.name == "E_RANGE"
     p.free()
     c.free()
+
+
+TRACE_CHECK = r"""
+import os, sys
+import numpy as np, torch
+sys.path.insert(0, os.getcwd())
+import oracle, workloads
+from paper_2310_00837_b200 import helios as H
+assert H.SO_PATH.endswith("libhelios_trace.so")
+c1 = workloads.make_inputs(workloads.CONFIGS["C1"], table=True)
+cfg = c1.cfg
+Hr, _ = workloads.tier_rows(cfg)
+S = cfg.V - Hr   # HBM + host tiers only (no feature file in this check)
+g = H.helios_graph_load(c1.graph.indptr, c1.graph.indices)
+hot = torch.zeros(cfg.V, dtype=torch.int64, device="cuda")
+H.helios_presample(g, torch.as_tensor(np.concatenate(c1.batches)).cuda(), cfg.B, cfg.fanouts,
+                   workloads.presample_keys(len(c1.batches)), hot)
+c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=c1.table, flags=H.HOST_ALIAS)
+p = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=3, flags=H.PLAN_TRACE)
+keys = workloads.batch_keys(0, len(c1.batches))
+for b in range(6):
+    H.helios_plan_submit(p, b % 3, c1.batches[b], keys[b])
+    if b % 3 == 2:
+        for k in range(3):
+            H.helios_plan_wait(p, k)
+        H.helios_sync(c)
+        for k in range(3):
+            ob = oracle.sample(c1.graph.indptr, c1.graph.indices, c1.batches[b - 2 + k], cfg.fanouts, keys[b - 2 + k])
+            blocks, feats, _ = p.outputs[k]
+            assert np.array_equal(blocks.to_host()["nodes"], ob.nodes)
+            assert np.array_equal(feats[: len(ob.nodes)].cpu().numpy(), oracle.gather(ob.nodes, cfg.R, table=c1.table))
+for k in range(3):
+    for back in range(2):
+        t = H.helios_plan_trace(p, k, back).astype(np.int64)
+        assert t.shape == (3 * len(cfg.fanouts) + 4, 2)
+        assert (t[:, 0] > 0).all() and (t[:, 1] >= t[:, 0]).all()
+        assert (t[1:, 0] >= t[:-1, 1] - 2000).all()   # each kernel starts after its predecessor ended (ns)
+try:
+    H.helios_plan_trace(p, 0, 2)
+    raise SystemExit("expected E_RANGE")
+except H.HeliosError as e:
+    assert e.name == "E_RANGE"
+print("trace ok")
+"""
+
+
+def test_plan_trace(H, c1):
+    """HELIOS_PLAN_TRACE: E_INVALID in the product build; in the traced build (HELIOS_LIB=trace, run
+    in a subprocess) outputs stay bit-exact, every kernel position of a batch ran, and each kernel of
+    the chain starts after its predecessor ended (programmatic-dependency wait / stream order)."""
+    import os
+    import subprocess
+    import sys
+    cfg = c1.cfg
+    Hr, S = workloads.tier_rows(cfg)
+    g, hot, c = build(H, c1, Hr, S, flags=H.HOST_ALIAS)
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=1, flags=H.PLAN_TRACE)
+    assert e.value.name == "E_INVALID"
+    c.free()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", TRACE_CHECK], cwd=root, env={**os.environ, "HELIOS_LIB": "trace"},
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "trace ok" in out.stdout, out.stderr[-3000:]
