@@ -26,6 +26,10 @@ import time
 
 import numpy as np
 
+# More hardware work queues than the default 8, so the plan's slot streams (12 in flight) and the IO /
+# link streams do not alias onto shared queues (C2 +6 % at depth 12); read at CUDA context creation.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -281,7 +285,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--parity-batches", type=int, default=2)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no baseline, no parity")
-    ap.add_argument("--depth", type=int, default=8, help="batches in flight (plan slots)")
+    ap.add_argument("--depth", type=int, default=12, help="batches in flight (plan slots)")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly instead of CUDA graphs")
     ap.add_argument("--serial-gather", type=int, default=0, help="1: gathers of successive batches run one at a time")
     ap.add_argument("--intra", action="store_true", help="intra-batch pipeline: per-hop gather passes (NEXT-1)")

@@ -12,7 +12,10 @@ import os
 from dataclasses import dataclass
 
 import numpy as np
-import torch
+# Plans run one stream per in-flight batch: ask for 32 hardware work queues (default 8) unless the
+# caller chose otherwise; effective only if CUDA is not initialised yet in this process.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+import torch  # noqa: E402
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # HELIOS_LIB=trace loads the traced build (device pipeline timeline, tools/trace_pipeline.py)
