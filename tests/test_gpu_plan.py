@@ -256,6 +256,8 @@ def test_plan_trace(H, c1):
     assert e.value.name == "E_INVALID"
     c.free()
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    from paper_2310_00837_b200 import build as hb
+    hb.build()   # both libraries; a no-op when they are up to date
     out = subprocess.run([sys.executable, "-c", TRACE_CHECK], cwd=root, env={**os.environ, "HELIOS_LIB": "trace"},
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "trace ok" in out.stdout, out.stderr[-3000:]
