@@ -34,13 +34,59 @@ def test_philox_kat(ctr, key, expect):
 
 
 def test_philox_u32_counter_layout():
-    # word j&3 of the block whose counter is {j>>2, h, lo32(v), hi32(v)}: checked on the KAT block
-    # (ctr = 0, key = 0 -> 6627e8d5 e169c58d bc57ac4c 9b00dbd8), i.e. key 0, hop 0, vertex 0, j = 0..3
-    expect = _kat()[0][2]
-    assert [oracle.philox_u32(0, 0, 0, j) for j in range(4)] == expect
-    # all-ones KAT: ctr = {ffffffff x4}, key = ffffffff x2 -> j>>2 = 0xffffffff, h = -1, v = -1
-    expect1 = _kat()[1][2]
-    assert [oracle.philox_u32(0xFFFFFFFFFFFFFFFF, -1, -1, (0xFFFFFFFF << 2) | j) for j in range(4)] == expect1
+    """Reading 2's counter layout {j>>2, h, lo32 v, hi32 v}, key {lo32 key, hi32 key}, word j&3,
+    pinned on the ASYMMETRIC Random123 KAT block (ctr = 243f6a88 85a308d3 13198a2e 03707344,
+    key = a4093822 299f31d0): every counter / key word differs, so swapping any two counter words,
+    h with lo32(v), or the key halves, or taking another output word, changes the result."""
+    ctr, key, expect = _kat()[2]
+    assert len(set(ctr)) == 4 and key[0] != key[1]
+    k64 = (key[1] << 32) | key[0]
+    h = ctr[1] - (1 << 32) if ctr[1] >= 1 << 31 else ctr[1]   # int32 hop index carrying the word 0x85a308d3
+    v = (ctr[3] << 32) | ctr[2]
+    got = [oracle.philox_u32(k64, h, v, (ctr[0] << 2) | w) for w in range(4)]
+    assert got == expect
+    # a permuted call must not reproduce it (the test can tell the fields apart)
+    assert [oracle.philox_u32(k64, ctr[2], (ctr[3] << 32) | ctr[1], (ctr[0] << 2) | w) for w in range(4)] != expect
+    # symmetric KATs too (ctr = 0 / all-ones)
+    assert [oracle.philox_u32(0, 0, 0, j) for j in range(4)] == _kat()[0][2]
+    assert [oracle.philox_u32(0xFFFFFFFFFFFFFFFF, -1, -1, (0xFFFFFFFF << 2) | j) for j in range(4)] == _kat()[1][2]
+
+
+def _host_curand_philox(seed: int, n: int):
+    """n outputs of cuRAND's HOST Philox4x32-10 generator (libcurand, a library independent of the
+    oracle), or None when libcurand is not available."""
+    import ctypes
+    import glob
+    libs = (glob.glob("/usr/local/cuda/lib64/libcurand.so*")
+            + glob.glob(os.path.join(os.path.dirname(np.__file__), "..", "nvidia", "curand", "lib", "libcurand.so*")))
+    if not libs:
+        return None
+    cr = ctypes.CDLL(sorted(libs)[0])
+    g = ctypes.c_void_p()
+    CURAND_RNG_PSEUDO_PHILOX4_32_10 = 161
+    assert cr.curandCreateGeneratorHost(ctypes.byref(g), CURAND_RNG_PSEUDO_PHILOX4_32_10) == 0
+    try:
+        assert cr.curandSetPseudoRandomGeneratorSeed(g, ctypes.c_ulonglong(seed)) == 0
+        out = np.zeros(n, dtype=np.uint32)
+        assert cr.curandGenerate(g, out.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(n)) == 0
+    finally:
+        cr.curandDestroyGenerator(g)
+    return out
+
+
+def test_philox_u32_vs_host_curand():
+    """Library pin of the key and vertex words: cuRAND's host Philox4x32-10 generator with seed s emits,
+    as its i-th block of 4 outputs, Philox(ctr = {0, 0, i, 0}, key = {lo32 s, hi32 s}) (one
+    subsequence per block; checked for the first 4096 blocks), which is philox_u32(s, h=0, v=i, j=0..3)
+    under reading 2.  The hop and slot-block words are pinned by the GPU test against
+    curand_init(key, v, (h << 34) | j) (tests/test_gpu_rng.py) and by the asymmetric KAT above."""
+    seed = 0x299F31D0A4093822
+    n_blocks = 4096
+    out = _host_curand_philox(seed, 4 * n_blocks)
+    if out is None:
+        pytest.skip("libcurand not found")
+    for i in list(range(64)) + [255, 256, 1000, 4095]:
+        assert [oracle.philox_u32(seed, 0, i, j) for j in range(4)] == [int(x) for x in out[4 * i: 4 * i + 4]], i
 
 
 @pytest.mark.parametrize("d", range(1, 8))
