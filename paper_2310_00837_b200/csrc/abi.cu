@@ -268,7 +268,7 @@ helios_status helios_presample(helios_graph* g, const int64_t* seeds, int64_t n_
     int64_t nb = std::min<int64_t>(batch, n_seeds - i);
     s = sample_default(g, seeds + i, nb, fanouts, L, keys[b], &g->pre_blocks, st);
     if (s != HELIOS_OK) return s;
-    s = hot_count_enqueue(g->pre_blocks.nodes, g->pre_blocks.level_counts + L, maxn, hotness, g->sms, st);
+    s = hot_count_enqueue(g->pre_blocks.nodes, g->pre_blocks.level_counts + L, maxn, g->V, hotness, g->sms, st);
     if (s != HELIOS_OK) return s;
   }
   return HELIOS_OK;
@@ -524,7 +524,6 @@ helios_status helios_sync(helios_cache* c, void* stream) {
   DeviceGuard dg(c->device);
   HCUDA(cudaStreamSynchronize((cudaStream_t)stream));
   if (c->s_submit) HCUDA(cudaStreamSynchronize(c->s_submit));
-  if (c->s_complete) HCUDA(cudaStreamSynchronize(c->s_complete));
   helios_status a = HELIOS_OK, b = HELIOS_OK;
   helios_status st = read_latched(c->d_err, &a);
   if (st != HELIOS_OK) return st;

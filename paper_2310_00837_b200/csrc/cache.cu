@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cerrno>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <fcntl.h>
 #include <immintrin.h>
@@ -364,14 +365,18 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
   int lo, hi;
   HCUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   HCUDA(cudaStreamCreateWithPriority(&c->s_submit, cudaStreamNonBlocking, hi));
-  HCUDA(cudaStreamCreateWithPriority(&c->s_complete, cudaStreamNonBlocking, hi));
   HCUDA(cudaEventCreateWithFlags(&c->ev_lookup, cudaEventDisableTiming));
   HCUDA(cudaEventCreateWithFlags(&c->ev_submit, cudaEventDisableTiming));
-  HCUDA(cudaEventCreateWithFlags(&c->ev_complete, cudaEventDisableTiming));
   HCUDA(cudaEventCreateWithFlags(&c->ev_io_done, cudaEventDisableTiming));
   if (c->has_file) {
     st = io_start(c, d);
     if (st != HELIOS_OK) return st;
+  }
+  {  // K4 grid: one CTA per SM when host rows are read (PCIe-latency bound, leaves SM slots to the
+     // other batches' sampling); HBM-only caches are bandwidth bound and want more warps in flight
+    int per_sm = (c->S > 0) ? 1 : 2;
+    if (const char* e = getenv("HELIOS_GATHER_CTAS_PER_SM")) per_sm = std::max(1, std::min(atoi(e), 4));
+    c->gather_ctas = c->sms * per_sm;
   }
   c->staged = c->staged && c->S > 0;
   if (c->staged) {
@@ -396,10 +401,8 @@ void cache_free_impl(helios_cache* c) {
   if (c->d_peers) cudaFree(c->d_peers);
   if (c->d_err) cudaFree(c->d_err);
   if (c->s_submit) cudaStreamDestroy(c->s_submit);
-  if (c->s_complete) cudaStreamDestroy(c->s_complete);
   if (c->ev_lookup) cudaEventDestroy(c->ev_lookup);
   if (c->ev_submit) cudaEventDestroy(c->ev_submit);
-  if (c->ev_complete) cudaEventDestroy(c->ev_complete);
   if (c->ev_io_done) cudaEventDestroy(c->ev_io_done);
 }
 

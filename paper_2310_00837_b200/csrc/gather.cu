@@ -5,12 +5,13 @@
 //   cached data in CPU memory by UVA ... or in GPU memory"): HBM (local shard or a peer shard read
 //   over NVLink), HOST (pinned, mapped, read zero-copy over PCIe), or FILE (appended to the miss
 //   list for the IO rings).  Per-tier row counts are warp-reduced into helios_gather_stats.
-// k_io_submit: thread-level parallel IO command submission (§3.1.1) — every lane
-//   owns one request, requests are striped over several SQ rings, the descriptor carries the file
-//   offset (the "SSD logic block") and the staging slot (the "temporary IO buffer").
-// k_io_complete: asynchronous completion handling (§3.1.2) — each warp claims a
-//   request, polls its CQ entry (acquire, system scope), then the whole warp moves the row from the
-//   staging slot into the output feature buffer and frees the slot.
+// k_io: the IO-request producer/consumer pair in one warp-specialised grid.  Submitter warps do
+//   thread-level parallel IO command submission (§3.1.1) — every lane owns one
+//   request, requests are striped over several SQ rings, the descriptor carries the file offset (the
+//   "SSD logic block") and the staging slot (the "temporary IO buffer").  Completer warps do the
+//   asynchronous completion handling (§3.1.2) — each warp claims a request, polls
+//   its CQ entry (acquire, system scope), then moves the row from the staging slot into the output
+//   feature buffer and frees the slot.
 #include <algorithm>
 #include <cstdlib>
 
@@ -37,8 +38,9 @@ struct ListPtrs {
 // Rows [*lo, *hi) of N_L (lo = NULL: from 0); the intra-batch pipeline runs one pass per node range.
 __global__ void __launch_bounds__(256) k_lookup(const int64_t* __restrict__ nodes, const int64_t* __restrict__ lo_ptr,
                                                 const int64_t* __restrict__ n_nodes,
-                                                const int64_t* __restrict__ dir, int32_t rank, ListPtrs L,
-                                                unsigned long long* ctl, const int64_t* trace_params, int trace_idx) {
+                                                const int64_t* __restrict__ dir, int64_t V, int32_t rank, ListPtrs L,
+                                                unsigned long long* ctl, int* err, const int64_t* trace_params,
+                                                int trace_idx) {
   pdl_wait();  // N_L is final once the sampling chain's last kernel has completed
   pdl_trigger();
   TraceScope ts(trace_params, trace_idx);
@@ -51,9 +53,14 @@ __global__ void __launch_bounds__(256) k_lookup(const int64_t* __restrict__ node
     int t = -1;
     uint64_t w = 0;
     if (base + lane < n) {
-      w = (uint64_t)dir[nodes[i]];
-      const uint32_t tier = (uint32_t)(w >> 62);
-      t = tier == 0 ? ((int)((w >> 56) & 63) == rank ? kListLocal : kListPeer) : (tier == 1 ? kListHost : kListFile);
+      const int64_t v = nodes[i];
+      if ((uint64_t)v < (uint64_t)V) {
+        w = (uint64_t)dir[v];
+        const uint32_t tier = (uint32_t)(w >> 62);
+        t = tier == 0 ? ((int)((w >> 56) & 63) == rank ? kListLocal : kListPeer) : (tier == 1 ? kListHost : kListFile);
+      } else {  // a seed out of range (latched by the sampler too) or a bad id passed to helios_gather:
+        latch(err, HELIOS_E_RANGE);  // no directory read, no row copied; the batch's output is undefined
+      }
     }
 #pragma unroll
     for (int q = 0; q < kLists; q++) {
@@ -156,6 +163,46 @@ __device__ __forceinline__ void copy_rows(const GatherArgs& a, int q, int64_t j0
   }
 }
 
+// HBM / NVLink-peer rows, flat mapping: a warp takes rw rows at a time and spreads their rw*nvec
+// 16-byte vectors over its 32 lanes x VU registers (vector f -> row f / nvec, column f % nvec), so
+// every lane is busy whatever the row size (R = 400 B: 25 vectors per row, 10 rows = 250 of 256
+// slots) and each lane has VU independent loads in flight before its stores.  Lanes < rw resolve
+// one row's source / destination pointers; the others get them by shuffle.  rw = max(1, 32*VU/nvec);
+// rows longer than 32*VU vectors take several passes.  inv = ceil(2^20 / nvec) (exact division for
+// f * nvec < 2^20, which holds whenever rw > 1).
+template <int VU>
+__device__ __forceinline__ void copy_rows_flat(const GatherArgs& a, int q, int64_t j0, int64_t cnt, int lane, int nvec,
+                                               int rw, uint32_t inv) {
+  const char* sp = nullptr;
+  char* dp = nullptr;
+  if (lane < rw && j0 + lane < cnt) {
+    const uint64_t w = a.L.w[q][j0 + lane];
+    const int64_t slot = (int64_t)(w & ((1ull << 56) - 1));
+    const char* base = q == kListLocal ? a.hbm : a.peers[(w >> 56) & 63];
+    sp = base + slot * a.R;
+    dp = a.out + a.L.i[q][j0 + lane] * (int64_t)a.R;
+  }
+  const int nrows = (int)min((int64_t)rw, cnt - j0);
+  const int nv = nrows * nvec;
+  for (int b0 = 0; b0 < nv; b0 += 32 * VU) {
+    int4 r[VU];
+#pragma unroll
+    for (int k = 0; k < VU; k++) {
+      const int f = b0 + lane + 32 * k;
+      const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
+      const char* s = (const char*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)sp, row);
+      if (f < nv) r[k] = ld_stream((const int4*)s + (f - row * nvec));
+    }
+#pragma unroll
+    for (int k = 0; k < VU; k++) {
+      const int f = b0 + lane + 32 * k;
+      const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
+      char* d = (char*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)dp, row);
+      if (f < nv) ((int4*)d)[f - row * nvec] = r[k];
+    }
+  }
+}
+
 // K4: warp-specialised gather.
 //   kPartAll (one kernel, every tier): when the host list is non-empty one warp in 8 serves host
 //     rows (zero-copy over PCIe; in staged mode a second warp in 8 consumes staged chunks) while the
@@ -201,11 +248,11 @@ __device__ __forceinline__ void host_rows(const GatherArgs& a, int64_t n_gpu, in
 __device__ __forceinline__ bool staged_rows(const GatherArgs& a, int64_t n_gpu, int64_t n_stage, int lane, int nvec) {
   const uint32_t seq = (uint32_t)a.ctl[kCtlStageSeq];
   const int64_t n_chunks = (n_stage + kStageChunk - 1) / kStageChunk;
-  const uint64_t t0 = globaltimer();
   for (;;) {
     const int64_t ch = warp_ticket(&a.ctl[kCtlStageTicket], 1, lane);
     if (ch >= n_chunks) break;
     bool ok = true;
+    const uint64_t t0 = globaltimer();
     unsigned backoff = 128;  // each poll is a PCIe read that competes with the row reads: back off
     while (ld_acquire_sys_u32_(&a.done[ch]) != seq) {  // every lane polls (one request)
       if (globaltimer() - t0 > kStageWatchdogNs) {
@@ -229,8 +276,8 @@ __device__ __forceinline__ bool staged_rows(const GatherArgs& a, int64_t n_gpu, 
   return true;
 }
 
-template <int VPL, int U, int UH>
-__global__ void __launch_bounds__(256, 4) k_gather_lists(GatherArgs a) {
+template <int VPL, int UH>
+__global__ void __launch_bounds__(256, 2) k_gather_lists(GatherArgs a) {
   pdl_wait();
   pdl_trigger();
   TraceScope ts(a.part == kPartHost ? nullptr : a.trace_params, a.trace_idx);
@@ -270,8 +317,11 @@ __global__ void __launch_bounds__(256, 4) k_gather_lists(GatherArgs a) {
   }
   const int64_t dw = (gw >> 3) * (8 - nspecial) + (r - nspecial);  // index among data warps
   const int64_t n_dw = (nw >> 3) * (8 - nspecial);
-  for (int64_t j0 = dw * U; j0 < n_peer; j0 += n_dw * U) copy_rows<VPL, U>(a, kListPeer, j0, n_peer, lane, nvec);
-  for (int64_t j0 = dw * U; j0 < n_local; j0 += n_dw * U) copy_rows<VPL, U>(a, kListLocal, j0, n_local, lane, nvec);
+  constexpr int VU = 8;
+  const int rw = max(1, 32 * VU / nvec);
+  const uint32_t inv = ((1u << 20) + (uint32_t)nvec - 1u) / (uint32_t)nvec;
+  for (int64_t j0 = dw * rw; j0 < n_peer; j0 += n_dw * rw) copy_rows_flat<VU>(a, kListPeer, j0, n_peer, lane, nvec, rw, inv);
+  for (int64_t j0 = dw * rw; j0 < n_local; j0 += n_dw * rw) copy_rows_flat<VU>(a, kListLocal, j0, n_local, lane, nvec, rw, inv);
 }
 
 // Plain row copy by id (setup: HBM-tier fill from a mapped host table).
@@ -341,10 +391,19 @@ struct IoArgs {
   int* err;
 };
 
-__global__ void __launch_bounds__(256) k_io_submit(IoArgs a) {
-  const int lane = threadIdx.x & 31;
+// K5 + K6 in ONE warp-specialised grid: in every CTA the first kIoSubmitWarps
+// warps are submitters (thread-level submission, §3.1.1: each lane takes one request by ticket,
+// waits for its ring slot to be free, writes the descriptor, publishes seq with st.release.sys) and
+// the other warps are completers (asynchronous completion, §3.1.2: a warp takes one request by
+// ticket, polls its CQ entry with ld.acquire.sys, moves the row staging -> out and frees the slot).
+// Tickets are taken only by running warps, and every wait is on a strictly smaller ticket (a slot
+// waits for request m - ring_size, a completion for its own submission), so the kernel makes progress
+// with any number of its CTAs resident — also when it is serialised against every other kernel
+// (ncu, CUDA_LAUNCH_BLOCKING, an SM-capped partition).  Watchdogs restart at every wait.
+constexpr int kIoSubmitWarps = 2;
+
+__device__ __forceinline__ void io_submit_warp(const IoArgs& a, int lane) {
   const unsigned long long M = a.ctl[kListFile];
-  const uint64_t t0 = globaltimer();
   for (;;) {
     unsigned long long tk = 0;
     if (lane == 0) tk = atomicAdd(&a.ctl[kCtlSubmit], 32ull);
@@ -358,7 +417,8 @@ __global__ void __launch_bounds__(256) k_io_submit(IoArgs a) {
       const uint32_t slot = (seq - 1u) & (uint32_t)(a.depth - 1);
       const int64_t idx = (int64_t)r * a.depth + slot;
       bool ok = true;
-      // slot reusable once its previous occupant (seq - depth) was consumed by io_complete
+      // slot reusable once its previous occupant (seq - depth) was consumed by a completer
+      const uint64_t t0 = globaltimer();
       while ((int32_t)(seq - (uint32_t)a.depth - ld_acquire_gpu_u32(a.free_seq + idx)) > 0) {
         if (globaltimer() - t0 > kWatchdogNs) {
           latch(a.err, HELIOS_E_TIMEOUT);
@@ -380,11 +440,9 @@ __global__ void __launch_bounds__(256) k_io_submit(IoArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_io_complete(IoArgs a) {
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void io_complete_warp(const IoArgs& a, int lane) {
   const unsigned long long M = a.ctl[kListFile];
   const int nvec = a.R >> 4;
-  const uint64_t t0 = globaltimer();
   for (;;) {
     unsigned long long m = 0;
     if (lane == 0) m = atomicAdd(&a.ctl[kCtlComplete], 1ull);
@@ -396,6 +454,7 @@ __global__ void __launch_bounds__(256) k_io_complete(IoArgs a) {
     const uint32_t slot = (seq - 1u) & (uint32_t)(a.depth - 1);
     const int64_t idx = (int64_t)r * a.depth + slot;
     bool ok = true;
+    const uint64_t t0 = globaltimer();
     while (ld_acquire_sys_u32(&a.cq[idx].seq) != seq) {  // every lane polls (one coalesced request)
       if (globaltimer() - t0 > kWatchdogNs) {
         ok = false;
@@ -424,16 +483,21 @@ __global__ void __launch_bounds__(256) k_io_complete(IoArgs a) {
   }
 }
 
+__global__ void __launch_bounds__(256) k_io(IoArgs a) {
+  const int lane = threadIdx.x & 31;
+  if ((threadIdx.x >> 5) < kIoSubmitWarps) io_submit_warp(a, lane);
+  else io_complete_warp(a, lane);
+}
+
 // Ablation (HELIOS_CACHE_IO_SYNC): the synchronous IO stack the paper measures GIDS/BaM with
 // (§2.2, Fig. iostack_bam): each warp owns one request end to end — its leader
 // reserves a ring slot and submits, the warp then spins on the completion and finally copies the
 // row — so a warp is tied up for the whole IO latency and at most one request per warp is in
-// flight.  Same rings and host workers as the decoupled k_io_submit / k_io_complete pair.
+// flight.  Same rings and host workers as the decoupled submit / complete roles of k_io.
 __global__ void __launch_bounds__(256) k_io_sync(IoArgs a) {
   const int lane = threadIdx.x & 31;
   const unsigned long long M = a.ctl[kListFile];
   const int nvec = a.R >> 4;
-  const uint64_t t0 = globaltimer();
   for (;;) {
     unsigned long long m = 0;
     if (lane == 0) m = atomicAdd(&a.ctl[kCtlSubmit], 1ull);
@@ -445,6 +509,7 @@ __global__ void __launch_bounds__(256) k_io_sync(IoArgs a) {
     const uint32_t slot = (seq - 1u) & (uint32_t)(a.depth - 1);
     const int64_t idx = (int64_t)r * a.depth + slot;
     bool ok = true;
+    uint64_t t0 = globaltimer();
     if (lane == 0) {
       while ((int32_t)(seq - (uint32_t)a.depth - ld_acquire_gpu_u32(a.free_seq + idx)) > 0) {
         if (globaltimer() - t0 > kWatchdogNs) {
@@ -464,6 +529,7 @@ __global__ void __launch_bounds__(256) k_io_sync(IoArgs a) {
       }
     }
     ok = __shfl_sync(0xFFFFFFFFu, ok, 0);
+    t0 = globaltimer();
     while (ok && ld_acquire_sys_u32(&a.cq[idx].seq) != seq) {
       if (globaltimer() - t0 > kWatchdogNs) ok = false;
       else __nanosleep(128);
@@ -493,32 +559,32 @@ __global__ void k_io_finish(unsigned long long* ctl, uint32_t* base_seq, int rin
     base_seq[r] += (uint32_t)(M / rings + ((unsigned long long)r < M % rings ? 1 : 0));
 }
 
-// The IO kernels wait on each other while running concurrently, so they must not be lazily
-// loaded (CUDA 12 lazy loading may wait for the running kernel before loading the other one).
+// The IO kernels spin on host workers, so they are loaded up front rather than lazily (CUDA 12
+// lazy loading of a kernel may wait for running work).
 helios_status io_preload_kernels() {
   cudaFuncAttributes fa;
-  HCUDA(cudaFuncGetAttributes(&fa, k_io_submit));
-  HCUDA(cudaFuncGetAttributes(&fa, k_io_complete));
+  HCUDA(cudaFuncGetAttributes(&fa, k_io));
   HCUDA(cudaFuncGetAttributes(&fa, k_io_finish));
   HCUDA(cudaFuncGetAttributes(&fa, k_io_sync));
   return HELIOS_OK;
 }
 
-// Persistent grid of one CTA per SM (8 warps each; one in 8 serves host rows).  A gather waits on
-// PCIe reads for most of its life, so a smaller grid leaves SM slots to the other in-flight batches'
-// sampling: measured against 4 CTAs per SM, C3 +6 % and C2 +6 %; 74-296 CTAs are within noise on
-// C3, 74 is 4 % slower on C2; 2 or 4 host warps per 8 are slower.
-template <int VPL, int U, int UH>
-static void launch_gather(const GatherArgs& a, int sms, cudaStream_t st) {
-  launch_pdl(k_gather_lists<VPL, U, UH>, dim3(sms), dim3(256), st, a);
+// Persistent grid (8 warps per CTA; one in 8 serves host rows when the batch has any).  With a host
+// tier: one CTA per SM — a gather waits on PCIe reads for most of its life, so a smaller resident
+// footprint leaves SM slots to the other in-flight batches' sampling (measured against 4 CTAs per
+// SM: C3 +6 %, C2 +6 %; 74-296 CTAs within noise on C3; 2 or 4 host warps per 8 are slower,
+// DESIGN.md §11).  HBM-only caches use c->gather_ctas CTAs (K4 grid sweep).
+template <int VPL, int UH>
+static void launch_gather(const GatherArgs& a, int grid, cudaStream_t st) {
+  launch_pdl(k_gather_lists<VPL, UH>, dim3(grid), dim3(256), st, a);
 }
 
-static void launch_gather_any(const GatherArgs& a, int sms, cudaStream_t st) {
+static void launch_gather_any(const GatherArgs& a, int grid, cudaStream_t st) {
   const int nvec = a.R / 16;
-  if (nvec <= 32) launch_gather<1, 4, 8>(a, sms, st);
-  else if (nvec <= 64) launch_gather<2, 2, 4>(a, sms, st);
-  else if (nvec <= 128) launch_gather<4, 1, 2>(a, sms, st);
-  else launch_gather<8, 1, 1>(a, sms, st);
+  if (nvec <= 32) launch_gather<1, 8>(a, grid, st);
+  else if (nvec <= 64) launch_gather<2, 4>(a, grid, st);
+  else if (nvec <= 128) launch_gather<4, 2>(a, grid, st);
+  else launch_gather<8, 1>(a, grid, st);
 }
 
 void gws_free(GatherWS& w) {
@@ -614,10 +680,10 @@ static helios_status gather_pass(helios_cache* c, GatherWS& w, const int64_t* no
   }
   GatherArgs a = make_args(c, w, out, stats, accumulate, part);
   const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_rows + 255) / 256), (int64_t)c->sms * 2);
-  launch_pdl(k_lookup, dim3(lg), dim3(256), st, nodes, lo, n_nodes, (const int64_t*)c->dir, c->rank, a.L, w.d_ctl,
-             w.trace_params, w.trace_idx);
+  launch_pdl(k_lookup, dim3(lg), dim3(256), st, nodes, lo, n_nodes, (const int64_t*)c->dir, c->V, c->rank, a.L, w.d_ctl,
+             c->d_err, w.trace_params, w.trace_idx);
   if (a.staged) launch_pdl(k_stage_publish, dim3(1), dim3(1), st, w.d_ctl, w.d_seq, w.d_mail, c->stage_frac, kStageCapRows);
-  launch_gather_any(a, c->sms, st);
+  launch_gather_any(a, c->gather_ctas, st);
   HCUDA(cudaGetLastError());
   return HELIOS_OK;
 }
@@ -643,7 +709,7 @@ helios_status gather_hbm_launch(helios_cache* c, GatherWS& w, const int64_t* nod
 helios_status gather_host_launch(helios_cache* c, GatherWS& w, void* out, cudaStream_t st) {
   HCHECK(!c->broken, HELIOS_E_STATE, "cache unusable after an IO / staging watchdog timeout");
   const GatherArgs a = make_args(c, w, out, nullptr, false, kPartHost);
-  launch_gather_any(a, c->sms, st);
+  launch_gather_any(a, c->gather_ctas, st);
   HCUDA(cudaGetLastError());
   return HELIOS_OK;
 }
@@ -701,7 +767,7 @@ helios_status probe_host_impl(helios_cache* c, int64_t n, uint64_t seed, int32_t
       k_probe_list<<<c->sms * 4, 256, 0, st>>>(a.L.i[kListHost], a.L.w[kListHost], w.d_ctl, n, range,
                                                 seed ^ (0x5851F42D4C957F2Dull * (uint64_t)(r + 1)));
       HCUDA(cudaEventRecord(e0, st));
-      launch_gather_any(a, c->sms, st);
+      launch_gather_any(a, c->sms, st);  // the host part: one CTA per SM as in the pipeline
       HCUDA(cudaEventRecord(e1, st));
       HCUDA(cudaEventSynchronize(e1));
       float t = 0;
@@ -747,24 +813,15 @@ helios_status io_launch(helios_cache* c, GatherWS& w, void* out, cudaStream_t st
   io.R = c->R;
   io.out = (char*)out;
   io.err = c->d_err;
+  HCHECK(!c->broken, HELIOS_E_STATE, "cache unusable after an IO / staging watchdog timeout");
   HCUDA(cudaEventRecord(c->ev_lookup, st));
   HCUDA(cudaStreamWaitEvent(c->s_submit, c->ev_lookup, 0));
-  HCUDA(cudaStreamWaitEvent(c->s_complete, c->ev_lookup, 0));
-  if (c->io_pending) {
-    HCUDA(cudaStreamWaitEvent(c->s_submit, c->ev_io_done, 0));
-    HCUDA(cudaStreamWaitEvent(c->s_complete, c->ev_io_done, 0));
-  }
-  if (c->io_sync) {
-    k_io_sync<<<c->io_ctas, 256, 0, c->s_complete>>>(io);
-  } else {
-    k_io_complete<<<c->io_ctas, 256, 0, c->s_complete>>>(io);
-    k_io_submit<<<c->io_ctas, 256, 0, c->s_submit>>>(io);
-  }
+  if (c->io_pending) HCUDA(cudaStreamWaitEvent(c->s_submit, c->ev_io_done, 0));
+  if (c->io_sync) k_io_sync<<<c->io_ctas, 256, 0, c->s_submit>>>(io);
+  else k_io<<<c->io_ctas, 256, 0, c->s_submit>>>(io);
   HCUDA(cudaGetLastError());
   HCUDA(cudaEventRecord(c->ev_submit, c->s_submit));
-  HCUDA(cudaEventRecord(c->ev_complete, c->s_complete));
   HCUDA(cudaStreamWaitEvent(st, c->ev_submit, 0));
-  HCUDA(cudaStreamWaitEvent(st, c->ev_complete, 0));
   k_io_finish<<<1, 64, 0, st>>>(w.d_ctl, c->io.d_base_seq, c->io.rings);
   HCUDA(cudaGetLastError());
   HCUDA(cudaEventRecord(c->ev_io_done, st));

@@ -240,6 +240,7 @@ struct helios_cache {
   std::string path;
   int64_t header = 0, stride = 0;
   int io_ctas = 32;
+  int gather_ctas = 148;            // K4 grid (one CTA per SM with a host tier, more for HBM-only caches)
   bool io_sync = false;            // HELIOS_CACHE_IO_SYNC ablation
   bool broken = false;             // a ring / staging watchdog fired: ring state is no longer consistent
   helios::IoRings io;
@@ -250,8 +251,8 @@ struct helios_cache {
   int stage_workers = 8;
   helios::Stager* stager = nullptr;
   helios::GatherWS gws;            // default gather context (helios_gather / helios_batch_prepare)
-  cudaStream_t s_submit = nullptr, s_complete = nullptr;
-  cudaEvent_t ev_lookup = nullptr, ev_submit = nullptr, ev_complete = nullptr, ev_io_done = nullptr;
+  cudaStream_t s_submit = nullptr;  // IO stream: k_io of successive batches, serialised (ring sequences)
+  cudaEvent_t ev_lookup = nullptr, ev_submit = nullptr, ev_io_done = nullptr;
   bool io_pending = false;         // ev_io_done recorded at least once
 };
 
@@ -331,7 +332,7 @@ helios_status ws_upload_params(SampleWS& w, uint64_t key, int64_t B, const int64
 helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const int32_t* fanouts, int32_t L,
                             const helios_blocks* out, cudaStream_t st,
                             const std::function<helios_status(int)>* stage_hook = nullptr);
-helios_status hot_count_enqueue(const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, uint64_t* hot,
+helios_status hot_count_enqueue(const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, int64_t V, uint64_t* hot,
                                 int sms, cudaStream_t st);
 helios_status gws_ensure(helios_cache* c, GatherWS& w, int64_t max_nodes);
 void gws_free(GatherWS& w);

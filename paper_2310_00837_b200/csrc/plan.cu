@@ -188,6 +188,7 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
   HCHECK(n >= 0 && n <= p->d.max_seeds, HELIOS_E_CAPACITY, "n_seeds %lld > plan capacity %lld", (long long)n,
          (long long)p->d.max_seeds);
   HCHECK(n == 0 || seeds, HELIOS_E_INVALID, "null seeds");
+  HCHECK(!p->c || !p->c->broken, HELIOS_E_STATE, "cache unusable after an IO / staging watchdog timeout");
   PlanSlot& sl = p->slots[slot];
   HCUDA(cudaEventRecord(sl.ev_caller, caller));
   HCUDA(cudaStreamWaitEvent(sl.stream, sl.ev_caller, 0));

@@ -394,16 +394,21 @@ __global__ void __launch_bounds__(256, 2) k_sample_batch(SampleCtx c) {
   dev_table_clear(c);
 }
 
-__global__ void k_hot_count(const int64_t* __restrict__ nodes, const int64_t* __restrict__ n_nodes, uint64_t* hot) {
+// hot[v] += 1 for every v of the batch's N_L.  An out-of-range id (a bad presample seed, already
+// latched E_RANGE by insert_seed) is skipped rather than counted out of bounds.
+__global__ void k_hot_count(const int64_t* __restrict__ nodes, const int64_t* __restrict__ n_nodes, int64_t V,
+                            uint64_t* hot) {
   const int64_t n = *n_nodes;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd((unsigned long long*)&hot[nodes[i]], 1ull);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = nodes[i];
+    if ((uint64_t)v < (uint64_t)V) atomicAdd((unsigned long long*)&hot[v], 1ull);
+  }
 }
 
-helios_status hot_count_enqueue(const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, uint64_t* hot, int sms,
-                                cudaStream_t st) {
+helios_status hot_count_enqueue(const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, int64_t V, uint64_t* hot,
+                                int sms, cudaStream_t st) {
   const int grid = (int)std::min<int64_t>((max_nodes + 255) / 256, (int64_t)sms * 8);
-  k_hot_count<<<std::max(grid, 1), 256, 0, st>>>(nodes, n_nodes, hot);
+  k_hot_count<<<std::max(grid, 1), 256, 0, st>>>(nodes, n_nodes, V, hot);
   HCUDA(cudaGetLastError());
   return HELIOS_OK;
 }
@@ -493,10 +498,10 @@ helios_status sample_check_out(const helios_graph* g, int64_t B, const int32_t* 
   return HELIOS_OK;
 }
 
-static uint32_t pow2_at_least(int64_t x) {
+static uint64_t pow2_at_least(int64_t x) {
   uint64_t p = 1024;
   while ((int64_t)p < x) p <<= 1;
-  return (uint32_t)p;
+  return p;
 }
 
 void ws_free(SampleWS& w) {
@@ -520,7 +525,11 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
     tiles_e = std::max(tiles_e, (edg[h] + kScanTile - 1) / kScanTile);
   }
   // worst-case load <= 0.8 (n_L bound / table); the typical batch fills a few percent of it
-  uint32_t T = pow2_at_least(std::min<int64_t>(g->V, std::max<int64_t>(maxn, 1)) * 5 / 4);
+  const uint64_t T64 = pow2_at_least(std::min<int64_t>(g->V, std::max<int64_t>(maxn, 1)) * 5 / 4);
+  // slots are u32-indexed with kEmpty = 2^32-1 reserved: at most 2^31 slots
+  HCHECK(T64 <= (1ull << 31), HELIOS_E_CAPACITY, "batch hash table of %llu slots exceeds 2^31 (V=%lld, node bound %lld)",
+         (unsigned long long)T64, (long long)g->V, (long long)maxn);
+  const uint32_t T = (uint32_t)T64;
   const int64_t max_nodes = std::max<int64_t>(maxn, 1);
   if (w.reset_base && T <= w.table_size && max_e <= w.cap_edges && tiles_r <= w.cap_tiles_rows &&
       tiles_e <= w.cap_tiles_edges && max_nodes <= w.cap_nodes && B <= w.cap_seeds)

@@ -134,6 +134,21 @@ def _stream(stream) -> int | None:
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
+def _device_ids(t: torch.Tensor, stream) -> torch.Tensor:
+    """int64, contiguous device ids for an enqueue-only call.  A converted copy is a temporary of the
+    current torch stream: when the call enqueues on another stream, the copy is recorded on that
+    stream so the caching allocator does not reuse its memory before the library's kernels read it."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("device ids must be a CUDA tensor")
+    if t.dtype == torch.int64 and t.is_contiguous():
+        return t
+    c = t.to(torch.int64).contiguous()
+    s = _stream(stream)
+    if s != torch.cuda.current_stream().cuda_stream:
+        c.record_stream(torch.cuda.ExternalStream(s))
+    return c
+
+
 def helios_abi_version() -> int:
     return _lib.helios_abi_version()
 
@@ -233,6 +248,7 @@ class Blocks:
 
 def helios_sample(g: Graph, seeds: torch.Tensor, fanouts, key: int, out: Blocks, stream=None) -> None:
     fan = np.ascontiguousarray(fanouts, dtype=np.int32)
+    seeds = _device_ids(seeds, stream)
     s = out.struct()
     _check(_lib.helios_sample(g.handle, _ptr(seeds), seeds.numel(), _ptr(fan), len(fan), key & (2**64 - 1),
                               ctypes.byref(s), _stream(stream)), "helios_sample")
@@ -253,6 +269,9 @@ def helios_presample(g: Graph, seeds: torch.Tensor, batch: int, fanouts, keys, h
                      stream=None) -> None:
     fan = np.ascontiguousarray(fanouts, dtype=np.int32)
     ks = np.ascontiguousarray([k & (2**64 - 1) for k in keys], dtype=np.uint64)
+    seeds = _device_ids(seeds, stream)
+    if hotness.dtype not in (torch.int64, torch.uint64) or not hotness.is_contiguous() or not hotness.is_cuda:
+        raise TypeError("hotness must be a contiguous 64-bit CUDA tensor [V] (accumulated in place)")
     _check(_lib.helios_presample(g.handle, _ptr(seeds), seeds.numel(), batch, _ptr(fan), len(fan), _ptr(ks),
                                  _ptr(hotness), _stream(stream)), "helios_presample")
 
@@ -318,6 +337,7 @@ def helios_cache_attach_peers(c: Cache, blobs: list[bytes]) -> None:
 
 def helios_gather(c: Cache, nodes: torch.Tensor, n_nodes: torch.Tensor, out: torch.Tensor,
                   stats: torch.Tensor | None = None, stream=None) -> None:
+    nodes = _device_ids(nodes, stream)
     _check(_lib.helios_gather(c.handle, _ptr(nodes), _ptr(n_nodes), nodes.numel(), _ptr(out), _ptr(stats),
                               _stream(stream)), "helios_gather")
 
@@ -325,6 +345,7 @@ def helios_gather(c: Cache, nodes: torch.Tensor, n_nodes: torch.Tensor, out: tor
 def helios_batch_prepare(g: Graph, c: Cache, seeds: torch.Tensor, fanouts, key: int, out: Blocks,
                          features: torch.Tensor, stats: torch.Tensor | None = None, stream=None) -> None:
     fan = np.ascontiguousarray(fanouts, dtype=np.int32)
+    seeds = _device_ids(seeds, stream)
     s = out.struct()
     _check(_lib.helios_batch_prepare(g.handle, c.handle, _ptr(seeds), seeds.numel(), _ptr(fan), len(fan),
                                      key & (2**64 - 1), ctypes.byref(s), _ptr(features), _ptr(stats),
@@ -416,10 +437,16 @@ def helios_plan_create(g: Graph, c: Cache | None, B: int, fanouts, depth: int = 
 
 def helios_plan_submit(p: Plan, slot: int, seeds, key: int, stream=None, timing: bool = False,
                        readback: bool = False) -> None:
-    if isinstance(seeds, torch.Tensor) and seeds.is_cuda:
+    if isinstance(seeds, torch.Tensor) and seeds.is_cuda and seeds.dtype == torch.int64 and seeds.is_contiguous():
+        # the plan reads them later on its slot stream: the caller keeps them alive until the batch
+        # completes (helios.h, helios_plan_submit)
         ptr, n, fl = seeds.data_ptr(), seeds.numel(), 0
     else:
-        arr = np.ascontiguousarray(seeds, dtype=np.int64) if not isinstance(seeds, torch.Tensor) else seeds
+        # host seeds, or device seeds needing a conversion: copied into the submit's parameter block
+        # (no temporary device buffer whose lifetime the plan would have to track)
+        if isinstance(seeds, torch.Tensor):
+            seeds = seeds.detach().to("cpu", torch.int64).numpy()
+        arr = np.ascontiguousarray(seeds, dtype=np.int64)
         ptr, n, fl = _ptr(arr), len(arr), SUBMIT_SEEDS_HOST
     if timing:
         fl |= SUBMIT_TIMING

@@ -182,3 +182,90 @@ def test_probe_host(H, c1, c1_hot, alias):
         H.helios_cache_probe_host(c0, 100)
     assert e.value.name == "E_STATE"
     c0.free()
+
+
+def _check_batch(H, c1, blocks, feats, seeds, key):
+    got = blocks.to_host()
+    orc = oracle.sample(c1.graph.indptr, c1.graph.indices, seeds, c1.cfg.fanouts, key)
+    assert np.array_equal(got["nodes"], orc.nodes)
+    for h in range(len(c1.cfg.fanouts)):
+        assert np.array_equal(got["block_indices"][h], orc.block_indices[h])
+    assert np.array_equal(feats[: len(orc.nodes)].cpu().numpy(), oracle.gather(orc.nodes, c1.cfg.R, table=c1.table))
+
+
+@pytest.mark.parametrize("bad", [-3, 10_005, 2**40])
+def test_bad_seed_latches_range(H, c1, c1_hot, bad):
+    """A seed outside [0, V) through helios_batch_prepare, helios_plan_submit (device and host seeds),
+    helios_gather and helios_presample latches E_RANGE (helios.h) without any out-of-bounds access:
+    the context stays healthy and the next good batch is bit-exact (memcheck: profiles/sanitizer_r02)."""
+    g, hot = c1_hot
+    cfg = c1.cfg
+    Hr, S = workloads.tier_rows(cfg)
+    c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=c1.table, feature_path=c1.feature_path,
+                             header_bytes=c1.header, file_stride=c1.stride, flags=H.HOST_ALIAS)
+    keys = workloads.batch_keys(0, 2)
+    good = c1.batches[0]
+    badseeds = good.copy()
+    badseeds[7] = bad
+    blocks = H.Blocks.allocate(cfg.B, cfg.fanouts, g.V, g.E)
+    feats = torch.empty((blocks.nodes.numel(), cfg.R), dtype=torch.uint8, device="cuda")
+    H.helios_batch_prepare(g, c, torch.as_tensor(badseeds).cuda(), cfg.fanouts, keys[0], blocks, feats)
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_sync(c)
+    assert e.value.name == "E_RANGE"
+    H.helios_batch_prepare(g, c, torch.as_tensor(good).cuda(), cfg.fanouts, keys[1], blocks, feats)
+    H.helios_sync(c)
+    _check_batch(H, c1, blocks, feats, good, keys[1])
+    # the plan (CUDA graphs), device seeds and host seeds
+    plan = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=2)
+    dev_bad = torch.as_tensor(badseeds).cuda()
+    for k, sd in enumerate((dev_bad, badseeds)):
+        H.helios_plan_submit(plan, k, sd, keys[0])
+        H.helios_plan_wait(plan, k)
+        with pytest.raises(H.HeliosError) as e:
+            H.helios_sync(c)
+        assert e.value.name == "E_RANGE"
+    H.helios_plan_submit(plan, 0, good, keys[1])
+    H.helios_plan_wait(plan, 0)
+    H.helios_sync(c)
+    blk, fts, _ = plan.outputs[0]
+    _check_batch(H, c1, blk, fts, good, keys[1])
+    plan.free()
+    # helios_gather of a bad id
+    out = torch.empty((4, cfg.R), dtype=torch.uint8, device="cuda")
+    H.helios_gather(c, torch.tensor([1, bad, 2, 3], device="cuda"), torch.tensor([4], device="cuda"), out)
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_sync(c)
+    assert e.value.name == "E_RANGE"
+    c.free()
+    # presample of a bad seed: latched, no out-of-bounds hotness update
+    hot2 = torch.zeros(cfg.V, dtype=torch.int64, device="cuda")
+    H.helios_presample(g, torch.as_tensor(badseeds).cuda(), cfg.B, cfg.fanouts, [keys[0]], hot2)
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_graph_sync(g)
+    assert e.value.name == "E_RANGE"
+    assert int(hot2.sum()) > 0
+
+
+def test_seed_dtype_conversion(H, c1, c1_hot):
+    """int32 / non-contiguous seeds are converted by the binding (never read as int64 past the end)."""
+    g, hot = c1_hot
+    cfg = c1.cfg
+    c = H.helios_cache_build(g, hot, cfg.R, cfg.V, 0, host_table=c1.table)
+    keys = workloads.batch_keys(0, 1)
+    good = c1.batches[0]
+    plan = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=1)
+    s32 = torch.as_tensor(good.astype(np.int32)).cuda()
+    H.helios_plan_submit(plan, 0, s32, keys[0])
+    H.helios_plan_wait(plan, 0)
+    H.helios_sync(c)
+    blk, fts, _ = plan.outputs[0]
+    _check_batch(H, c1, blk, fts, good, keys[0])
+    plan.free()
+    blocks = H.Blocks.allocate(cfg.B, cfg.fanouts, g.V, g.E)
+    feats = torch.empty((blocks.nodes.numel(), cfg.R), dtype=torch.uint8, device="cuda")
+    strided = torch.as_tensor(np.repeat(good, 2)).cuda()[::2]
+    H.helios_batch_prepare(g, c, strided.to(torch.int32), cfg.fanouts, keys[0], blocks, feats)
+    H.helios_sync(c)
+    _check_batch(H, c1, blocks, feats, good, keys[0])
+    c.free()
