@@ -251,26 +251,53 @@ def interval_union(iv) -> float:
 
 # ---------------------------------------------------------------------------------------------
 
-def run_oracle_baseline(inp, keys, budget_s: float, check=None, dir_=None) -> dict:
-    """The oracle as it stands (single-threaded C++), on a bounded sample of the same batches.
-    Rows come from the canonical host table, or by pread from the feature file when the config
-    keeps no table (a CPU-managed cache)."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def run_oracle_baseline(inp, keys, budget_s: float, check=None, dir_=None, threads: int = 1) -> dict:
+    """The oracle as it stands (single-threaded C++ per batch), on a bounded sample of the same
+    batches.  threads > 1: that many host threads, each preparing independent batches (one batch per
+    thread at a time; the oracle's ctypes calls release the GIL), as SURVEY §8(d)'s P-core leg.  Rows
+    come from the canonical host table, or by pread from the feature file when the config keeps no
+    table (a CPU-managed cache)."""
     import oracle
     cfg = inp.cfg
+    lock = threading.Lock()
+    state = {"next": 0, "done": 0, "rows": 0}
     t0 = time.perf_counter()
-    done, rows = 0, 0
-    for b, (seeds, key) in enumerate(zip(inp.batches, keys)):
-        ob = oracle.sample(inp.graph.indptr, inp.graph.indices, seeds, cfg.fanouts, key)
-        feats = oracle.gather(ob.nodes, cfg.R, table=inp.table, path=inp.feature_path, header=inp.header,
-                              stride=inp.stride, dir_=dir_)
-        if check is not None:
-            check(b, ob, feats)
-        done += 1
-        rows += len(ob.nodes)
-        if time.perf_counter() - t0 > budget_s:
-            break
+
+    def worker():
+        while True:
+            with lock:
+                b = state["next"]
+                if b >= len(inp.batches) or time.perf_counter() - t0 > budget_s:
+                    return
+                state["next"] += 1
+            ob = oracle.sample(inp.graph.indptr, inp.graph.indices, inp.batches[b], cfg.fanouts, keys[b])
+            feats = oracle.gather(ob.nodes, cfg.R, table=inp.table, path=inp.feature_path, header=inp.header,
+                                  stride=inp.stride, dir_=dir_)
+            if check is not None:
+                check(b, ob, feats)
+            with lock:
+                state["done"] += 1
+                state["rows"] += len(ob.nodes)
+
+    ths = [threading.Thread(target=worker) for _ in range(max(1, threads))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
     dt = time.perf_counter() - t0
-    return {"batches": done, "seconds": dt, "value": done / dt, "gbs": rows * cfg.R / dt / 1e9}
+    return {"batches": state["done"], "seconds": dt, "value": state["done"] / dt,
+            "gbs": state["rows"] * cfg.R / dt / 1e9, "threads": max(1, threads)}
 
 
 def main():
@@ -297,13 +324,18 @@ def main():
                     help="CSR in pinned host memory, sampled zero-copy (the paper's placement; SURVEY NEXT-2)")
     ap.add_argument("--hbm-frac", type=float, default=-1.0, help="override the HBM-tier share of V (tier ablation)")
     ap.add_argument("--host-frac", type=float, default=-1.0, help="override the host-tier share of V (tier ablation)")
-    ap.add_argument("--host-staged", type=float, default=0.0,
-                    help="share of host-tier rows copied by host stager threads (0 = pure zero-copy)")
-    ap.add_argument("--stage-workers", type=int, default=8)
+    ap.add_argument("--host-staged", type=float, default=1.0,
+                    help="host tier: dynamic split between GPU zero-copy reads and host stager threads, with this "
+                         "cap on the stagers' share of a batch's host rows (default 1.0 = no cap); 0 = pure zero-copy")
+    ap.add_argument("--zero-copy", action="store_true", help="ablation: pure GPU zero-copy host tier (= --host-staged 0)")
+    ap.add_argument("--stage-workers", type=int, default=14,
+                    help="host stager threads (HOST_STAGED); 14 of the GPU box's 16 cores measured best")
     ap.add_argument("--ring-depth", type=int, default=256)
     ap.add_argument("--io-ctas", type=int, default=32, help="CTA budget of each IO kernel (PAPER.md:244)")
     ap.add_argument("--io-sync", action="store_true", help="ablation: GIDS-style coupled IO (one warp per request)")
     args = ap.parse_args()
+    if args.zero_copy:
+        args.host_staged = 0.0
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -454,6 +486,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    staged0 = c.info().staged_rows
     torch.cuda.nvtx.range_push("timed")
     with ClockSampler(local) as clk:
         start = torch.cuda.Event(enable_timing=True)
@@ -472,6 +505,7 @@ def main():
         torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
     H.helios_sync(c)
+    staged_timed = c.info().staged_rows - staged0
     total_ms = start.elapsed_time(end)
     sample_ms, gather_ms, link_ms, gather_iv, link_iv = [], [], [], [], []
     for k in range(depth):
@@ -558,21 +592,57 @@ def main():
             if file_cfg:   # CPU-managed cache: FILE-tier rows by pread, the rest from memory
                 dir_host = H.device_view(c.info().dir, cfg.V, torch.int64).cpu().numpy()
             r = run_oracle_baseline(inp, keys, args.cpu_budget, dir_=dir_host)
+            P = len(os.sched_getaffinity(0))
+            rP = run_oracle_baseline(inp, keys, args.cpu_budget, dir_=dir_host, threads=P)
             cpu = {"value": round(r["value"], 4), "unit": "batches/s", "cores": 1, "kind": "oracle",
                    "sample": f"{r['batches']} batches of {cfg.name} (first of epoch 0), single-threaded C++ oracle "
                              f"sample+gather ({'FILE-tier rows by buffered pread, ' if file_cfg else ''}"
                              f"{'other rows from the canonical host table' if table is not None else 'rows by pread from the feature file'}), "
-                             f"{r['seconds']:.1f}s",
-                   "feature_gbs": round(r["gbs"], 3)}
+                             f"{r['seconds']:.1f}s; P-core leg: the same oracle on {P} threads, one independent batch "
+                             f"per thread at a time, {rP['batches']} batches in {rP['seconds']:.1f}s",
+                   "feature_gbs": round(r["gbs"], 3), "cores_P": P, "value_P": round(rP["value"], 4),
+                   "feature_gbs_P": round(rP["gbs"], 3), "cpu_model": cpu_model()}
 
     # ---- roofline of the dominant kernel (lookup+gather, K3/K4) ----
-    probe = None
-    if S > 0 and not args.profile:   # the host link's random-row ceiling for K4 (fresh uniform rows, alone)
+    probe = link_probe = lists_alone = None
+    if S > 0 and not args.profile:
         n_probe, reps = 1 << 18, 8
+        # (1) independent ceiling: a loads-only microkernel that is not K4 (best of 4 in-flight depths)
+        l_ms, l_depth = H.helios_cache_probe_link(c, n_probe, seed=11, reps=4)
+        link_probe = {"Mrows_s": round(n_probe / l_ms / 1e3, 2), "gbs": round(n_probe * cfg.R / l_ms / 1e6, 2),
+                      "how": f"helios_cache_probe_link: loads-only microkernel (not K4), {n_probe} uniformly random "
+                             f"host-tier rows per launch, fresh rows every launch, best of 8 grid x loads-in-flight "
+                             f"settings (best: ~{l_depth} rows in flight)"}
+        # (2) K4's own host part on uniform random rows (the round-1 probe; kept for comparison)
         p_ms = H.helios_cache_probe_host(c, n_probe, seed=7, reps=reps)
         probe = {"Mrows_s": round(n_probe / p_ms / 1e3, 2), "gbs": round(n_probe * cfg.R / p_ms / 1e6, 2),
                  "how": f"helios_cache_probe_host: K4 host part alone, {n_probe} uniformly random host-tier rows per "
                         f"launch, fresh rows each of {reps} launches (no L2 reuse)"}
+        # (3) the real lists alone: K3+K4 (helios_gather) on the first sampled batches of the run, one at
+        # a time on an otherwise idle GPU (no concurrent sampling), device-timed
+        blkA, featsA, statsA = plan.outputs[0]
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot_ms, tot_host, tot_rows = 0.0, 0, 0
+        H.helios_gather(c, blkA.nodes, blkA.level_counts[L:L + 1], featsA, statsA, stream)  # workspace warm-up
+        H.helios_sync(c)
+        for i in range(min(8, args.steps)):
+            b = seq[args.warmup + i]
+            H.helios_plan_submit(plan, 0, seed_of[b], keys[b], stream)
+            H.helios_plan_wait(plan, 0, stream)
+            stream.synchronize()
+            ev0.record(stream)
+            H.helios_gather(c, blkA.nodes, blkA.level_counts[L:L + 1], featsA, statsA, stream)
+            ev1.record(stream)
+            ev1.synchronize()
+            H.helios_sync(c)
+            tot_ms += ev0.elapsed_time(ev1)
+            stt = statsA.cpu().tolist()
+            tot_host += stt[2]
+            tot_rows += int(blkA.level_counts[L].item())
+        lists_alone = {"Mrows_s_host": round(tot_host / tot_ms / 1e3, 2), "ms_per_batch": round(tot_ms / 8, 4),
+                       "host_rows_per_batch": round(tot_host / 8, 1),
+                       "how": "helios_gather (K3 + K4, host tier mode as configured) on 8 real sampled batches of the "
+                              "run, one at a time on an idle GPU, CUDA events; host rows / gather time"}
     pk = measured_peaks()
     bw_hbm = float(pk.get("hbm_gbs", HBM_PEAK_FALLBACK))
     bw_pcie = pcie_h2d_peak(torch) if rank == 0 else 0.0
@@ -644,16 +714,20 @@ def main():
                                       "sampled positions + one per node (directory), averaged over the first 16 timed "
                                       "batches (bench.sampling_accesses); sector_rate = helios_graph_probe_random "
                                       "(uniform 4 B loads over the CSR indices)"}
-    if probe is not None and n_host > 0:
+    if link_probe is not None and n_host > 0:
         got = n_host * (world * steps / (max_ms / 1e3)) / world / 1e6
-        roof["host_link"] = {"achieved_Mrows_s": round(got, 2), "random_row_ceiling": probe,
-                             "frac_of_ceiling": round(got / probe["Mrows_s"], 4),
-                             "note": "host-tier rows per second of the whole timed run vs the measured ceiling of "
-                                     "random zero-copy rows on this platform (DESIGN.md §6)"}
+        roof["host_link"] = {"achieved_Mrows_s": round(got, 2), "random_row_ceiling": link_probe,
+                             "frac_of_ceiling": round(got / link_probe["Mrows_s"], 4),
+                             "k4_host_part_uniform_rows": probe, "real_lists_alone": lists_alone,
+                             "cpu_staged_rows_per_batch": round(staged_timed / steps, 1) if args.host_staged > 0 else 0,
+                             "note": "host-tier rows per second of the whole timed run (zero-copy and staged rows) vs "
+                                     "the random zero-copy row ceiling measured by an independent loads-only kernel "
+                                     "(DESIGN.md §6); the staged share can exceed the zero-copy ceiling because host "
+                                     "threads stream it"}
     value = world * steps / (max_ms / 1e3)
     e2e_val = world * steps / e2e_s
     launches_per_step = (3 * L + 2 + 2 + ((2 if args.io_sync else 3) if c.info().file_rows > 0 else 0)
-                         + (1 if args.host_staged > 0 else 0) + (1 if plan.link else 0))
+                         + (1 if (args.host_staged > 0 and S > 0) else 0) + (1 if plan.link else 0))
     out = {
         "metric": "sampled+gathered mini-batches/sec (feature GB/s and tier-roofline fraction alongside)",
         "value": round(value, 3), "unit": "batches/s", "n_gpus": 1 if one_gpu else world, "steps": steps, "warmup": args.warmup,
@@ -668,8 +742,9 @@ def main():
                    "batch_per_rank": cfg.B, "fanouts": cfg.fanouts, "hbm_rows_per_gpu": Hr, "host_rows": S,
                    "scale": s, "parallelism": f"dp{world} (seeds split per rank, HBM tier sharded)",
                    "host_tier": ("alias of canonical table (by id)" if args.host_alias else "packed, hot-rank order")
-                   + (f"; {args.host_staged:.0%} of host rows staged by {args.stage_workers} host threads"
-                      if args.host_staged > 0 else "; GPU zero-copy reads"),
+                   + (f"; dynamic split: GPU zero-copy from the front of each batch's host list, {args.stage_workers} "
+                      f"host stager threads from its end (cap {args.host_staged:.0%})"
+                      if args.host_staged > 0 else "; GPU zero-copy reads only (ablation)"),
                    "batches_in_flight": depth, "cuda_graphs": not args.no_graph, "serial_gather": bool(args.serial_gather),
                    "link_stream": bool(plan.link),
                    "intra_batch_pipeline": bool(args.intra),
@@ -681,6 +756,7 @@ def main():
         "stage_ms": {"sample": round(statistics.mean(sample_ms), 4), "gather": round(g_ms, 4),
                      "link_host_kernel": round(statistics.mean(link_ms), 4) if link_ms else None,
                      "note": f"mean per batch, device events around the two graph segments of every timed batch ({n_timed}), {depth} batches in flight"},
+        "lookups_per_s": round(world * nL * steps / (max_ms / 1e3)),
         "rows_per_batch": {"n_L": round(nL, 1), "hbm_local": round(n_local, 1), "hbm_peer": round(n_peer, 1),
                            "host": round(n_host, 1), "file": round(n_file, 1)},
         "roofline": roof,
@@ -752,7 +828,8 @@ def reference_arm(args, cfg, rank, world):
                    "batch_per_rank": cfg.B, "fanouts": cfg.fanouts},
         "feature_gbs": round(rows * cfg.R / dt / 1e9, 3),
         "cpu_baseline": {"value": round(v, 4), "unit": "batches/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{args.steps} full batches of {cfg.name}, single-threaded C++ oracle"},
+                         "sample": f"{args.steps} full batches of {cfg.name}, single-threaded C++ oracle",
+                         "cpu_model": cpu_model()},
         "e2e": {"value": round(v, 4), "unit": "batches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "setup_s": {"inputs": round(gen_s, 1)},
     }), flush=True)

@@ -155,8 +155,11 @@ helios_status helios_presample(helios_graph* g, const int64_t* seeds, int64_t n_
 #define HELIOS_CACHE_NO_DIRECT_IO 0x4u   /* open feature_path without O_DIRECT                    */
 #define HELIOS_CACHE_HOST_FILL 0x8u      /* fill the caller-provided host_tier (else assumed filled) */
 #define HELIOS_CACHE_HOST_TIER_MAPPED 0x10u /* caller-provided host_tier already registered + mapped */
-#define HELIOS_CACHE_HOST_STAGED 0x20u  /* split host-tier rows: a share is copied by host stager threads into
-                                           a contiguous pinned staging buffer read sequentially by the GPU */
+#define HELIOS_CACHE_HOST_STAGED 0x20u  /* dynamic split of every batch's host-tier rows: the GPU reads rows
+                                           zero-copy from the front of the batch's host list while host
+                                           stager threads copy 64-row chunks from its end into a contiguous
+                                           pinned staging buffer that the GPU streams (
+                                           reading 14).  The GPU still initiates every request. */
 #define HELIOS_CACHE_IO_SYNC 0x40u      /* ablation: GIDS/BaM-style coupled IO, one warp per request does
                                            submit + completion poll + copy (§2.2)   */
 #define HELIOS_CACHE_IO_FAULT_AT 0x100u  /* test builds: IO workers fail the io_fault_at-th read  */
@@ -183,7 +186,8 @@ typedef struct {
                                  the library iff HELIOS_CACHE_HOST_FILL; registered unless HOST_TIER_MAPPED.
                                  NULL: the library allocates (pinned) and fills it.  Ignored with HOST_ALIAS. */
   int32_t stage_workers;      /* HOST_STAGED: host stager threads (0 = 8)                                */
-  float stage_frac;           /* HOST_STAGED: share of each batch's host rows staged by the CPU (0 = 0.6) */
+  float stage_frac;           /* HOST_STAGED: cap on the share of each batch's host-row chunks the stagers
+                                 may claim (0 = 1.0: no cap beyond the 2^16-row staging buffer)       */
 } helios_cache_desc;
 
 /* Builds the directory and fills the tiers (blocking).  The HBM tier is filled from host_table
@@ -200,6 +204,7 @@ typedef struct {
   int32_t row_bytes, world_size, rank, peers_attached;
   int32_t io_rings, ring_depth, direct_io;
   int64_t io_reads;           /* file reads completed by the IO workers since build */
+  int64_t staged_rows;        /* HOST_STAGED: host-tier rows copied by the stager threads since build */
 } helios_cache_info;
 helios_status helios_cache_query(const helios_cache* c, helios_cache_info* out);
 
@@ -225,6 +230,14 @@ typedef struct {
  * rep (CUDA events around the kernel).  E_INVALID for n_rows <= 0 or reps <= 0, E_STATE without a
  * host tier.  Library-owned scratch is freed before return. */
 helios_status helios_cache_probe_host(helios_cache* c, int64_t n_rows, uint64_t seed, int32_t reps, float* ms);
+/* Measurement aid (blocking): the same ceiling measured by a kernel that is NOT K4 — a loads-only
+ * microkernel (no lists, no stores, no warp roles) reading n_rows uniformly random host-tier rows
+ * (fresh rows every launch), swept over 8 settings of grid size x loads in flight per thread (about
+ * 150 to 40 k rows in flight), `reps` launches each; *ms = the best mean device time per launch,
+ * *best_depth (may be NULL) = the rows in flight of that setting.
+ * E_INVALID for n_rows <= 0 or reps <= 0, E_STATE without a host tier. */
+helios_status helios_cache_probe_link(helios_cache* c, int64_t n_rows, uint64_t seed, int32_t reps, float* ms,
+                                      int32_t* best_depth);
 helios_status helios_gather(helios_cache* c, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, void* out,
                             helios_gather_stats* stats, void* stream);
 

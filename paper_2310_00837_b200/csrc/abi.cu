@@ -324,6 +324,7 @@ helios_status helios_cache_query(const helios_cache* c, helios_cache_info* o) {
   o->ring_depth = c->io.depth;
   o->direct_io = c->io.direct ? 1 : 0;
   o->io_reads = c->io.reads.load();
+  o->staged_rows = stager_rows(c);
   return HELIOS_OK;
 }
 
@@ -395,6 +396,15 @@ helios_status helios_cache_probe_host(helios_cache* c, int64_t n_rows, uint64_t 
   HCHECK(c, HELIOS_E_INVALID, "null cache");
   DeviceGuard dg(c->device);
   return probe_host_impl(c, n_rows, seed, reps, ms);
+  GUARD_END
+}
+
+helios_status helios_cache_probe_link(helios_cache* c, int64_t n_rows, uint64_t seed, int32_t reps, float* ms,
+                                      int32_t* best_depth) {
+  GUARD_BEGIN
+  HCHECK(c, HELIOS_E_INVALID, "null cache");
+  DeviceGuard dg(c->device);
+  return probe_link_impl(c, n_rows, seed, reps, ms, best_depth);
   GUARD_END
 }
 

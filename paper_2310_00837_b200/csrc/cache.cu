@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <immintrin.h>
 #include <unistd.h>
 
@@ -70,50 +71,7 @@ helios_status cache_sort_and_dir(helios_cache* c, const uint64_t* hot, int32_t* 
   return HELIOS_OK;
 }
 
-// ---- host IO workers -----------------------------------------------------------------------
-
-static void io_worker(helios_cache* c, int r) {
-  IoRings& io = c->io;
-  uint32_t next = 1;
-  int idle = 0;
-  while (!io.stop.load(std::memory_order_relaxed)) {
-    const int64_t idx = (int64_t)r * io.depth + ((next - 1u) & (uint32_t)(io.depth - 1));
-    SqEntry* e = io.sq + idx;
-    uint32_t s = __atomic_load_n(&e->seq, __ATOMIC_ACQUIRE);
-    if (s != next) {
-      if (++idle < 2000) _mm_pause();
-      else if (idle < 4000) std::this_thread::yield();
-      else usleep(50);
-      continue;
-    }
-    idle = 0;
-    const uint64_t off = e->file_off;
-    const uint32_t len = e->len;
-    const uint32_t slot = e->slot;
-    char* dst = io.staging + (int64_t)slot * io.slot_bytes;
-    int32_t status = 0;
-    int64_t k = io.read_counter.fetch_add(1) + 1;
-    if (io.fault_at > 0 && k == io.fault_at) {
-      status = HELIOS_E_IO;
-    } else {
-      uint32_t done = 0;
-      while (done < len) {
-        ssize_t got = pread(io.fd, dst + done, len - done, (off_t)(off + done));
-        if (got < 0 && errno == EINTR) continue;
-        if (got <= 0) break;
-        done += (uint32_t)got;
-      }
-      // a short read is an error only if it does not cover the row bytes
-      if (done < (uint32_t)c->R) status = HELIOS_E_IO;
-    }
-    if (status) io.host_err.store(status);
-    io.reads.fetch_add(1, std::memory_order_relaxed);
-    CqEntry* q = io.cq + idx;
-    q->status = status;
-    __atomic_store_n(&q->seq, next, __ATOMIC_RELEASE);
-    next++;
-  }
-}
+// ---- host IO workers (io_workers.cu) ------------------------------------------------------
 
 helios_status io_start(helios_cache* c, const helios_cache_desc* d) {
   IoRings& io = c->io;
@@ -238,7 +196,7 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
   c->staged = (d->flags & HELIOS_CACHE_HOST_STAGED) != 0;
   c->io_sync = (d->flags & HELIOS_CACHE_IO_SYNC) != 0;
   c->stage_workers = d->stage_workers > 0 ? d->stage_workers : 8;
-  c->stage_frac = d->stage_frac > 0.f ? std::min(d->stage_frac, 1.0f) : 0.6f;
+  c->stage_frac = d->stage_frac > 0.f ? std::min(d->stage_frac, 1.0f) : 1.0f;
   const int64_t V = c->V;
   // clamp tiers to V
   const int64_t GH = std::min<int64_t>((int64_t)c->G * c->H, V);
@@ -325,7 +283,19 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
           }
         }
       } else {
-        HCUDA(cudaHostAlloc(&c->host_tier, tier_bytes, cudaHostAllocMapped));
+        // anonymous memory with transparent huge pages, then pinned + mapped: the GPU reads it
+        // zero-copy, and the host stagers' random row copies (HOST_STAGED) take 2 MB TLB entries
+        // instead of a 4 KB page walk per row over the 51 GB tier
+        void* m = mmap(nullptr, tier_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        HCHECK(m != MAP_FAILED, HELIOS_E_NOMEM, "mmap of the host tier (%zu B) failed", tier_bytes);
+        madvise(m, tier_bytes, MADV_HUGEPAGE);
+        cudaError_t e = cudaHostRegister(m, tier_bytes, cudaHostRegisterMapped);
+        if (e != cudaSuccess) {
+          munmap(m, tier_bytes);
+          cudaGetLastError();
+          return fail(HELIOS_E_NOMEM, "cudaHostRegister(host tier, %zu B): %s", tier_bytes, cudaGetErrorString(e));
+        }
+        c->host_tier = (char*)m;
         c->host_owned = true;
       }
       HCUDA(cudaHostGetDevicePointer((void**)&c->d_host_tier, c->host_tier, 0));
@@ -376,6 +346,8 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
      // other batches' sampling); HBM-only caches are bandwidth bound and want more warps in flight
     int per_sm = (c->S > 0) ? 1 : 2;
     if (const char* e = getenv("HELIOS_GATHER_CTAS_PER_SM")) per_sm = std::max(1, std::min(atoi(e), 4));
+    if (const char* e = getenv("HELIOS_GATHER_BULK")) c->gather_bulk = atoi(e) != 0;
+    if (c->gather_bulk) per_sm = 1;  // 192 KB of shared memory per CTA
     c->gather_ctas = c->sms * per_sm;
   }
   c->staged = c->staged && c->S > 0;
@@ -394,7 +366,10 @@ void cache_free_impl(helios_cache* c) {
   for (int r = 0; r < HELIOS_MAX_RANKS; r++)
     if (r != c->rank && c->peer_ptrs[r]) cudaIpcCloseMemHandle(c->peer_ptrs[r]);
   if (c->host_registered) cudaHostUnregister((void*)c->host_table);
-  if (c->host_owned && c->host_tier) cudaFreeHost(c->host_tier);
+  if (c->host_owned && c->host_tier) {
+    cudaHostUnregister(c->host_tier);
+    munmap(c->host_tier, (size_t)c->S * c->R);
+  }
   if (c->host_tier_registered) cudaHostUnregister(c->host_tier);
   if (c->hbm) cudaFree(c->hbm);
   if (c->dir) cudaFree(c->dir);

@@ -27,10 +27,12 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
   return r;
 }
 
-// Base pointers of the four tier lists (the host list is in pinned memory in staged mode).
+// Base pointers of the four tier lists (device memory).  In staged mode the host list's directory
+// words are mirrored into pinned memory (host_w_mirror) for the host stager threads.
 struct ListPtrs {
   int64_t* i[kLists];
   uint64_t* w[kLists];
+  uint64_t* host_w_mirror;
 };
 
 // K3: one thread per row of N_L: dir[v] -> tier list (local HBM / peer HBM / host / file), appended
@@ -74,6 +76,7 @@ __global__ void __launch_bounds__(256) k_lookup(const int64_t* __restrict__ node
           const int64_t pos = (int64_t)b + __popc(m & ((1u << lane) - 1u));
           L.i[q][pos] = i;
           L.w[q][pos] = w;
+          if (q == kListHost && L.host_w_mirror) L.host_w_mirror[pos] = w;
         }
       }
     }
@@ -84,22 +87,17 @@ __device__ __forceinline__ void st_release_sys_u32_(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Staged mode: split this batch's host rows between the zero-copy path [0, n_gpu) and the host
-// stagers [n_gpu, n_host), then post the mailbox {seq, n_host, n_gpu, n_stage} (release, system).
-__global__ void k_stage_publish(unsigned long long* ctl, uint32_t* seq_ctr, uint32_t* mail, float frac,
-                                int64_t stage_cap) {
+// Staged mode (dynamic split): post the batch's mailbox {seq, n_host} (release,
+// system scope) for the host stagers, which then claim 64-row chunks of the host list from its END
+// while the GPU's host-row warps take rows from its FRONT (host_rows_dyn).
+__global__ void k_stage_publish(unsigned long long* ctl, uint32_t* seq_ctr, uint32_t* mail) {
   pdl_wait();
   pdl_trigger();
   const int64_t n_host = (int64_t)ctl[kListHost];
-  const int64_t n_stage = min((int64_t)((double)n_host * frac), stage_cap);
-  const int64_t n_gpu = n_host - n_stage;
   const uint32_t seq = *seq_ctr + 1u;
   *seq_ctr = seq;
-  ctl[kCtlStageGpu] = (unsigned long long)n_gpu;
   ctl[kCtlStageSeq] = seq;
   mail[1] = (uint32_t)n_host;
-  mail[2] = (uint32_t)n_gpu;
-  mail[3] = (uint32_t)n_stage;
   __threadfence_system();
   st_release_sys_u32_(&mail[0], seq);
 }
@@ -113,8 +111,9 @@ struct GatherArgs {
   int host_warps;           // kPartAll: zero-copy host-row warps per 8 warps
   bool staged;
   bool accumulate;          // intra-batch passes: add this pass's row counts to stats
-  const char* stage;        // device alias of the pinned staging rows
-  const uint32_t* done;     // device alias of the per-chunk completion flags
+  const char* stage;        // device alias of the pinned staging rows (chunk k from the list's end at row 64k)
+  const unsigned long long* chunk;  // device alias of the per-chunk state words ((seq << 2) | CLAIMED / DONE)
+  unsigned long long* hint; // device alias of the pinned front hint ((seq << 32) | chunk the GPU reached)
   int* err;
   const char* hbm;          // this rank's shard
   char* const* peers;       // device [G]
@@ -167,52 +166,148 @@ __device__ __forceinline__ void copy_rows(const GatherArgs& a, int q, int64_t j0
 // 16-byte vectors over its 32 lanes x VU registers (vector f -> row f / nvec, column f % nvec), so
 // every lane is busy whatever the row size (R = 400 B: 25 vectors per row, 10 rows = 250 of 256
 // slots) and each lane has VU independent loads in flight before its stores.  Lanes < rw resolve
-// one row's source / destination pointers; the others get them by shuffle.  rw = max(1, 32*VU/nvec);
-// rows longer than 32*VU vectors take several passes.  inv = ceil(2^20 / nvec) (exact division for
+// one row's source / destination pointers (list entry -> tier slot) and the others get them by
+// shuffle; the list entries of the warp's NEXT group are loaded before this group's rows, so the
+// list-read latency overlaps the row loads instead of preceding them.  rw = max(1, 32*VU/nvec); rows
+// longer than 32*VU vectors take several passes.  inv = ceil(2^20 / nvec) (exact division for
 // f * nvec < 2^20, which holds whenever rw > 1).
 template <int VU>
-__device__ __forceinline__ void copy_rows_flat(const GatherArgs& a, int q, int64_t j0, int64_t cnt, int lane, int nvec,
-                                               int rw, uint32_t inv) {
+__device__ __forceinline__ void flat_rows(const GatherArgs& a, int q, int64_t cnt, int64_t dw, int64_t n_dw, int lane,
+                                          int nvec) {
+  const int rw = max(1, 32 * VU / nvec);
+  const uint32_t inv = ((1u << 20) + (uint32_t)nvec - 1u) / (uint32_t)nvec;
+  const int64_t step = n_dw * rw;
+  int64_t j0 = dw * rw;
+  if (j0 >= cnt) return;
+  const uint64_t* __restrict__ lw = a.L.w[q];
+  const int64_t* __restrict__ li = a.L.i[q];
+  auto resolve = [&](int64_t j, const char** sp, char** dp) {
+    if (lane < rw && j + lane < cnt) {
+      const uint64_t w = lw[j + lane];
+      const char* base = q == kListLocal ? a.hbm : a.peers[(w >> 56) & 63];
+      *sp = base + (int64_t)(w & ((1ull << 56) - 1)) * a.R;
+      *dp = a.out + li[j + lane] * (int64_t)a.R;
+    }
+  };
   const char* sp = nullptr;
   char* dp = nullptr;
-  if (lane < rw && j0 + lane < cnt) {
-    const uint64_t w = a.L.w[q][j0 + lane];
-    const int64_t slot = (int64_t)(w & ((1ull << 56) - 1));
-    const char* base = q == kListLocal ? a.hbm : a.peers[(w >> 56) & 63];
-    sp = base + slot * a.R;
-    dp = a.out + a.L.i[q][j0 + lane] * (int64_t)a.R;
+  resolve(j0, &sp, &dp);
+  for (; j0 < cnt; j0 += step) {
+    const char* sp_n = nullptr;
+    char* dp_n = nullptr;
+    if (j0 + step < cnt) resolve(j0 + step, &sp_n, &dp_n);  // next group's list entries, in flight now
+    const int nrows = (int)min((int64_t)rw, cnt - j0);
+    const int nv = nrows * nvec;
+    for (int b0 = 0; b0 < nv; b0 += 32 * VU) {
+      int4 r[VU];
+#pragma unroll
+      for (int k = 0; k < VU; k++) {
+        const int f = b0 + lane + 32 * k;
+        const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
+        const char* src = (const char*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)sp, row);
+        if (f < nv) r[k] = ld_stream((const int4*)src + (f - row * nvec));
+      }
+#pragma unroll
+      for (int k = 0; k < VU; k++) {
+        const int f = b0 + lane + 32 * k;
+        const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
+        char* dst = (char*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)dp, row);
+        if (f < nv) ((int4*)dst)[f - row * nvec] = r[k];
+      }
+    }
+    sp = sp_n;
+    dp = dp_n;
   }
-  const int nrows = (int)min((int64_t)rw, cnt - j0);
-  const int nv = nrows * nvec;
-  for (int b0 = 0; b0 < nv; b0 += 32 * VU) {
-    int4 r[VU];
-#pragma unroll
-    for (int k = 0; k < VU; k++) {
-      const int f = b0 + lane + 32 * k;
-      const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
-      const char* s = (const char*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)sp, row);
-      if (f < nv) r[k] = ld_stream((const int4*)s + (f - row * nvec));
+}
+
+// ---- bulk-copy (TMA engine) variant of the HBM / peer row copy (HELIOS_GATHER_BULK=1) ----------
+// Rows move global -> shared -> global with cp.async.bulk (SASS UBLKCP): no register staging, and up
+// to kBulkWarpBytes per warp in flight per direction.  Lane l of a warp owns row slot l of each of
+// the warp's two shared-memory stages: it issues that row's bulk load (completing on the stage's
+// mbarrier, armed with the group's byte count by lane 0) and, once the mbarrier phase completes,
+// the row's bulk store; the stage is reloaded only after the lane's own earlier store finished
+// reading it (cp.async.bulk.wait_group.read).  Loads of group g+1 overlap the stores of group g.
+constexpr int kBulkWarpBytes = 12 * 1024;   // per stage; 8 warps x 2 stages = 192 KB per CTA
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Rows of list q in groups of G = min(32, kBulkWarpBytes / R); this warp takes groups dw, dw + n_dw, ...
+__device__ __forceinline__ void bulk_rows(const GatherArgs& a, int q, int64_t cnt, int64_t dw, int64_t n_dw, int lane,
+                                          char* stage0, uint64_t* bars, uint32_t* phase) {
+  const int G = max(1, min(32, kBulkWarpBytes / a.R));
+  const int64_t ngroups = (cnt + G - 1) / G;
+  int64_t g = dw;
+  if (g >= ngroups) return;
+  auto issue = [&](int64_t grp, int st) {
+    const int64_t j = grp * G + lane;
+    const int n = (int)min((int64_t)G, cnt - grp * G);
+    if (lane == 0) mbar_expect_tx(bars + st, (uint32_t)(n * a.R));
+    __syncwarp();
+    if (lane < n) {
+      const uint64_t w = a.L.w[q][j];
+      const char* base = q == kListLocal ? a.hbm : a.peers[(w >> 56) & 63];
+      bulk_load(stage0 + (size_t)st * kBulkWarpBytes + lane * a.R, base + (int64_t)(w & ((1ull << 56) - 1)) * a.R,
+                (uint32_t)a.R, bars + st);
     }
-#pragma unroll
-    for (int k = 0; k < VU; k++) {
-      const int f = b0 + lane + 32 * k;
-      const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
-      char* d = (char*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)dp, row);
-      if (f < nv) ((int4*)d)[f - row * nvec] = r[k];
+  };
+  int st = 0;
+  issue(g, 0);
+  for (; g < ngroups; g += n_dw) {
+    const int64_t nxt = g + n_dw;
+    if (nxt < ngroups) {
+      bulk_wait_read0();  // this lane's store from stage st^1 has finished reading it
+      __syncwarp();
+      issue(nxt, st ^ 1);
     }
+    mbar_wait(bars + st, phase[st]);
+    phase[st] ^= 1u;
+    const int n = (int)min((int64_t)G, cnt - g * G);
+    if (lane < n)
+      bulk_store(a.out + a.L.i[q][g * G + lane] * (int64_t)a.R, stage0 + (size_t)st * kBulkWarpBytes + lane * a.R,
+                 (uint32_t)a.R);
+    bulk_commit();
+    st ^= 1;
   }
 }
 
 // K4: warp-specialised gather.
-//   kPartAll (one kernel, every tier): when the host list is non-empty one warp in 8 serves host
-//     rows (zero-copy over PCIe; in staged mode a second warp in 8 consumes staged chunks) while the
+//   kPartAll (one kernel, every tier): when the host list is non-empty one warp in 8 (two in staged
+//     mode) serves host rows (zero-copy over PCIe, or the dynamic zero-copy / staged split) while the
 //     others copy peer (NVLink) then local HBM rows.
 //   kPartHbm: every warp copies peer then local rows (link mode, slot stream).
-//   kPartHost: every warp serves host rows (link mode: the plan's link stream; staged mode: odd
-//     warps consume staged chunks).
-// Host rows and staged chunks are taken by ticket (UH rows per grab), not by a static split: CTAs
-// that become resident late (SMs busy with other batches' sampling) then take less work instead of
-// stretching the tail of the link transfer.
+//   kPartHost: every warp serves host rows (link mode: the plan's link stream).
+// Host rows are taken by ticket (UH rows per grab), not by a static split: CTAs that become resident
+// late (SMs busy with other batches' sampling) then take less work instead of stretching the tail of
+// the link transfer.
 __device__ __forceinline__ uint32_t ld_acquire_sys_u32_(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -234,49 +329,105 @@ __device__ __forceinline__ int64_t warp_ticket(unsigned long long* ctr, int n, i
   return (int64_t)__shfl_sync(0xFFFFFFFFu, t, 0);
 }
 
-// Zero-copy host rows [0, n_gpu), UH rows per ticket.
+// Zero-copy host rows [0, n), UH rows per ticket.
 template <int VPL, int UH>
-__device__ __forceinline__ void host_rows(const GatherArgs& a, int64_t n_gpu, int lane, int nvec) {
+__device__ __forceinline__ void host_rows(const GatherArgs& a, int64_t n, int lane, int nvec) {
   for (;;) {
     const int64_t j0 = warp_ticket(&a.ctl[kCtlHostTicket], UH, lane);
-    if (j0 >= n_gpu) break;
-    copy_rows<VPL, UH>(a, kListHost, j0, n_gpu, lane, nvec);
+    if (j0 >= n) break;
+    copy_rows<VPL, UH>(a, kListHost, j0, n, lane, nvec);
   }
 }
 
-// Staged host rows [n_gpu, n_host): one chunk per ticket, polled until its host stager published it.
-__device__ __forceinline__ bool staged_rows(const GatherArgs& a, int64_t n_gpu, int64_t n_stage, int lane, int nvec) {
-  const uint32_t seq = (uint32_t)a.ctl[kCtlStageSeq];
-  const int64_t n_chunks = (n_stage + kStageChunk - 1) / kStageChunk;
-  for (;;) {
-    const int64_t ch = warp_ticket(&a.ctl[kCtlStageTicket], 1, lane);
-    if (ch >= n_chunks) break;
-    bool ok = true;
-    const uint64_t t0 = globaltimer();
-    unsigned backoff = 128;  // each poll is a PCIe read that competes with the row reads: back off
-    while (ld_acquire_sys_u32_(&a.done[ch]) != seq) {  // every lane polls (one request)
-      if (globaltimer() - t0 > kStageWatchdogNs) {
-        ok = false;
-        break;
-      }
-      __nanosleep(backoff);
-      backoff = min(backoff * 2u, 2048u);
-    }
-    if (!__all_sync(0xFFFFFFFFu, ok)) {
-      if (lane == 0) latch(a.err, HELIOS_E_TIMEOUT);
-      return false;
-    }
-    const int64_t j1 = min(n_stage, (ch + 1) * kStageChunk);
-    for (int64_t j = ch * kStageChunk; j < j1; j++) {
-      const int4* src = (const int4*)(a.stage + j * a.R);
-      int4* dst = (int4*)(a.out + a.L.i[kListHost][n_gpu + j] * (int64_t)a.R);
-      for (int k = lane; k < nvec; k += 32) dst[k] = ld_volatile_v4_(src + k);
-    }
-  }
-  return true;
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Staged mode: the GPU's host-row warps and the host stagers split the batch's host list [0, n_host)
+// dynamically, in 64-row chunks.  The warps take chunks from the front (one device-side ticket, a
+// posted write of the front hint, one relaxed system-scope read of the chunk's state word); the
+// stagers claim chunks from the back (state = seq|CLAIMED), copy the rows into the contiguous pinned
+// staging buffer and publish them (state = seq|DONE, release).  A published chunk is streamed from
+// staging (one acquire orders the rows after the state word); a claimed one is waited for up to
+// kStageStealNs and then copied zero-copy by the GPU itself; an unclaimed one is read zero-copy
+// right away.  So the CPU's share is what it claims before the GPU's front arrives (capped by
+// stage_frac), and a slow or descheduled stager costs at most the steal timeout.  A chunk both sides
+// copy is copied twice (identical bytes; the staged copy is unused): no exclusivity is needed, only
+// "every row by at least one side", and the GPU alone decides which rows it still has to copy.  The
+// list the warps read is in device memory; the stagers read its pinned mirror.
+constexpr uint64_t kStageStealNs = 100000;
 template <int VPL, int UH>
+__device__ __forceinline__ void host_rows_dyn(const GatherArgs& a, int64_t n_host, int lane, int nvec) {
+  const uint32_t seq = (uint32_t)a.ctl[kCtlStageSeq];
+  const unsigned long long claimed = ((unsigned long long)seq << 2) | kChunkClaimed;
+  const unsigned long long done = ((unsigned long long)seq << 2) | kChunkDone;
+  const int64_t n_chunks = (n_host + kStageChunk - 1) / kStageChunk;
+  for (;;) {
+    const int64_t j0 = warp_ticket(&a.ctl[kCtlHostTicket], kStageChunk, lane);
+    if (j0 >= n_host) break;
+    const int64_t c = j0 / kStageChunk;
+    const int64_t j1 = min(n_host, j0 + kStageChunk);
+    unsigned long long st = 0;
+    if (lane == 0) {
+      st_relaxed_sys_u64(a.hint, ((unsigned long long)seq << 32) | (unsigned long long)c);
+      st = ld_relaxed_sys_u64(&a.chunk[c]);
+      if (st == claimed) {  // a stager is copying it: wait a bounded time, then take it back
+        const uint64_t t0 = globaltimer();
+        unsigned backoff = 256;
+        while (st == claimed && globaltimer() - t0 < kStageStealNs) {
+          __nanosleep(backoff);
+          backoff = min(backoff * 2u, 4096u);
+          st = ld_relaxed_sys_u64(&a.chunk[c]);
+        }
+      }
+      if (st == done) (void)ld_acquire_sys_u64(&a.chunk[c]);  // orders the staged rows after the state word
+    }
+    st = __shfl_sync(0xFFFFFFFFu, st, 0);
+    if (st != done) {  // not staged: read the chunk's rows zero-copy
+      for (int64_t j = j0; j < j1; j += UH) copy_rows<VPL, UH>(a, kListHost, j, j1, lane, nvec);
+      continue;
+    }
+    __syncwarp();
+    // chunk c is staged at chunk position n_chunks - 1 - c of the staging buffer, rows contiguous
+    const char* sbase = a.stage + (n_chunks - 1 - c) * kStageChunk * (int64_t)a.R;
+    for (int64_t j = j0; j < j1; j += UH) {
+      int4 r[UH][VPL];
+#pragma unroll
+      for (int u = 0; u < UH; u++)
+        if (j + u < j1) {
+#pragma unroll
+          for (int k = 0; k < VPL; k++) {
+            const int idx = lane + 32 * k;
+            if (idx < nvec) r[u][k] = ld_volatile_v4_((const int4*)(sbase + (j + u - j0) * (int64_t)a.R) + idx);
+          }
+        }
+#pragma unroll
+      for (int u = 0; u < UH; u++)
+        if (j + u < j1) {
+          int4* dst = (int4*)(a.out + a.L.i[kListHost][j + u] * (int64_t)a.R);
+#pragma unroll
+          for (int k = 0; k < VPL; k++) {
+            const int idx = lane + 32 * k;
+            if (idx < nvec) dst[idx] = r[u][k];
+          }
+        }
+    }
+  }
+}
+
+// HOST = false: the instantiation for caches without a host tier (no host-row code, so the HBM copy
+// loop alone sets the register budget).
+template <int VPL, int UH, bool BULK, bool HOST>
 __global__ void __launch_bounds__(256, 2) k_gather_lists(GatherArgs a) {
   pdl_wait();
   pdl_trigger();
@@ -287,11 +438,9 @@ __global__ void __launch_bounds__(256, 2) k_gather_lists(GatherArgs a) {
   const int nvec = a.R >> 4;
   const int64_t n_local = (int64_t)a.ctl[kListLocal], n_peer = (int64_t)a.ctl[kListPeer],
                 n_host = (int64_t)a.ctl[kListHost];
-  const int64_t n_gpu = a.staged ? (int64_t)a.ctl[kCtlStageGpu] : n_host;
-  const int64_t n_stage = n_host - n_gpu;
-  if (a.part == kPartHost) {
-    if (a.staged && (gw & 1)) staged_rows(a, n_gpu, n_stage, lane, nvec);
-    else host_rows<VPL, UH>(a, n_gpu, lane, nvec);
+  if (HOST && a.part == kPartHost) {
+    if (a.staged) host_rows_dyn<VPL, UH>(a, n_host, lane, nvec);
+    else host_rows<VPL, UH>(a, n_host, lane, nvec);
     return;
   }
   if (a.stats && gw == 0 && lane == 0) {
@@ -306,22 +455,37 @@ __global__ void __launch_bounds__(256, 2) k_gather_lists(GatherArgs a) {
     }
     a.stats->rows_file = (int64_t)a.ctl[kListFile];  // the file list accumulates over passes
   }
-  // kPartAll warp roles: r = gw % 8.  r == 0: zero-copy host rows; r == 1 (staged mode): stage
-  // consumers; other warps: peer then local HBM rows.
-  const int nspecial = (a.part == kPartAll && n_host > 0) ? (a.staged ? 1 : 0) + a.host_warps : 0;
+  // kPartAll warp roles: r = gw % 8.  r < host_warps: host rows (zero-copy, or the dynamic
+  // zero-copy / staged split); other warps: peer then local HBM rows.
+  const int nspecial = (HOST && a.part == kPartAll && n_host > 0) ? a.host_warps : 0;
   const int r = (int)(gw & 7);
-  if (r < nspecial) {
-    if (r < a.host_warps) host_rows<VPL, UH>(a, n_gpu, lane, nvec);
-    else staged_rows(a, n_gpu, n_stage, lane, nvec);
+  if (HOST && r < nspecial) {
+    if (a.staged) host_rows_dyn<VPL, UH>(a, n_host, lane, nvec);
+    else host_rows<VPL, UH>(a, n_host, lane, nvec);
     return;
   }
   const int64_t dw = (gw >> 3) * (8 - nspecial) + (r - nspecial);  // index among data warps
   const int64_t n_dw = (nw >> 3) * (8 - nspecial);
-  constexpr int VU = 8;
-  const int rw = max(1, 32 * VU / nvec);
-  const uint32_t inv = ((1u << 20) + (uint32_t)nvec - 1u) / (uint32_t)nvec;
-  for (int64_t j0 = dw * rw; j0 < n_peer; j0 += n_dw * rw) copy_rows_flat<VU>(a, kListPeer, j0, n_peer, lane, nvec, rw, inv);
-  for (int64_t j0 = dw * rw; j0 < n_local; j0 += n_dw * rw) copy_rows_flat<VU>(a, kListLocal, j0, n_local, lane, nvec, rw, inv);
+  if constexpr (BULK) {
+    extern __shared__ __align__(128) char bulk_smem[];
+    __shared__ uint64_t bars[8][2];
+    const int wi = threadIdx.x >> 5;
+    uint32_t phase[2] = {0u, 0u};
+    if (lane == 0) {
+      mbar_init(&bars[wi][0], 1);
+      mbar_init(&bars[wi][1], 1);
+    }
+    __syncwarp();
+    char* stage0 = bulk_smem + (size_t)wi * 2 * kBulkWarpBytes;
+    bulk_rows(a, kListPeer, n_peer, dw, n_dw, lane, stage0, bars[wi], phase);
+    bulk_wait_read0();
+    __syncwarp();
+    bulk_rows(a, kListLocal, n_local, dw, n_dw, lane, stage0, bars[wi], phase);
+    bulk_wait0();  // this lane's row stores are complete before the kernel ends
+  } else {
+    flat_rows<8>(a, kListPeer, n_peer, dw, n_dw, lane, nvec);
+    flat_rows<8>(a, kListLocal, n_local, dw, n_dw, lane, nvec);
+  }
 }
 
 // Plain row copy by id (setup: HBM-tier fill from a mapped host table).
@@ -574,17 +738,37 @@ helios_status io_preload_kernels() {
 // footprint leaves SM slots to the other in-flight batches' sampling (measured against 4 CTAs per
 // SM: C3 +6 %, C2 +6 %; 74-296 CTAs within noise on C3; 2 or 4 host warps per 8 are slower,
 // DESIGN.md §11).  HBM-only caches use c->gather_ctas CTAs (K4 grid sweep).
-template <int VPL, int UH>
-static void launch_gather(const GatherArgs& a, int grid, cudaStream_t st) {
-  launch_pdl(k_gather_lists<VPL, UH>, dim3(grid), dim3(256), st, a);
+// HELIOS_GATHER_BULK=1 (read at cache build; the bulk-copy ablation): one CTA per SM
+// with 192 KB of dynamic shared memory.
+constexpr int kBulkSmem = 8 * 2 * kBulkWarpBytes;
+
+template <int VPL, int UH, bool HOST>
+static void launch_gather(const GatherArgs& a, int grid, bool bulk, cudaStream_t st) {
+  if (bulk) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_gather_lists<VPL, UH, true, HOST>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
+      attr = true;
+    }
+    launch_pdl_smem(k_gather_lists<VPL, UH, true, HOST>, dim3(grid), dim3(256), kBulkSmem, st, a);
+  } else {
+    launch_pdl(k_gather_lists<VPL, UH, false, HOST>, dim3(grid), dim3(256), st, a);
+  }
 }
 
-static void launch_gather_any(const GatherArgs& a, int grid, cudaStream_t st) {
+template <bool HOST>
+static void launch_gather_rows(const GatherArgs& a, int grid, bool bulk, cudaStream_t st) {
   const int nvec = a.R / 16;
-  if (nvec <= 32) launch_gather<1, 8>(a, grid, st);
-  else if (nvec <= 64) launch_gather<2, 4>(a, grid, st);
-  else if (nvec <= 128) launch_gather<4, 2>(a, grid, st);
-  else launch_gather<8, 1>(a, grid, st);
+  if (nvec <= 32) launch_gather<1, 8, HOST>(a, grid, bulk, st);
+  else if (nvec <= 64) launch_gather<2, 4, HOST>(a, grid, bulk, st);
+  else if (nvec <= 128) launch_gather<4, 2, HOST>(a, grid, bulk, st);
+  else launch_gather<8, 1, HOST>(a, grid, bulk, st);
+}
+
+// host: the cache has a host tier (else the lean HBM-only instantiation)
+static void launch_gather_any(const GatherArgs& a, int grid, bool bulk, bool host, cudaStream_t st) {
+  if (host) launch_gather_rows<true>(a, grid, bulk, st);
+  else launch_gather_rows<false>(a, grid, bulk, st);
 }
 
 void gws_free(GatherWS& w) {
@@ -592,10 +776,10 @@ void gws_free(GatherWS& w) {
   if (w.d_list_i) cudaFree(w.d_list_i);
   if (w.d_list_w) cudaFree(w.d_list_w);
   if (w.d_ctl) cudaFree(w.d_ctl);
-  if (w.h_host_i) cudaFreeHost(w.h_host_i);
   if (w.h_host_w) cudaFreeHost(w.h_host_w);
   if (w.h_stage) cudaFreeHost(w.h_stage);
-  if (w.h_done) cudaFreeHost(w.h_done);
+  if (w.h_chunk) cudaFreeHost(w.h_chunk);
+  if (w.h_hint) cudaFreeHost(w.h_hint);
   if (w.h_mail) cudaFreeHost(w.h_mail);
   if (w.d_seq) cudaFree(w.d_seq);
   w = GatherWS{};
@@ -613,19 +797,22 @@ helios_status gws_ensure(helios_cache* c, GatherWS& w, int64_t max_nodes) {
   w.cap = cap;
   w.owner = c;
   if (c->staged) {
-    const int64_t chunks = kStageCapRows / kStageChunk + 1;
-    HCUDA(cudaHostAlloc(&w.h_host_i, cap * 8, cudaHostAllocMapped));
+    const int64_t chunks = (cap + kStageChunk - 1) / kStageChunk;  // state words per list chunk
+    HCHECK(chunks < 65536, HELIOS_E_CAPACITY, "staged host tier: %lld rows per batch exceed 2^22", (long long)cap);
+    w.stage_rows = std::min<int64_t>(kStageCapRows, chunks * kStageChunk);
     HCUDA(cudaHostAlloc(&w.h_host_w, cap * 8, cudaHostAllocMapped));
-    HCUDA(cudaHostAlloc(&w.h_stage, kStageCapRows * (int64_t)c->R, cudaHostAllocMapped));
-    HCUDA(cudaHostAlloc(&w.h_done, chunks * 4, cudaHostAllocMapped));
+    HCUDA(cudaHostAlloc(&w.h_stage, w.stage_rows * (int64_t)c->R, cudaHostAllocMapped));
+    HCUDA(cudaHostAlloc(&w.h_chunk, chunks * 8, cudaHostAllocMapped));
     HCUDA(cudaHostAlloc(&w.h_mail, 16, cudaHostAllocMapped));
-    memset(w.h_done, 0, chunks * 4);
+    HCUDA(cudaHostAlloc(&w.h_hint, 8, cudaHostAllocMapped));
+    memset(w.h_chunk, 0, chunks * 8);
     memset(w.h_mail, 0, 16);
-    HCUDA(cudaHostGetDevicePointer((void**)&w.d_host_i, w.h_host_i, 0));
+    memset(w.h_hint, 0, 8);
     HCUDA(cudaHostGetDevicePointer((void**)&w.d_host_w, w.h_host_w, 0));
     HCUDA(cudaHostGetDevicePointer((void**)&w.d_stage, w.h_stage, 0));
-    HCUDA(cudaHostGetDevicePointer((void**)&w.d_done, w.h_done, 0));
+    HCUDA(cudaHostGetDevicePointer((void**)&w.d_chunk, w.h_chunk, 0));
     HCUDA(cudaHostGetDevicePointer((void**)&w.d_mail, w.h_mail, 0));
+    HCUDA(cudaHostGetDevicePointer((void**)&w.d_hint, w.h_hint, 0));
     HCUDA(cudaMalloc(&w.d_seq, 4));
     HCUDA(cudaMemset(w.d_seq, 0, 4));
     helios_status st = stager_register(c, w);
@@ -641,20 +828,18 @@ static GatherArgs make_args(helios_cache* c, GatherWS& w, void* out, helios_gath
     a.L.i[q] = w.d_list_i + q * w.cap;
     a.L.w[q] = w.d_list_w + q * w.cap;
   }
-  const bool staged = c->staged && w.d_host_i;
-  if (staged) {
-    a.L.i[kListHost] = w.d_host_i;
-    a.L.w[kListHost] = w.d_host_w;
-  }
+  const bool staged = c->staged && w.d_host_w;
+  a.L.host_w_mirror = staged ? w.d_host_w : nullptr;
   a.out = (char*)out;
   a.R = c->R;
   a.ctl = w.d_ctl;
   a.part = part;
-  a.host_warps = 1;
+  a.host_warps = staged ? 2 : 1;
   a.staged = staged;
   a.accumulate = accumulate;
   a.stage = w.d_stage;
-  a.done = w.d_done;
+  a.chunk = w.d_chunk;
+  a.hint = w.d_hint;
   a.err = c->d_err;
   a.hbm = c->hbm;
   a.peers = c->d_peers;
@@ -676,14 +861,14 @@ static helios_status gather_pass(helios_cache* c, GatherWS& w, const int64_t* no
     if (!w.ctl_preset) HCUDA(cudaMemsetAsync(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long), st));
   } else {
     HCUDA(cudaMemsetAsync(w.d_ctl, 0, kListFile * sizeof(unsigned long long), st));
-    HCUDA(cudaMemsetAsync(w.d_ctl + kCtlHostTicket, 0, 2 * sizeof(unsigned long long), st));
+    HCUDA(cudaMemsetAsync(w.d_ctl + kCtlHostTicket, 0, sizeof(unsigned long long), st));
   }
   GatherArgs a = make_args(c, w, out, stats, accumulate, part);
   const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_rows + 255) / 256), (int64_t)c->sms * 2);
   launch_pdl(k_lookup, dim3(lg), dim3(256), st, nodes, lo, n_nodes, (const int64_t*)c->dir, c->V, c->rank, a.L, w.d_ctl,
              c->d_err, w.trace_params, w.trace_idx);
-  if (a.staged) launch_pdl(k_stage_publish, dim3(1), dim3(1), st, w.d_ctl, w.d_seq, w.d_mail, c->stage_frac, kStageCapRows);
-  launch_gather_any(a, c->gather_ctas, st);
+  if (a.staged) launch_pdl(k_stage_publish, dim3(1), dim3(1), st, w.d_ctl, w.d_seq, w.d_mail);
+  launch_gather_any(a, c->gather_ctas, c->gather_bulk, c->S > 0, st);
   HCUDA(cudaGetLastError());
   return HELIOS_OK;
 }
@@ -709,7 +894,7 @@ helios_status gather_hbm_launch(helios_cache* c, GatherWS& w, const int64_t* nod
 helios_status gather_host_launch(helios_cache* c, GatherWS& w, void* out, cudaStream_t st) {
   HCHECK(!c->broken, HELIOS_E_STATE, "cache unusable after an IO / staging watchdog timeout");
   const GatherArgs a = make_args(c, w, out, nullptr, false, kPartHost);
-  launch_gather_any(a, c->gather_ctas, st);
+  launch_gather_any(a, c->gather_ctas, false, true, st);
   HCUDA(cudaGetLastError());
   return HELIOS_OK;
 }
@@ -767,7 +952,7 @@ helios_status probe_host_impl(helios_cache* c, int64_t n, uint64_t seed, int32_t
       k_probe_list<<<c->sms * 4, 256, 0, st>>>(a.L.i[kListHost], a.L.w[kListHost], w.d_ctl, n, range,
                                                 seed ^ (0x5851F42D4C957F2Dull * (uint64_t)(r + 1)));
       HCUDA(cudaEventRecord(e0, st));
-      launch_gather_any(a, c->sms, st);  // the host part: one CTA per SM as in the pipeline
+      launch_gather_any(a, c->sms, false, true, st);  // the host part: one CTA per SM as in the pipeline
       HCUDA(cudaEventRecord(e1, st));
       HCUDA(cudaEventSynchronize(e1));
       float t = 0;
@@ -788,6 +973,86 @@ helios_status probe_host_impl(helios_cache* c, int64_t n, uint64_t seed, int32_t
   w = GatherWS{};
   if (s == HELIOS_OK) *ms = tot / reps;
   return s;
+}
+
+// ---- independent host-link probe (measurement; not K4) --------------------------------------------
+// Loads only: thread t of the grid reads D 16-byte vectors, vector k of the thread being vector
+// (t*D + k) mod nvec of random row (t*D + k) / nvec, rows drawn uniformly (SplitMix64 of (seed, row))
+// over the host tier; no stores, no lists, no warp roles.  D (loads in flight per thread) is swept
+// by the host together with the grid size (rows in flight) and the best rate kept, so this is the
+// ceiling of random R-byte zero-copy reads on this platform, independent of K4's code.
+template <int D>
+__global__ void k_probe_link(const char* __restrict__ host, int64_t range, int32_t R, int64_t n_rows, uint64_t seed,
+                             int* sink) {
+  const int nvec = R >> 4;
+  const int64_t total = n_rows * nvec;
+  int acc = 0;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * D; base < total;
+       base += (int64_t)gridDim.x * blockDim.x * D) {
+    int4 r[D];
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+      const int64_t f = base + k;
+      r[k] = make_int4(0, 0, 0, 0);
+      if (f < total) {
+        const int64_t row = f / nvec;
+        uint64_t z = seed + 0x9E3779B97F4A7C15ull * (uint64_t)(row + 1);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const int64_t slot = (int64_t)__umul64hi(z, (uint64_t)range);
+        r[k] = ld_stream((const int4*)(host + slot * R) + (f - row * nvec));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < D; k++) acc ^= r[k].x ^ r[k].w;
+  }
+  if (acc == 0x7FFFFFFF) *sink = acc;
+}
+
+helios_status probe_link_impl(helios_cache* c, int64_t n, uint64_t seed, int32_t reps, float* ms, int32_t* best_depth) {
+  HCHECK(n > 0 && reps > 0 && ms, HELIOS_E_INVALID, "probe: n_rows %lld, reps %d", (long long)n, reps);
+  HCHECK(c->S > 0 && c->d_host_tier, HELIOS_E_STATE, "probe: the cache has no host tier");
+  const int64_t range = (c->flags & HELIOS_CACHE_HOST_ALIAS) ? c->V : c->S;
+  int* sink = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  HCUDA(cudaMalloc(&sink, sizeof(int)));
+  HCUDA(cudaEventCreate(&e0));
+  HCUDA(cudaEventCreate(&e1));
+  float best = 1e30f;
+  int bd = 0;
+  uint64_t salt = seed;
+  cudaError_t err = cudaSuccess;
+  // rows in flight = threads * d / nvec: swept from ~150 to ~40 k rows (random zero-copy rows slow down
+  // when far too many are outstanding, so the sweep covers both sides of the optimum)
+  const int nvec = c->R / 16;
+  for (int cfg = 0; cfg < 8; cfg++) {
+    const int d = (cfg & 1) ? 8 : 2;
+    const int grid_c = std::max(1, (c->sms / 4) << (cfg >> 1));  // 37, 74, 148, 296 CTAs (B200)
+    float tot = 0;
+    for (int r = 0; r < reps && err == cudaSuccess; r++) {
+      salt = salt * 0x5851F42D4C957F2Dull + 0x14057B7EF767814Full;  // fresh rows every launch (no L2 reuse)
+      cudaEventRecord(e0, 0);
+      if (d == 2) k_probe_link<2><<<grid_c, 256>>>(c->d_host_tier, range, c->R, n, salt, sink);
+      else k_probe_link<8><<<grid_c, 256>>>(c->d_host_tier, range, c->R, n, salt, sink);
+      cudaEventRecord(e1, 0);
+      err = cudaEventSynchronize(e1);
+      float t = 0;
+      if (err == cudaSuccess) err = cudaEventElapsedTime(&t, e0, e1);
+      tot += t;
+    }
+    if (err == cudaSuccess && tot / reps < best) {
+      best = tot / reps;
+      bd = (int)((int64_t)grid_c * 256 * d / std::max(1, nvec));  // rows in flight of the best setting
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  if (err != cudaSuccess) return fail(HELIOS_E_CUDA, "probe_link: %s", cudaGetErrorString(err));
+  *ms = best;
+  if (best_depth) *best_depth = bd;
+  return HELIOS_OK;
 }
 
 // K5 / K6 on the cache's IO streams for the misses recorded in w by the preceding gather_launch on

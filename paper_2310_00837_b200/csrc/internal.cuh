@@ -66,6 +66,21 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, c
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl_smem(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                   Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // empty hash key / unassigned local id / no minpos
 constexpr int kScanBlock = 256;
@@ -107,6 +122,8 @@ struct SampleWS {
   char* scan_base = nullptr;
   size_t scan_bytes = 0;
   unsigned* bar = nullptr;      // persistent-sampler grid barrier {arrivals, generation} (in the scan region)
+  int cluster = 0;              // > 0: the whole batch in one launch of a cluster of this many CTAs
+                                // (HELIOS_SAMPLE_MODE=cluster|cluster16|chain)
   bool persistent = false;      // one cooperative kernel per batch instead of the 2+3L-kernel chain
                                 // (HELIOS_SAMPLE_PERSISTENT=1; measured slower)
   // per-batch parameters, read by the kernels from device memory so that a captured CUDA graph
@@ -120,12 +137,12 @@ struct SampleWS {
 // Per-gather bookkeeping (one per gather context): per-tier work lists written by the lookup
 // kernel, and the ticket / count words shared with the gather and IO kernels.
 enum : int { kListLocal = 0, kListPeer = 1, kListHost = 2, kListFile = 3, kLists = 4 };
-enum : int { kCtlSubmit = 4, kCtlComplete = 5, kCtlStageGpu = 6, kCtlStageSeq = 7, kCtlHostTicket = 8,
-             kCtlStageTicket = 9, kCtlWords = 10 };
+enum : int { kCtlSubmit = 4, kCtlComplete = 5, kCtlStageSeq = 6, kCtlHostTicket = 7, kCtlWords = 8 };
 // Which rows a k_gather_lists launch copies: every tier (one kernel), only the HBM tiers (local +
 // peer), or only the host tier (zero-copy + staged rows; the plan's link stream).
 enum : int { kPartAll = 0, kPartHbm = 1, kPartHost = 2 };
-constexpr int kStageChunk = 64;              // rows per staging chunk (one completion flag each)
+constexpr int kStageChunk = 64;              // rows per staging chunk (one state word each)
+constexpr unsigned long long kChunkClaimed = 1, kChunkDone = 2;  // chunk state word: (seq << 2) | state
 constexpr int64_t kStageCapRows = 1 << 16;   // staged rows per batch at most (the rest: zero-copy)
 struct StageCtx;
 struct Stager;
@@ -134,19 +151,21 @@ struct GatherWS {
   int64_t* d_list_i = nullptr;          // [kLists * cap] output row of each entry
   uint64_t* d_list_w = nullptr;         // [kLists * cap] directory word of each entry
   unsigned long long* d_ctl = nullptr;  // [kCtlWords]: counts per list, IO tickets, staging split
-  // HELIOS_CACHE_HOST_STAGED: the host list lives in pinned memory (host stager threads read it),
-  // rows [n_gpu, n_host) are copied by the stagers into a contiguous pinned buffer, chunk by chunk.
+  // HELIOS_CACHE_HOST_STAGED: the host list's directory words are mirrored into pinned memory for the
+  // host stager threads, which copy 64-row chunks claimed from the list's end into a contiguous
+  // pinned buffer.
   helios_cache* owner = nullptr;
-  int64_t* h_host_i = nullptr;          // pinned [cap] (device alias d_host_i)
-  uint64_t* h_host_w = nullptr;         // pinned [cap] (device alias d_host_w)
-  int64_t* d_host_i = nullptr;
-  uint64_t* d_host_w = nullptr;
-  char* h_stage = nullptr;              // pinned [kStageCapRows, R]
+  uint64_t* h_host_w = nullptr;         // pinned [cap] mirror of the host list's directory words (the
+  uint64_t* d_host_w = nullptr;         //   stagers read it; device alias d_host_w, written by k_lookup)
+  char* h_stage = nullptr;              // pinned [stage_rows, R]: chunk k from the list's end at row 64k
   char* d_stage = nullptr;
-  uint32_t* h_done = nullptr;           // pinned [chunks]: batch sequence of each finished chunk
-  uint32_t* d_done = nullptr;
-  uint32_t* h_mail = nullptr;           // pinned {seq, n_host, n_gpu, n_stage}, published by the GPU
+  int64_t stage_rows = 0;
+  unsigned long long* h_chunk = nullptr;  // pinned [chunks]: (seq << 2) | kChunkClaimed / kChunkDone
+  unsigned long long* d_chunk = nullptr;
+  uint32_t* h_mail = nullptr;           // pinned {seq, n_host, -, -}, published by the GPU
   uint32_t* d_mail = nullptr;
+  unsigned long long* h_hint = nullptr; // pinned (seq << 32) | chunk the GPU's host warps reached
+  unsigned long long* d_hint = nullptr;
   uint32_t* d_seq = nullptr;            // device batch counter of this context
   bool ctl_preset = false;              // the plan zeroes d_ctl at the batch start (off the K2 -> K3 edge)
   const int64_t* trace_params = nullptr;  // HELIOS_PLAN_TRACE: the slot's parameter block (params[3] = trace row)
@@ -241,13 +260,14 @@ struct helios_cache {
   int64_t header = 0, stride = 0;
   int io_ctas = 32;
   int gather_ctas = 148;            // K4 grid (one CTA per SM with a host tier, more for HBM-only caches)
+  bool gather_bulk = false;         // HELIOS_GATHER_BULK=1: HBM rows by cp.async.bulk (ablation)
   bool io_sync = false;            // HELIOS_CACHE_IO_SYNC ablation
   bool broken = false;             // a ring / staging watchdog fired: ring state is no longer consistent
   helios::IoRings io;
   bool has_file = false;
   // host staging (HELIOS_CACHE_HOST_STAGED)
   bool staged = false;
-  float stage_frac = 0.6f;
+  float stage_frac = 1.0f;          // HOST_STAGED: share of a batch's host chunks the stagers may claim at most
   int stage_workers = 8;
   helios::Stager* stager = nullptr;
   helios::GatherWS gws;            // default gather context (helios_gather / helios_batch_prepare)
@@ -354,6 +374,8 @@ helios_status gather_range_launch(helios_cache* c, GatherWS& w, const int64_t* n
 helios_status probe_random_impl(helios_graph* g, int64_t n, int32_t reps, float* ms);
 // Host-link probe: mean device time (ms) of K4's host part over n uniformly random host-tier rows.
 helios_status probe_host_impl(helios_cache* c, int64_t n, uint64_t seed, int32_t reps, float* ms);
+// Independent host-link probe (not K4): loads-only random-row kernel, best of 4 in-flight depths.
+helios_status probe_link_impl(helios_cache* c, int64_t n, uint64_t seed, int32_t reps, float* ms, int32_t* best_depth);
 // IO rings for the misses of the last gather_launch on `st` (not capturable: cross-stream events).
 helios_status io_launch(helios_cache* c, GatherWS& w, void* out, cudaStream_t st);
 helios_status validate_csr_device(const int64_t* indptr, const int32_t* indices, int64_t V, int64_t E, int* d_flag,
@@ -362,10 +384,12 @@ helios_status cache_sort_and_dir(helios_cache* c, const uint64_t* hot, int32_t* 
 helios_status gather_rows_by_id(const char* src_dev, int32_t R, const int32_t* ids, int64_t n, char* dst, int sms,
                                 cudaStream_t st);
 helios_status io_start(helios_cache* c, const helios_cache_desc* d);
+void io_worker(helios_cache* c, int ring);  // host IO worker draining SQ ring `ring` (io_workers.cu)
 helios_status io_preload_kernels();
 void io_stop(helios_cache* c);
 helios_status stager_start(helios_cache* c);
 void stager_stop(helios_cache* c);
+int64_t stager_rows(const helios_cache* c);  // rows the stagers copied since build (0 without stagers)
 helios_status stager_register(helios_cache* c, GatherWS& w);
 void stager_unregister(helios_cache* c, GatherWS& w);
 

@@ -93,8 +93,10 @@ __device__ __forceinline__ void insert_seed(const SampleCtx& c, int64_t i, const
 // Hop h degree scan: k_i = min(deg(N_h[i]), f_h), block_indptr[h] = exclusive scan (persistent tile
 // loop + decoupled look-back), e_h = total.  Hop 0 reads N_0 = seeds from the parameters and inserts
 // them into the table on the side; hop h > 0 relabels hop h-1's edges on the side.
+template <int BLK>
 __device__ __forceinline__ void dev_count_scan(const SampleCtx& c, int h) {
-  using BS = cub::BlockScan<long long, kScanBlock>;
+  constexpr int kTile = BLK * kScanItems;
+  using BS = cub::BlockScan<long long, BLK>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ unsigned s_tile;
   __shared__ long long s_prefix;
@@ -106,7 +108,7 @@ __device__ __forceinline__ void dev_count_scan(const SampleCtx& c, int h) {
   int32_t* __restrict__ bp = c.bp[h];
   for (;;) {  // tiles are taken in ticket order until they pass n
     const unsigned tile = tile_ticket(ss, &s_tile);
-    const int64_t base = (int64_t)tile * kScanTile;
+    const int64_t base = (int64_t)tile * kTile;
     if (tile > 0 && base >= n) break;
     if (h == 0 && tile == 0 && threadIdx.x == 0) c.level_counts[0] = n;
     long long k[kScanItems];
@@ -134,7 +136,7 @@ __device__ __forceinline__ void dev_count_scan(const SampleCtx& c, int h) {
       if (i < n) bp[i] = (int32_t)run;
       run += k[q];
     }
-    if (threadIdx.x == 0 && ((n == 0 && tile == 0) || (base < n && n <= base + kScanTile))) {
+    if (threadIdx.x == 0 && ((n == 0 && tile == 0) || (base < n && n <= base + kTile))) {
       bp[n] = (int32_t)(prefix + agg);
       c.edge_counts[h] = prefix + agg;
     }
@@ -225,8 +227,10 @@ __device__ __forceinline__ int fill_group(int32_t f) { return (f < 0 || f > 16) 
 // Hop h dedup/relabel: flag = "this edge is the first occurrence of an id new at this hop"; the
 // scan of the flags numbers the new ids n_h, n_h+1, ... in first-occurrence order and appends them
 // to N_{h+1} (persistent tile loop + decoupled look-back).
+template <int BLK>
 __device__ __forceinline__ void dev_assign(const SampleCtx& c, int h) {
-  using BS = cub::BlockScan<int, kScanBlock>;
+  constexpr int kTile = BLK * kScanItems;
+  using BS = cub::BlockScan<int, BLK>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ unsigned s_tile;
   __shared__ long long s_prefix;
@@ -235,7 +239,7 @@ __device__ __forceinline__ void dev_assign(const SampleCtx& c, int h) {
   const ScanState& ss = c.edge_scan[h];
   for (;;) {
     const unsigned tile = tile_ticket(ss, &s_tile);
-    const int64_t base = (int64_t)tile * kScanTile;
+    const int64_t base = (int64_t)tile * kTile;
     if (tile > 0 && base >= eh) break;
     int flag[kScanItems];
     uint32_t slot[kScanItems];
@@ -265,7 +269,7 @@ __device__ __forceinline__ void dev_assign(const SampleCtx& c, int h) {
         run++;
       }
     }
-    if (threadIdx.x == 0 && ((eh == 0 && tile == 0) || (base < eh && eh <= base + kScanTile)))
+    if (threadIdx.x == 0 && ((eh == 0 && tile == 0) || (base < eh && eh <= base + kTile)))
       c.level_counts[h + 1] = nh + prefix + agg;
     __syncthreads();
   }
@@ -303,7 +307,7 @@ __global__ void __launch_bounds__(kScanBlock) k_count_scan(SampleCtx c, int h) {
   if (h > 0) pdl_wait();
   pdl_trigger();
   TraceScope ts(c.params, 3 * h);
-  dev_count_scan(c, h);
+  dev_count_scan<kScanBlock>(c, h);
 }
 template <int G>
 __global__ void __launch_bounds__(256) k_fill_insert(SampleCtx c, int h) {
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(kScanBlock) k_dedup_assign(SampleCtx c, int h)
   pdl_wait();
   pdl_trigger();
   TraceScope ts(c.params, 3 * h + 2);
-  dev_assign(c, h);
+  dev_assign<kScanBlock>(c, h);
 }
 __global__ void __launch_bounds__(256) k_relabel(SampleCtx c, int h) {
   pdl_wait();
@@ -375,7 +379,7 @@ __global__ void __launch_bounds__(256, 2) k_sample_batch(SampleCtx c) {
     if (!grid_sync(c)) return;
   }
   for (int h = 0; h < c.L; h++) {
-    dev_count_scan(c, h);
+    dev_count_scan<kScanBlock>(c, h);
     if (!grid_sync(c)) return;
     switch (fill_group(c.fan[h])) {
       case 4: dev_fill_insert<4>(c, h); break;
@@ -384,12 +388,48 @@ __global__ void __launch_bounds__(256, 2) k_sample_batch(SampleCtx c) {
       default: dev_fill_insert<32>(c, h); break;
     }
     if (!grid_sync(c)) return;
-    dev_assign(c, h);
+    dev_assign<kScanBlock>(c, h);
     if (!grid_sync(c)) return;
   }
   if (c.L > 0) {
     dev_relabel(c, c.L - 1);
     if (!grid_sync(c)) return;
+  }
+  dev_table_clear(c);
+}
+
+// ---- cluster path (default): the whole batch in ONE launch of one thread-block cluster ------------
+// The cluster's CTAs are co-scheduled by the hardware (on one GPC) and its barrier
+// (barrier.cluster.arrive.release / wait.acquire) is a hardware barrier with cluster-scope memory
+// ordering, so the 3L + 1 phase boundaries cost no kernel launches, no PDL waits and no software
+// grid barrier; batches of different plan slots run as independent clusters side by side.  The
+// phases are the chain's device functions (same code, same results) on BLK-thread CTAs.
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int BLK>
+__global__ void __launch_bounds__(BLK, 1) k_sample_cluster(SampleCtx c) {
+  if (c.L == 0) {
+    dev_insert_seeds(c);
+    cluster_sync();
+  }
+  for (int h = 0; h < c.L; h++) {
+    dev_count_scan<BLK>(c, h);
+    cluster_sync();
+    switch (fill_group(c.fan[h])) {
+      case 4: dev_fill_insert<4>(c, h); break;
+      case 8: dev_fill_insert<8>(c, h); break;
+      case 16: dev_fill_insert<16>(c, h); break;
+      default: dev_fill_insert<32>(c, h); break;
+    }
+    cluster_sync();
+    dev_assign<BLK>(c, h);
+    cluster_sync();
+  }
+  if (c.L > 0) {
+    dev_relabel(c, c.L - 1);
+    cluster_sync();
   }
   dev_table_clear(c);
 }
@@ -514,6 +554,8 @@ void ws_free(SampleWS& w) {
   w = SampleWS{};
 }
 
+static bool cluster_fits(int cl);
+
 helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* fanouts, int32_t L) {
   int64_t maxn, lvl[HELIOS_MAX_HOPS + 1], edg[HELIOS_MAX_HOPS];
   helios_status s = sample_bounds(B, fanouts, L, g->V, g->E, &maxn, lvl, edg);
@@ -572,6 +614,17 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
   p += 8;
   w.scan_bytes = (size_t)(p - w.scan_base);
   if (const char* e = getenv("HELIOS_SAMPLE_PERSISTENT")) w.persistent = atoi(e) != 0;
+  if (const char* e = getenv("HELIOS_SAMPLE_MODE")) {
+    if (!strcmp(e, "cluster")) w.cluster = 8;
+    else if (!strcmp(e, "cluster16")) w.cluster = 16;
+    else if (!strcmp(e, "chain")) w.cluster = 0;
+  }
+  if (w.cluster) {  // a cluster of this size must be schedulable, else the chain is used
+    static int ok8 = -1, ok16 = -1;
+    int& ok = (w.cluster == 16) ? ok16 : ok8;
+    if (ok < 0) ok = cluster_fits(w.cluster) ? 1 : 0;
+    if (!ok) w.cluster = 0;
+  }
   HCUDA(cudaMemset(w.reset_base, 0xFF, w.reset_bytes));  // the table starts all-EMPTY
   return HELIOS_OK;
 }
@@ -640,6 +693,40 @@ static int persistent_grid(int sms) {
   return sms * per_sm;
 }
 
+constexpr int kClusterBlock = 1024;
+
+static cudaLaunchConfig_t cluster_cfg(int cl, cudaStream_t st, cudaLaunchAttribute* attr) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl);
+  cfg.blockDim = dim3(kClusterBlock);
+  cfg.stream = st;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
+// Whether a cluster of `cl` kClusterBlock-thread CTAs can be resident (16 needs the non-portable
+// cluster size attribute).
+static bool cluster_fits(int cl) {
+  if (cl > 8 && cudaFuncSetAttribute(k_sample_cluster<kClusterBlock>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                    cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = cluster_cfg(cl, nullptr, attr);
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_sample_cluster<kClusterBlock>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return n > 0;
+}
+
 helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const int32_t* fanouts, int32_t L,
                             const helios_blocks* out, cudaStream_t st, const std::function<helios_status(int)>* hook) {
   int64_t maxn, lvl[HELIOS_MAX_HOPS + 1], edg[HELIOS_MAX_HOPS];
@@ -647,6 +734,12 @@ helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const i
   if (s != HELIOS_OK) return s;
   const SampleCtx c = make_ctx(g, w, fanouts, L, out);
   HCUDA(cudaMemsetAsync(w.scan_base, 0xFF, w.scan_bytes, st));
+  if (w.cluster && !hook) {  // the whole batch: one cluster, one launch
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = cluster_cfg(w.cluster, st, attr);
+    HCUDA(cudaLaunchKernelEx(&cfg, k_sample_cluster<kClusterBlock>, c));
+    return HELIOS_OK;
+  }
   if (w.persistent && !hook) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(persistent_grid(g->sms));

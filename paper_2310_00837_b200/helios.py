@@ -62,7 +62,7 @@ class helios_batch_timing(ctypes.Structure):
 class helios_cache_info(ctypes.Structure):
     _fields_ = [("dir", vp), ("hbm_tier", vp), ("host_tier", vp), ("V", i64), ("hbm_rows", i64), ("host_rows", i64),
                 ("file_rows", i64), ("row_bytes", i32), ("world_size", i32), ("rank", i32), ("peers_attached", i32),
-                ("io_rings", i32), ("ring_depth", i32), ("direct_io", i32), ("io_reads", i64)]
+                ("io_rings", i32), ("ring_depth", i32), ("direct_io", i32), ("io_reads", i64), ("staged_rows", i64)]
 
 
 _sig = {
@@ -84,6 +84,7 @@ _sig = {
     "helios_cache_attach_peers": (ctypes.c_int, [vp, vp, ctypes.c_size_t]),
     "helios_gather": (ctypes.c_int, [vp, vp, vp, i64, vp, vp, vp]),
     "helios_cache_probe_host": (ctypes.c_int, [vp, i64, u64, i32, ctypes.POINTER(ctypes.c_float)]),
+    "helios_cache_probe_link": (ctypes.c_int, [vp, i64, u64, i32, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32)]),
     "helios_batch_prepare": (ctypes.c_int, [vp, vp, vp, i64, vp, i32, u64, ctypes.POINTER(helios_blocks), vp, vp, vp]),
     "helios_sync": (ctypes.c_int, [vp, vp]),
     "helios_plan_create": (ctypes.c_int, [vp, vp, ctypes.POINTER(helios_plan_desc), ctypes.POINTER(vp)]),
@@ -358,6 +359,16 @@ def helios_cache_probe_host(c: Cache, n_rows: int, seed: int = 1, reps: int = 5)
     _check(_lib.helios_cache_probe_host(c.handle, n_rows, seed & (2**64 - 1), reps, ctypes.byref(ms)),
            "helios_cache_probe_host")
     return ms.value
+
+
+def helios_cache_probe_link(c: Cache, n_rows: int, seed: int = 1, reps: int = 3) -> tuple[float, int]:
+    """(best mean ms, rows in flight of that setting) of a loads-only random-row microkernel (not K4)
+    over n_rows uniformly random host-tier rows, swept over grid size x loads in flight: the host
+    link's random-row ceiling."""
+    ms, d = ctypes.c_float(), i32()
+    _check(_lib.helios_cache_probe_link(c.handle, n_rows, seed & (2**64 - 1), reps, ctypes.byref(ms), ctypes.byref(d)),
+           "helios_cache_probe_link")
+    return ms.value, d.value
 
 
 def helios_sync(c: Cache, stream=None) -> None:

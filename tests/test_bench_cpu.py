@@ -5,6 +5,7 @@ import os
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -88,3 +89,26 @@ def test_sampling_sector_count():
     expect_sectors = 3 + 1 + mc + 3          # indptr per row + v0's sector + sampled + directory
     assert abs(got["sectors"] - expect_sectors) < 0.25
     assert got["stream_bytes"] == 4 * (3 + 5 + 5) + 4 * 4 + 8 * 3
+
+
+def test_oracle_baseline_threads():
+    """The P-core leg of cpu_baseline: several threads each prepare independent batches; every batch
+    equals the single-threaded oracle's (the threads share no state but the batch counter)."""
+    import bench
+    import oracle
+    import workloads
+    cfg = workloads.Config("tiny", 3000, 30_000, 16, 64, [5, 3], 0.1, 0.4, train_pct=100)
+    inp = workloads.make_inputs(cfg, table=True)
+    keys = workloads.batch_keys(0, len(inp.batches))
+    seen = {}
+
+    def check(b, ob, feats):
+        seen[b] = (ob.nodes.copy(), feats.copy())
+
+    r = bench.run_oracle_baseline(inp, keys, 5.0, check=check, threads=3)
+    assert r["threads"] == 3 and r["batches"] == len(seen) > 0 and r["value"] > 0
+    for b, (nodes, feats) in list(seen.items())[:5]:
+        ob = oracle.sample(inp.graph.indptr, inp.graph.indices, inp.batches[b], cfg.fanouts, keys[b])
+        assert np.array_equal(nodes, ob.nodes)
+        assert np.array_equal(feats, oracle.gather(ob.nodes, cfg.R, table=inp.table))
+    assert bench.cpu_model()

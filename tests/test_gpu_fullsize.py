@@ -19,7 +19,7 @@ import oracle  # noqa: E402
 import workloads  # noqa: E402
 
 
-def setup(H, cfg):
+def setup(H, cfg, flags=0):
     inp = workloads.make_inputs(cfg, table=True)
     g = H.helios_graph_load(inp.graph.indptr, inp.graph.indices)
     hot = torch.zeros(cfg.V, dtype=torch.int64, device="cuda")
@@ -30,7 +30,7 @@ def setup(H, cfg):
     Hr, S = workloads.tier_rows(cfg)
     if cfg.hbm_frac + cfg.host_frac >= 1.0:
         S = max(0, cfg.V - Hr)
-    c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=inp.table)
+    c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=inp.table, flags=flags)
     dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S)
     return inp, g, c, dref
 
@@ -87,9 +87,10 @@ def test_c2_full_size_plan(H):
     g.free()
 
 
-def test_c3_scaled_plan(H):
+@pytest.mark.parametrize("staged", [False, True])
+def test_c3_scaled_plan(H, staged):
     cfg = workloads.scaled(workloads.CONFIGS["C3"], 0.1)
-    inp, g, c, dref = setup(H, cfg)
+    inp, g, c, dref = setup(H, cfg, flags=H.HOST_STAGED if staged else 0)
     got = check_batches(H, inp, g, c, dref, 16)
     assert sum(int(v[2][2]) for v in got.values()) > 0   # host-tier rows were exercised
     c.free()
@@ -98,14 +99,15 @@ def test_c3_scaled_plan(H):
 
 def test_c3_full_size_plan(H):
     """C3 at BASELINE.json's full size (111 M / 1.6 B, 56.8 GB feature table, 51 GB packed host tier):
-    8 batches through the bench's plan configuration, every output bit-exact."""
+    8 batches through the bench's plan configuration (dynamic staged host tier, 12 in flight), every
+    output bit-exact."""
     cfg = workloads.CONFIGS["C3"]
     import os
     avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
     if avail < 150e9:
         pytest.skip(f"needs ~125 GB of host RAM for the table + packed host tier, {avail / 1e9:.0f} GB available")
-    inp, g, c, dref = setup(H, cfg)
-    got = check_batches(H, inp, g, c, dref, 8)
+    inp, g, c, dref = setup(H, cfg, flags=H.HOST_STAGED)
+    got = check_batches(H, inp, g, c, dref, 24, depth=12)
     assert sum(int(v[2][2]) for v in got.values()) > 0
     c.free()
     g.free()

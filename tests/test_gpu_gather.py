@@ -69,19 +69,20 @@ def gather_and_check(H, c, inp, nodes_np, stats_ref):
     assert stats.cpu().numpy().tolist() == stats_ref.tolist()
 
 
-@pytest.mark.parametrize("alias,staged", [(False, False), (True, False), (False, True), (True, True)])
-def test_gather_three_tiers_c1(H, c1, c1_hot, alias, staged):
+@pytest.mark.parametrize("alias,staged,frac", [(False, False, 0), (True, False, 0), (False, True, 0.5), (True, True, 0.5),
+                                               (False, True, 1.0)])
+def test_gather_three_tiers_c1(H, c1, c1_hot, alias, staged, frac):
     g, hot = c1_hot
     cfg = c1.cfg
     Hr, S = workloads.tier_rows(cfg)
     c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=c1.table, feature_path=c1.feature_path,
                              header_bytes=c1.header, file_stride=c1.stride,
                              flags=(H.HOST_ALIAS if alias else 0) | (H.HOST_STAGED if staged else 0),
-                             stage_workers=3, stage_frac=0.5)
+                             stage_workers=3, stage_frac=frac)
     assert c.info().file_rows == cfg.V - Hr - S
     dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S, host_slot_is_id=alias)
     rng = np.random.default_rng(0)
-    for n in (1, 31, 1000, 4097, cfg.V):
+    for n in (1, 31, 1000, 4097, cfg.V) + ((cfg.V,) * 6 if staged else ()):   # staged: GPU/CPU meeting points vary
         nodes = rng.permutation(cfg.V)[:n]
         gather_and_check(H, c, c1, nodes, oracle.lookup_counts(dref, nodes))
     c.free()
@@ -165,6 +166,8 @@ def test_probe_host(H, c1, c1_hot, alias):
                              header_bytes=c1.header, file_stride=c1.stride, flags=H.HOST_ALIAS if alias else 0)
     ms = H.helios_cache_probe_host(c, 50_000, seed=3, reps=3)
     assert 0 < ms < 1000
+    lms, depth = H.helios_cache_probe_link(c, 50_000, seed=3, reps=2)
+    assert 0 < lms < 1000 and depth > 0
     assert 0 < H.helios_graph_probe_random(g, 1 << 20, reps=2) < 1000
     with pytest.raises(H.HeliosError) as e:
         H.helios_graph_probe_random(g, 0)
@@ -180,6 +183,9 @@ def test_probe_host(H, c1, c1_hot, alias):
     c0 = H.helios_cache_build(g, hot, c1.cfg.R, c1.cfg.V, 0, host_table=c1.table)
     with pytest.raises(H.HeliosError) as e:
         H.helios_cache_probe_host(c0, 100)
+    assert e.value.name == "E_STATE"
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_cache_probe_link(c0, 100)
     assert e.value.name == "E_STATE"
     c0.free()
 

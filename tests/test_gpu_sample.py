@@ -40,6 +40,15 @@ def assert_same(gpu, orc, L):
         assert np.array_equal(gpu["block_indices"][h], orc.block_indices[h]), f"hop {h} indices"
 
 
+@pytest.fixture(params=["chain", "cluster", "cluster16"])
+def mode(request, monkeypatch):
+    """Sampler launch mode (HELIOS_SAMPLE_MODE, read when a graph's workspace is allocated): the chain of
+    2 + 3L kernels, or the whole batch in one launch of an 8- or 16-CTA cluster.  Same device code,
+    so the same bits."""
+    monkeypatch.setenv("HELIOS_SAMPLE_MODE", request.param)
+    return request.param
+
+
 @pytest.fixture(scope="module")
 def c1():
     return workloads.make_inputs(workloads.CONFIGS["C1"], table=False)
@@ -50,7 +59,7 @@ def medium():
     return synth.graph(300_000, 6_000_000, seed=21)
 
 
-def test_c1_full_epoch(H, c1):
+def test_c1_full_epoch(H, c1, mode):
     cfg = c1.cfg
     g = H.helios_graph_load(c1.graph.indptr, c1.graph.indices)
     keys = workloads.batch_keys(0, len(c1.batches))
@@ -62,7 +71,7 @@ def test_c1_full_epoch(H, c1):
 
 @pytest.mark.parametrize("B,fanouts", [(1024, [15, 10, 5]), (1000, [25, 10]), (333, [3, 3, 3, 3]), (77, [40]),
                                        (5, [-1, -1]), (1, [15, 10, 5])])
-def test_medium_graph(H, medium, B, fanouts):
+def test_medium_graph(H, medium, B, fanouts, mode):
     g = H.helios_graph_load(medium.indptr, medium.indices)
     rng = np.random.default_rng(B)
     seeds = rng.choice(medium.V, B, replace=False)
@@ -72,7 +81,7 @@ def test_medium_graph(H, medium, B, fanouts):
         assert_same(gpu, orc, len(fanouts))
 
 
-def test_hub_and_isolated(H):
+def test_hub_and_isolated(H, mode):
     d = 200_000
     adj_len = np.zeros(d + 2, dtype=np.int64)
     adj_len[0] = d
