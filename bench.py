@@ -328,6 +328,9 @@ def main():
                     help="host tier: dynamic split between GPU zero-copy reads and host stager threads, with this "
                          "cap on the stagers' share of a batch's host rows (default 1.0 = no cap); 0 = pure zero-copy")
     ap.add_argument("--zero-copy", action="store_true", help="ablation: pure GPU zero-copy host tier (= --host-staged 0)")
+    ap.add_argument("--stage-reserve", type=float, default=0.6,
+                    help="HOST_STAGED: share of each batch's host-row chunks (from the list's end) the GPU leaves to "
+                         "the stagers, waiting a bounded time before copying them itself (0 = pure dynamic split)")
     ap.add_argument("--stage-workers", type=int, default=14,
                     help="host stager threads (HOST_STAGED); 14 of the GPU box's 16 cores measured best")
     ap.add_argument("--ring-depth", type=int, default=256)
@@ -439,7 +442,8 @@ def main():
     fkw = dict(feature_path=inp.feature_path, header_bytes=inp.header, file_stride=inp.stride,
                io_rings=args.io_rings, ring_depth=args.ring_depth, io_ctas=args.io_ctas) if file_cfg else {}
     if args.host_staged > 0:
-        fkw.update(stage_workers=args.stage_workers, stage_frac=args.host_staged)
+        fkw.update(stage_workers=args.stage_workers, stage_frac=args.host_staged,
+                   stage_reserve=min(args.stage_reserve, args.host_staged))
     sflag = (H.HOST_STAGED if args.host_staged > 0 else 0) | (H.IO_SYNC if args.io_sync else 0)
     if (args.host_alias and table is not None) or S == 0:
         c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
@@ -611,7 +615,7 @@ def main():
         l_ms, l_depth = H.helios_cache_probe_link(c, n_probe, seed=11, reps=4)
         link_probe = {"Mrows_s": round(n_probe / l_ms / 1e3, 2), "gbs": round(n_probe * cfg.R / l_ms / 1e6, 2),
                       "how": f"helios_cache_probe_link: loads-only microkernel (not K4), {n_probe} uniformly random "
-                             f"host-tier rows per launch, fresh rows every launch, best of 8 grid x loads-in-flight "
+                             f"host-tier rows per launch, fresh rows every launch, best of 16 grid x loads-in-flight "
                              f"settings (best: ~{l_depth} rows in flight)"}
         # (2) K4's own host part on uniform random rows (the round-1 probe; kept for comparison)
         p_ms = H.helios_cache_probe_host(c, n_probe, seed=7, reps=reps)
@@ -716,14 +720,20 @@ def main():
                                       "(uniform 4 B loads over the CSR indices)"}
     if link_probe is not None and n_host > 0:
         got = n_host * (world * steps / (max_ms / 1e3)) / world / 1e6
+        st_rows = staged_timed / steps if args.host_staged > 0 else 0.0
+        zc = max(0.0, n_host - st_rows) * (steps / (max_ms / 1e3)) / 1e6  # GPU zero-copy rows (upper bound)
         roof["host_link"] = {"achieved_Mrows_s": round(got, 2), "random_row_ceiling": link_probe,
                              "frac_of_ceiling": round(got / link_probe["Mrows_s"], 4),
+                             "zero_copy_Mrows_s": round(zc, 2),
+                             "zero_copy_frac_of_ceiling": round(zc / link_probe["Mrows_s"], 4),
                              "k4_host_part_uniform_rows": probe, "real_lists_alone": lists_alone,
                              "cpu_staged_rows_per_batch": round(staged_timed / steps, 1) if args.host_staged > 0 else 0,
                              "note": "host-tier rows per second of the whole timed run (zero-copy and staged rows) vs "
                                      "the random zero-copy row ceiling measured by an independent loads-only kernel "
                                      "(DESIGN.md §6); the staged share can exceed the zero-copy ceiling because host "
-                                     "threads stream it"}
+                                     "threads stream it; zero_copy_* counts only the rows the stagers did not copy "
+                                     "(a lower bound on the stagers' share, since a chunk both sides copy is counted "
+                                     "as staged)"}
     value = world * steps / (max_ms / 1e3)
     e2e_val = world * steps / e2e_s
     launches_per_step = (3 * L + 2 + 2 + ((2 if args.io_sync else 3) if c.info().file_rows > 0 else 0)
@@ -743,7 +753,8 @@ def main():
                    "scale": s, "parallelism": f"dp{world} (seeds split per rank, HBM tier sharded)",
                    "host_tier": ("alias of canonical table (by id)" if args.host_alias else "packed, hot-rank order")
                    + (f"; dynamic split: GPU zero-copy from the front of each batch's host list, {args.stage_workers} "
-                      f"host stager threads from its end (cap {args.host_staged:.0%})"
+                      f"host stager threads from its end (cap {args.host_staged:.0%}, last "
+                      f"{min(args.stage_reserve, args.host_staged):.0%} reserved for the stagers)"
                       if args.host_staged > 0 else "; GPU zero-copy reads only (ablation)"),
                    "batches_in_flight": depth, "cuda_graphs": not args.no_graph, "serial_gather": bool(args.serial_gather),
                    "link_stream": bool(plan.link),

@@ -188,6 +188,11 @@ typedef struct {
   int32_t stage_workers;      /* HOST_STAGED: host stager threads (0 = 8)                                */
   float stage_frac;           /* HOST_STAGED: cap on the share of each batch's host-row chunks the stagers
                                  may claim (0 = 1.0: no cap beyond the 2^16-row staging buffer)       */
+  float stage_reserve;        /* HOST_STAGED: share of each batch's host-row chunks, counted from the list's
+                                 end, that the GPU's host-row warps leave to the stagers: a warp reaching
+                                 such a chunk waits up to 200 us for a stager to claim it (and the steal
+                                 timeout for a claimed one) before copying it zero-copy itself.  0 = none:
+                                 the pure dynamic split (whoever reaches a chunk first copies it).   */
 } helios_cache_desc;
 
 /* Builds the directory and fills the tiers (blocking).  The HBM tier is filled from host_table

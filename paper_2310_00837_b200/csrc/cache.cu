@@ -197,6 +197,7 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
   c->io_sync = (d->flags & HELIOS_CACHE_IO_SYNC) != 0;
   c->stage_workers = d->stage_workers > 0 ? d->stage_workers : 8;
   c->stage_frac = d->stage_frac > 0.f ? std::min(d->stage_frac, 1.0f) : 1.0f;
+  c->stage_reserve = d->stage_reserve > 0.f ? std::min(d->stage_reserve, c->stage_frac) : 0.0f;
   const int64_t V = c->V;
   // clamp tiers to V
   const int64_t GH = std::min<int64_t>((int64_t)c->G * c->H, V);
@@ -342,9 +343,11 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
     st = io_start(c, d);
     if (st != HELIOS_OK) return st;
   }
-  {  // K4 grid: one CTA per SM when host rows are read (PCIe-latency bound, leaves SM slots to the
-     // other batches' sampling); HBM-only caches are bandwidth bound and want more warps in flight
-    int per_sm = (c->S > 0) ? 1 : 2;
+  {  // K4 grid: one CTA per SM.  With host rows the gather is PCIe-latency bound; HBM-only, 2 CTAs per
+     // SM make K4 alone faster (C2: 22.5 vs 30.6 us per launch) but the whole pipeline slower (C2
+     // 28.6 k vs 30.2 k batches/s, profiles/r02/bench_c2_gather_grid.jsonl): the smaller footprint
+     // leaves SM slots to the other batches' sampling kernels.
+    int per_sm = 1;
     if (const char* e = getenv("HELIOS_GATHER_CTAS_PER_SM")) per_sm = std::max(1, std::min(atoi(e), 4));
     if (const char* e = getenv("HELIOS_GATHER_BULK")) c->gather_bulk = atoi(e) != 0;
     if (c->gather_bulk) per_sm = 1;  // 192 KB of shared memory per CTA

@@ -114,6 +114,8 @@ struct GatherArgs {
   const char* stage;        // device alias of the pinned staging rows (chunk k from the list's end at row 64k)
   const unsigned long long* chunk;  // device alias of the per-chunk state words ((seq << 2) | CLAIMED / DONE)
   unsigned long long* hint; // device alias of the pinned front hint ((seq << 32) | chunk the GPU reached)
+  float stage_reserve;      // share of the batch's chunks (from the list's end) left to the stagers
+  int64_t stage_max_chunks; // chunks the staging buffer holds (the stagers never claim more)
   int* err;
   const char* hbm;          // this rank's shard
   char* const* peers;       // device [G]
@@ -365,13 +367,21 @@ __device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsign
 // copy is copied twice (identical bytes; the staged copy is unused): no exclusivity is needed, only
 // "every row by at least one side", and the GPU alone decides which rows it still has to copy.  The
 // list the warps read is in device memory; the stagers read its pinned mirror.
+// Reserved chunks (stage_reserve > 0): the last ceil(stage_reserve * n_chunks) chunks of the list are
+// left to the stagers.  A warp reaching an unclaimed reserved chunk does not advance the front hint;
+// it polls the chunk's state for up to kStageReserveNs (the stagers claim from the back, so they get
+// there late in the batch) and only then takes the chunk itself (hint, zero-copy), so a stall of the
+// host threads still costs a bounded wait, never a hang.
 constexpr uint64_t kStageStealNs = 100000;
+constexpr uint64_t kStageReserveNs = 200000;
 template <int VPL, int UH>
 __device__ __forceinline__ void host_rows_dyn(const GatherArgs& a, int64_t n_host, int lane, int nvec) {
   const uint32_t seq = (uint32_t)a.ctl[kCtlStageSeq];
   const unsigned long long claimed = ((unsigned long long)seq << 2) | kChunkClaimed;
   const unsigned long long done = ((unsigned long long)seq << 2) | kChunkDone;
   const int64_t n_chunks = (n_host + kStageChunk - 1) / kStageChunk;
+  const int64_t n_res = min(min(n_chunks, a.stage_max_chunks), (int64_t)ceilf(a.stage_reserve * (float)n_chunks));
+  const int64_t c_res = n_chunks - n_res;  // chunks [c_res, n_chunks) are reserved for the stagers
   for (;;) {
     const int64_t j0 = warp_ticket(&a.ctl[kCtlHostTicket], kStageChunk, lane);
     if (j0 >= n_host) break;
@@ -379,8 +389,18 @@ __device__ __forceinline__ void host_rows_dyn(const GatherArgs& a, int64_t n_hos
     const int64_t j1 = min(n_host, j0 + kStageChunk);
     unsigned long long st = 0;
     if (lane == 0) {
-      st_relaxed_sys_u64(a.hint, ((unsigned long long)seq << 32) | (unsigned long long)c);
       st = ld_relaxed_sys_u64(&a.chunk[c]);
+      if (c >= c_res && st != claimed && st != done) {  // reserved: give the stagers time to claim it
+        const uint64_t t0 = globaltimer();
+        unsigned backoff = 512;
+        while (st != claimed && st != done && globaltimer() - t0 < kStageReserveNs) {
+          __nanosleep(backoff);
+          backoff = min(backoff * 2u, 8192u);
+          st = ld_relaxed_sys_u64(&a.chunk[c]);
+        }
+      }
+      if (st != claimed && st != done)  // this warp copies the chunk: stagers stop at the front
+        st_relaxed_sys_u64(a.hint, ((unsigned long long)seq << 32) | (unsigned long long)c);
       if (st == claimed) {  // a stager is copying it: wait a bounded time, then take it back
         const uint64_t t0 = globaltimer();
         unsigned backoff = 256;
@@ -840,6 +860,8 @@ static GatherArgs make_args(helios_cache* c, GatherWS& w, void* out, helios_gath
   a.stage = w.d_stage;
   a.chunk = w.d_chunk;
   a.hint = w.d_hint;
+  a.stage_reserve = c->stage_reserve;
+  a.stage_max_chunks = w.stage_rows / kStageChunk;
   a.err = c->d_err;
   a.hbm = c->hbm;
   a.peers = c->d_peers;
@@ -976,23 +998,26 @@ helios_status probe_host_impl(helios_cache* c, int64_t n, uint64_t seed, int32_t
 }
 
 // ---- independent host-link probe (measurement; not K4) --------------------------------------------
-// Loads only: thread t of the grid reads D 16-byte vectors, vector k of the thread being vector
-// (t*D + k) mod nvec of random row (t*D + k) / nvec, rows drawn uniformly (SplitMix64 of (seed, row))
-// over the host tier; no stores, no lists, no warp roles.  D (loads in flight per thread) is swept
-// by the host together with the grid size (rows in flight) and the best rate kept, so this is the
-// ceiling of random R-byte zero-copy reads on this platform, independent of K4's code.
+// Loads only: warp w of the grid reads D x 32 consecutive 16-byte vectors of the flattened sequence
+// of random rows (load k of lane l: vector f = (w*D + k)*32 + l, i.e. vector f mod nvec of random row
+// f / nvec), so every load instruction covers 512 contiguous bytes of rows, as a coalesced gather
+// would; rows are drawn uniformly (SplitMix64 of (seed, row)) over the host tier; no stores, no
+// lists, no warp roles.  D (loads in flight per lane) is swept by the host together with the grid
+// size (rows in flight) and the best rate kept, so this is the ceiling of random R-byte zero-copy
+// reads on this platform, independent of K4's code.
 template <int D>
 __global__ void k_probe_link(const char* __restrict__ host, int64_t range, int32_t R, int64_t n_rows, uint64_t seed,
                              int* sink) {
   const int nvec = R >> 4;
   const int64_t total = n_rows * nvec;
   int acc = 0;
-  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * D; base < total;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 32 * D; base < total;
        base += (int64_t)gridDim.x * blockDim.x * D) {
     int4 r[D];
 #pragma unroll
     for (int k = 0; k < D; k++) {
-      const int64_t f = base + k;
+      const int64_t f = base + 32 * k + lane;
       r[k] = make_int4(0, 0, 0, 0);
       if (f < total) {
         const int64_t row = f / nvec;
@@ -1023,17 +1048,19 @@ helios_status probe_link_impl(helios_cache* c, int64_t n, uint64_t seed, int32_t
   int bd = 0;
   uint64_t salt = seed;
   cudaError_t err = cudaSuccess;
-  // rows in flight = threads * d / nvec: swept from ~150 to ~40 k rows (random zero-copy rows slow down
-  // when far too many are outstanding, so the sweep covers both sides of the optimum)
+  // rows in flight = threads * d / nvec: swept from ~300 to ~19 k rows at R = 512 (random zero-copy
+  // rows slow down when far too many are outstanding, so the sweep covers both sides of the optimum)
   const int nvec = c->R / 16;
-  for (int cfg = 0; cfg < 8; cfg++) {
-    const int d = (cfg & 1) ? 8 : 2;
-    const int grid_c = std::max(1, (c->sms / 4) << (cfg >> 1));  // 37, 74, 148, 296 CTAs (B200)
+  for (int cfg = 0; cfg < 16; cfg++) {
+    const int d = 1 << (cfg & 3);                                // 1, 2, 4, 8 loads in flight per lane
+    const int grid_c = std::max(1, (c->sms / 4) << (cfg >> 2));  // 37, 74, 148, 296 CTAs (B200)
     float tot = 0;
     for (int r = 0; r < reps && err == cudaSuccess; r++) {
       salt = salt * 0x5851F42D4C957F2Dull + 0x14057B7EF767814Full;  // fresh rows every launch (no L2 reuse)
       cudaEventRecord(e0, 0);
-      if (d == 2) k_probe_link<2><<<grid_c, 256>>>(c->d_host_tier, range, c->R, n, salt, sink);
+      if (d == 1) k_probe_link<1><<<grid_c, 256>>>(c->d_host_tier, range, c->R, n, salt, sink);
+      else if (d == 2) k_probe_link<2><<<grid_c, 256>>>(c->d_host_tier, range, c->R, n, salt, sink);
+      else if (d == 4) k_probe_link<4><<<grid_c, 256>>>(c->d_host_tier, range, c->R, n, salt, sink);
       else k_probe_link<8><<<grid_c, 256>>>(c->d_host_tier, range, c->R, n, salt, sink);
       cudaEventRecord(e1, 0);
       err = cudaEventSynchronize(e1);

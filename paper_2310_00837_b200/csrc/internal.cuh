@@ -268,6 +268,7 @@ struct helios_cache {
   // host staging (HELIOS_CACHE_HOST_STAGED)
   bool staged = false;
   float stage_frac = 1.0f;          // HOST_STAGED: share of a batch's host chunks the stagers may claim at most
+  float stage_reserve = 0.0f;       // HOST_STAGED: share (from the list's end) the GPU leaves to the stagers
   int stage_workers = 8;
   helios::Stager* stager = nullptr;
   helios::GatherWS gws;            // default gather context (helios_gather / helios_batch_prepare)

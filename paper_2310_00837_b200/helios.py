@@ -47,7 +47,7 @@ class helios_cache_desc(ctypes.Structure):
                 ("hotness", vp), ("host_table", vp), ("feature_path", ctypes.c_char_p), ("header_bytes", i64),
                 ("file_stride", i64), ("io_rings", i32), ("ring_depth", i32), ("io_ctas", i32),
                 ("io_fault_at", i32), ("flags", u32), ("host_tier", vp), ("stage_workers", i32),
-                ("stage_frac", ctypes.c_float)]
+                ("stage_frac", ctypes.c_float), ("stage_reserve", ctypes.c_float)]
 
 
 class helios_plan_desc(ctypes.Structure):
@@ -304,7 +304,8 @@ def helios_cache_build(g: Graph, hotness: torch.Tensor, row_bytes: int, hbm_rows
                        host_table: np.ndarray | None = None, feature_path: str | None = None, header_bytes: int = 0,
                        file_stride: int = 0, world_size: int = 1, rank: int = 0, io_rings: int = 4,
                        ring_depth: int = 256, io_ctas: int = 32, flags: int = 0, io_fault_at: int = 0,
-                       host_tier=None, stage_workers: int = 0, stage_frac: float = 0.0) -> Cache:
+                       host_tier=None, stage_workers: int = 0, stage_frac: float = 0.0,
+                       stage_reserve: float = 0.0) -> Cache:
     d = helios_cache_desc()
     d.row_bytes, d.world_size, d.rank = row_bytes, world_size, rank
     d.hbm_rows, d.host_rows = hbm_rows, host_rows
@@ -315,7 +316,7 @@ def helios_cache_build(g: Graph, hotness: torch.Tensor, row_bytes: int, hbm_rows
     d.header_bytes, d.file_stride = header_bytes, file_stride
     d.io_rings, d.ring_depth, d.io_ctas, d.io_fault_at, d.flags = io_rings, ring_depth, io_ctas, io_fault_at, flags
     d.host_tier = _ptr(host_tier)
-    d.stage_workers, d.stage_frac = stage_workers, stage_frac
+    d.stage_workers, d.stage_frac, d.stage_reserve = stage_workers, stage_frac, stage_reserve
     h = vp()
     _check(_lib.helios_cache_build(g.handle, ctypes.byref(d), ctypes.byref(h)), "helios_cache_build")
     return Cache(h.value, g, (host_table, path, host_tier))

@@ -30,7 +30,9 @@ def setup(H, cfg, flags=0):
     Hr, S = workloads.tier_rows(cfg)
     if cfg.hbm_frac + cfg.host_frac >= 1.0:
         S = max(0, cfg.V - Hr)
-    c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=inp.table, flags=flags)
+    # staged caches as the bench builds them: 14 stagers, last 60 % of each batch's host chunks reserved
+    skw = dict(stage_workers=14, stage_reserve=0.6) if flags & H.HOST_STAGED else {}
+    c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=inp.table, flags=flags, **skw)
     dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S)
     return inp, g, c, dref
 

@@ -69,16 +69,17 @@ def gather_and_check(H, c, inp, nodes_np, stats_ref):
     assert stats.cpu().numpy().tolist() == stats_ref.tolist()
 
 
-@pytest.mark.parametrize("alias,staged,frac", [(False, False, 0), (True, False, 0), (False, True, 0.5), (True, True, 0.5),
-                                               (False, True, 1.0)])
-def test_gather_three_tiers_c1(H, c1, c1_hot, alias, staged, frac):
+@pytest.mark.parametrize("alias,staged,frac,reserve", [(False, False, 0, 0), (True, False, 0, 0), (False, True, 0.5, 0),
+                                                       (True, True, 0.5, 0), (False, True, 1.0, 0), (False, True, 1.0, 0.6),
+                                                       (True, True, 0.7, 0.7)])
+def test_gather_three_tiers_c1(H, c1, c1_hot, alias, staged, frac, reserve):
     g, hot = c1_hot
     cfg = c1.cfg
     Hr, S = workloads.tier_rows(cfg)
     c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=c1.table, feature_path=c1.feature_path,
                              header_bytes=c1.header, file_stride=c1.stride,
                              flags=(H.HOST_ALIAS if alias else 0) | (H.HOST_STAGED if staged else 0),
-                             stage_workers=3, stage_frac=frac)
+                             stage_workers=3, stage_frac=frac, stage_reserve=reserve)
     assert c.info().file_rows == cfg.V - Hr - S
     dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S, host_slot_is_id=alias)
     rng = np.random.default_rng(0)

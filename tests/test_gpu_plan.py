@@ -25,7 +25,8 @@ def c1(tmp_path_factory):
 
 
 def build(H, inp, Hr, S, flags=0):
-    # staged-mode caches use 3 stager threads and stage 70 % of each batch's host rows
+    # staged-mode caches use 3 stager threads, stage at most 70 % of each batch's host rows and reserve
+    # the last 50 % for the stagers
     cfg = inp.cfg
     g = H.helios_graph_load(inp.graph.indptr, inp.graph.indices)
     hot = torch.zeros(cfg.V, dtype=torch.int64, device="cuda")
@@ -33,7 +34,7 @@ def build(H, inp, Hr, S, flags=0):
     H.helios_presample(g, torch.as_tensor(np.concatenate(inp.batches)).cuda(), cfg.B, cfg.fanouts, pk, hot)
     c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=inp.table, feature_path=inp.feature_path,
                              header_bytes=inp.header, file_stride=inp.stride, flags=flags, stage_workers=3,
-                             stage_frac=0.7)
+                             stage_frac=0.7, stage_reserve=0.5)
     return g, hot, c
 
 
