@@ -312,7 +312,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--parity-batches", type=int, default=2)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no baseline, no parity")
-    ap.add_argument("--depth", type=int, default=12, help="batches in flight (plan slots)")
+    ap.add_argument("--depth", type=int, default=12, help="plan slots (groups in flight)")
+    ap.add_argument("--group", type=int, default=1,
+                    help="batches per plan slot: each kernel of a slot's chain launches once for its whole group "
+                         "(gridDim.y); batches in flight = depth x group")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly instead of CUDA graphs")
     ap.add_argument("--serial-gather", type=int, default=0, help="1: gathers of successive batches run one at a time")
     ap.add_argument("--intra", action="store_true", help="intra-batch pipeline: per-hop gather passes (NEXT-1)")
@@ -328,7 +331,7 @@ def main():
                     help="host tier: dynamic split between GPU zero-copy reads and host stager threads, with this "
                          "cap on the stagers' share of a batch's host rows (default 1.0 = no cap); 0 = pure zero-copy")
     ap.add_argument("--zero-copy", action="store_true", help="ablation: pure GPU zero-copy host tier (= --host-staged 0)")
-    ap.add_argument("--stage-reserve", type=float, default=0.6,
+    ap.add_argument("--stage-reserve", type=float, default=0.7,
                     help="HOST_STAGED: share of each batch's host-row chunks (from the list's end) the GPU leaves to "
                          "the stagers, waiting a bounded time before copying them itself (0 = pure dynamic split)")
     ap.add_argument("--stage-workers", type=int, default=14,
@@ -336,6 +339,10 @@ def main():
     ap.add_argument("--ring-depth", type=int, default=256)
     ap.add_argument("--io-ctas", type=int, default=32, help="CTA budget of each IO kernel (PAPER.md:244)")
     ap.add_argument("--io-sync", action="store_true", help="ablation: GIDS-style coupled IO (one warp per request)")
+    ap.add_argument("--hbm-replicated", action="store_true",
+                    help="C5-rep ablation: every rank's HBM tier holds the same hottest rows (no peer rows)")
+    ap.add_argument("--io-sms", type=int, default=0,
+                    help="run the IO kernel on a green-context partition of this many SMs (SURVEY NEXT-3; 0 = none)")
     args = ap.parse_args()
     if args.zero_copy:
         args.host_staged = 0.0
@@ -433,18 +440,21 @@ def main():
     H.helios_graph_sync(g)
     allreduce(hot)
     presample_s = time.time() - t1
-    Hr, S = workloads.tier_rows(cfg, world)
+    Gd = 1 if args.hbm_replicated else world   # the directory's world size (C5-rep: replicated HBM tier)
+    Hr, S = workloads.tier_rows(cfg, Gd)
     if cfg.hbm_frac + cfg.host_frac >= 1.0:
-        S = max(0, cfg.V - world * Hr)
+        S = max(0, cfg.V - Gd * Hr)
     else:
-        S = max(0, min(S, cfg.V - world * Hr))
+        S = max(0, min(S, cfg.V - Gd * Hr))
     t2 = time.time()
     fkw = dict(feature_path=inp.feature_path, header_bytes=inp.header, file_stride=inp.stride,
-               io_rings=args.io_rings, ring_depth=args.ring_depth, io_ctas=args.io_ctas) if file_cfg else {}
+               io_rings=args.io_rings, ring_depth=args.ring_depth, io_ctas=args.io_ctas,
+               io_sms=args.io_sms) if file_cfg else {}
     if args.host_staged > 0:
         fkw.update(stage_workers=args.stage_workers, stage_frac=args.host_staged,
                    stage_reserve=min(args.stage_reserve, args.host_staged))
-    sflag = (H.HOST_STAGED if args.host_staged > 0 else 0) | (H.IO_SYNC if args.io_sync else 0)
+    sflag = ((H.HOST_STAGED if args.host_staged > 0 else 0) | (H.IO_SYNC if args.io_sync else 0)
+             | (H.HBM_REPLICATED if args.hbm_replicated else 0))
     if (args.host_alias and table is not None) or S == 0:
         c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=table, world_size=world, rank=rank,
                                  flags=(H.HOST_ALIAS if S else 0) | sflag, **fkw)
@@ -479,11 +489,13 @@ def main():
     depth = args.depth
     pflags = ((H.PLAN_NO_GRAPH if args.no_graph else 0) | (H.PLAN_SERIAL_GATHER if args.serial_gather else 0)
               | (H.PLAN_INTRA_BATCH if args.intra else 0) | (H.PLAN_LINK_STREAM if args.link_stream else 0))
-    plan = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=depth, flags=pflags)
+    G = args.group
+    plan = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=depth, flags=pflags, group=G)
+    P = plan.positions   # depth x G batch positions; a group's kernels launch once for its G batches
 
     for i in range(args.warmup):
-        H.helios_plan_submit(plan, i % depth, seed_of[seq[i]], keys[seq[i]], stream)
-    for k in range(depth):
+        H.helios_plan_submit(plan, i % P, seed_of[seq[i]], keys[seq[i]], stream)
+    for k in range(P):
         H.helios_plan_wait(plan, k, stream)
     H.helios_sync(c)
     torch.cuda.synchronize()
@@ -497,13 +509,13 @@ def main():
         end = torch.cuda.Event(enable_timing=True)
         start.record(stream)
         H.helios_plan_mark(plan, stream)
-        # device timing events on every batch of the last depth*1000 (all of them by default): the
-        # per-batch segments give the stage times and the union of the gather segments' intervals
-        timed_from = max(0, args.steps - depth * 1000)
+        # device timing events on every launch of the last depth*1000 (all of them by default): the
+        # per-launch segments give the stage times and the union of the gather segments' intervals
+        timed_from = max(0, args.steps - depth * 1000 * G)
         for i in range(args.steps):
             b = seq[args.warmup + i]
-            H.helios_plan_submit(plan, i % depth, seed_of[b], keys[b], stream, timing=(i >= timed_from))
-        for k in range(depth):
+            H.helios_plan_submit(plan, i % P, seed_of[b], keys[b], stream, timing=(i >= timed_from))
+        for k in range(P):
             H.helios_plan_wait(plan, k, stream)
         end.record(stream)
         torch.cuda.synchronize()
@@ -512,8 +524,8 @@ def main():
     staged_timed = c.info().staged_rows - staged0
     total_ms = start.elapsed_time(end)
     sample_ms, gather_ms, link_ms, gather_iv, link_iv = [], [], [], [], []
-    for k in range(depth):
-        n_k = sum(1 for i in range(k, args.steps, depth) if i >= timed_from)
+    for k in range(0, P, G):   # group leaders: one timing record per group launch (the launching submit)
+        n_k = sum(1 for i in range(k + G - 1, args.steps, P) if i >= timed_from)
         for back in range(n_k):
             tb = H.helios_plan_timing(plan, k, back)
             sample_ms.append(tb.sample_ms)
@@ -521,7 +533,7 @@ def main():
             gather_iv.append((tb.t_gather, tb.t_end))
             if tb.link_ms >= 0:
                 link_ms.append(tb.link_ms)
-    n_timed = len(gather_iv)
+    n_timed = len(gather_iv) * G   # batches of the timed launches
     gather_busy_ms = interval_union(gather_iv)
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     allreduce(t, dist.ReduceOp.MAX)
@@ -549,19 +561,19 @@ def main():
 
     # ---- e2e: through the public API with host buffers (host seeds in, counts + tier stats out) ----
     host_seeds = {b: np.ascontiguousarray(inp.batches[b]) for b in sorted(set(seq))}
-    out_host = np.empty((depth, L + 1 + 4), dtype=np.int64)
+    out_host = np.empty((P, L + 1 + 4), dtype=np.int64)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t_e2e = time.perf_counter()
     for i in range(args.steps):
         b = seq[args.warmup + i]
-        k = i % depth
-        if i >= depth:   # the slot's previous batch: its result must be on the host before reuse
+        k = i % P
+        if i >= P:   # the position's previous batch: its result must be on the host before reuse
             H.helios_plan_readback(plan, k, out_host[k])
         H.helios_plan_submit(plan, k, host_seeds[b], keys[b], stream, readback=True)
-    for i in range(max(0, args.steps - depth), args.steps):
-        H.helios_plan_readback(plan, i % depth, out_host[i % depth])
+    for i in range(max(0, args.steps - P), args.steps):
+        H.helios_plan_readback(plan, i % P, out_host[i % P])
     e2e_s = time.perf_counter() - t_e2e
     H.helios_sync(c)
     e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
@@ -575,7 +587,7 @@ def main():
         checked, ok = 0, True
         pb = sorted(set(seq))[: args.parity_batches]
         for j, b in enumerate(pb):   # the timed launch configuration: plan slots + CUDA graphs
-            k = j % depth
+            k = j % P
             H.helios_plan_submit(plan, k, seed_of[b], keys[b], stream)
             H.helios_plan_wait(plan, k, stream)
             H.helios_sync(c)
@@ -689,8 +701,8 @@ def main():
                 "busy_ms": round(gather_busy_ms, 3), "launches_timed": n_timed,
                 "note": "achieved = algorithmic tier bytes (HBM tier read + output write + ids/dir, PCIe host rows, "
                         "NVLink peer rows, storage) of the timed launches / union of their execution intervals "
-                        f"(CUDA events on the slot streams over the timed region; {depth} batches in flight, so "
-                        "launches overlap); peak = the same bytes / T_roof, the tier sum form "
+                        f"(CUDA events on the slot streams over the timed region; {P} batches in flight in {depth} "
+                        f"groups of {G}, each group one launch of every kernel, so launches overlap); peak = the same bytes / T_roof, the tier sum form "
                         "sum(bytes_link / BW_link); frac_throughput = T_roof / ms_per_step"}
     roof.update({
         "peaks_used": {"hbm_gbs": bw_hbm, "hbm_src": "MEASURED_PEAKS.json" if pk else "fallback",
@@ -736,8 +748,11 @@ def main():
                                      "as staged)"}
     value = world * steps / (max_ms / 1e3)
     e2e_val = world * steps / e2e_s
-    launches_per_step = (3 * L + 2 + 2 + ((2 if args.io_sync else 3) if c.info().file_rows > 0 else 0)
-                         + (1 if (args.host_staged > 0 and S > 0) else 0) + (1 if plan.link else 0))
+    # per group launch: the sampling chain (3L + 2 kernels), lookup + gather (2), the staged-tier publish;
+    # per batch: the IO kernel + its finish (file tier), the link-stream host kernel (G = 1 only)
+    per_group = 3 * L + 2 + 2 + (1 if (args.host_staged > 0 and S > 0) else 0)
+    per_batch = (2 if c.info().file_rows > 0 else 0) + (1 if plan.link else 0)
+    gpu_launches = per_group * ((steps + G - 1) // G) + per_batch * steps
     out = {
         "metric": "sampled+gathered mini-batches/sec (feature GB/s and tier-roofline fraction alongside)",
         "value": round(value, 3), "unit": "batches/s", "n_gpus": 1 if one_gpu else world, "steps": steps, "warmup": args.warmup,
@@ -747,16 +762,18 @@ def main():
         "config": {"workload": cfg.name, "desc": cfg.note, "V": cfg.V, "E": int(inp.graph.E), "dim": cfg.dim,
                    "file_tier": {"rows": int(c.info().file_rows), "direct_io": bool(c.info().direct_io),
                                  "io_rings": args.io_rings, "ring_depth": args.ring_depth, "io_ctas": args.io_ctas,
-                                 "io_mode": "sync (GIDS-style ablation)" if args.io_sync else "decoupled submit/complete"}
+                                 "io_mode": "sync (GIDS-style ablation)" if args.io_sync else "decoupled submit/complete",
+                                 "io_sms": int(c.info().io_sms) or "all (no partition)"}
                    if file_cfg else None,
                    "batch_per_rank": cfg.B, "fanouts": cfg.fanouts, "hbm_rows_per_gpu": Hr, "host_rows": S,
-                   "scale": s, "parallelism": f"dp{world} (seeds split per rank, HBM tier sharded)",
+                   "scale": s, "parallelism": f"dp{world} (seeds split per rank, HBM tier "
+                                              f"{'replicated' if args.hbm_replicated else 'sharded'})",
                    "host_tier": ("alias of canonical table (by id)" if args.host_alias else "packed, hot-rank order")
                    + (f"; dynamic split: GPU zero-copy from the front of each batch's host list, {args.stage_workers} "
                       f"host stager threads from its end (cap {args.host_staged:.0%}, last "
                       f"{min(args.stage_reserve, args.host_staged):.0%} reserved for the stagers)"
                       if args.host_staged > 0 else "; GPU zero-copy reads only (ablation)"),
-                   "batches_in_flight": depth, "cuda_graphs": not args.no_graph, "serial_gather": bool(args.serial_gather),
+                   "batches_in_flight": P, "plan_slots": depth, "batches_per_launch": G, "cuda_graphs": not args.no_graph, "serial_gather": bool(args.serial_gather),
                    "link_stream": bool(plan.link),
                    "intra_batch_pipeline": bool(args.intra),
                    "topology": "pinned host, zero-copy (UVA)" if args.topo_host else "HBM",
@@ -766,14 +783,14 @@ def main():
         "feature_gbs": round(world * n_rows / steps * R * steps / (max_ms / 1e3) / 1e9, 2),
         "stage_ms": {"sample": round(statistics.mean(sample_ms), 4), "gather": round(g_ms, 4),
                      "link_host_kernel": round(statistics.mean(link_ms), 4) if link_ms else None,
-                     "note": f"mean per batch, device events around the two graph segments of every timed batch ({n_timed}), {depth} batches in flight"},
+                     "note": f"mean per launch ({G} batch(es) each), device events around the two graph segments of every timed launch ({len(gather_iv)}), {P} batches in flight"},
         "lookups_per_s": round(world * nL * steps / (max_ms / 1e3)),
         "rows_per_batch": {"n_L": round(nL, 1), "hbm_local": round(n_local, 1), "hbm_peer": round(n_peer, 1),
                            "host": round(n_host, 1), "file": round(n_file, 1)},
         "roofline": roof,
         "e2e": {"value": round(e2e_val, 3), "unit": "batches/s", "h2d_bytes_per_step": cfg.B * 8,
                 "d2h_bytes_per_step": (L + 1 + 4) * 8},
-        "gpu_launches": launches_per_step * steps,
+        "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "parity": parity,

@@ -162,6 +162,9 @@ helios_status helios_presample(helios_graph* g, const int64_t* seeds, int64_t n_
                                            reading 14).  The GPU still initiates every request. */
 #define HELIOS_CACHE_IO_SYNC 0x40u      /* ablation: GIDS/BaM-style coupled IO, one warp per request does
                                            submit + completion poll + copy (§2.2)   */
+#define HELIOS_CACHE_HBM_REPLICATED 0x200u /* C5-rep ablation: every rank's HBM tier holds the
+                                           same hottest hbm_rows rows (directory of world_size 1: no peer
+                                           rows, no NVLink traffic); host_rows then count from hot rank H */
 #define HELIOS_CACHE_IO_FAULT_AT 0x100u  /* test builds: IO workers fail the io_fault_at-th read  */
 
 typedef struct {
@@ -193,6 +196,12 @@ typedef struct {
                                  such a chunk waits up to 200 us for a stager to claim it (and the steal
                                  timeout for a claimed one) before copying it zero-copy itself.  0 = none:
                                  the pure dynamic split (whoever reaches a chunk first copies it).   */
+  int32_t io_sms;             /* > 0 (with a file tier): run the IO kernel on a CUDA green context holding
+                                 this many SMs (rounded up to the driver's granularity, 8 on sm_100), the
+                                 in-process analog of the paper's MPS cap on operator SMs (PAPER.md:244,
+                                 :352-357); everything else keeps the whole GPU.  0 = no partition.
+                                 E_INVALID if the device cannot be split so; helios_cache_query reports
+                                 the SMs provisioned. */
 } helios_cache_desc;
 
 /* Builds the directory and fills the tiers (blocking).  The HBM tier is filled from host_table
@@ -210,6 +219,7 @@ typedef struct {
   int32_t io_rings, ring_depth, direct_io;
   int64_t io_reads;           /* file reads completed by the IO workers since build */
   int64_t staged_rows;        /* HOST_STAGED: host-tier rows copied by the stager threads since build */
+  int32_t io_sms;             /* SMs of the IO green context (0 = the IO kernel may use every SM)   */
 } helios_cache_info;
 helios_status helios_cache_query(const helios_cache* c, helios_cache_info* out);
 
@@ -288,6 +298,7 @@ helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64
 #define HELIOS_SUBMIT_TIMING 0x2u      /* record device timing events around the sample / gather phases */
 #define HELIOS_SUBMIT_READBACK 0x4u    /* copy the batch's level counts and tier stats to plan-owned pinned
                                           host memory at its end (read with helios_plan_readback) */
+#define HELIOS_SUBMIT_FLUSH 0x8u       /* group > 1: launch the position's group now, even if not full */
 typedef struct helios_plan helios_plan;
 typedef struct {
   int64_t max_seeds;
@@ -295,6 +306,15 @@ typedef struct {
   int32_t fanouts[HELIOS_MAX_HOPS];
   int32_t depth;
   uint32_t flags;
+  int32_t group;   /* batches per slot, 1..4 (0 = 1).  With group G > 1 the plan has depth x G batch
+                      POSITIONS (the `slot` argument of every plan call below is a position): positions
+                      g*G .. g*G+G-1 form slot g, whose batches run as one group, each kernel of the
+                      chain launched once for all G of them (gridDim.y = G, every batch with its own
+                      table, scan state and outputs: results are those of G separate submits).  A
+                      submit to the slot's last position launches the group, as does
+                      HELIOS_SUBMIT_FLUSH or a helios_plan_wait on a position of a partly submitted
+                      group (positions not submitted run as empty batches).  Timing is per group.
+                      Not combinable with INTRA_BATCH, LINK_STREAM or TRACE (E_INVALID). */
 } helios_plan_desc;
 helios_status helios_plan_create(helios_graph* g, helios_cache* c, const helios_plan_desc* desc, helios_plan** out);
 /* Free a plan before the cache and graph it was created on. */

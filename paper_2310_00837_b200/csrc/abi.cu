@@ -317,14 +317,15 @@ helios_status helios_cache_query(const helios_cache* c, helios_cache_info* o) {
   o->host_rows = c->S;
   o->file_rows = c->file_rows;
   o->row_bytes = c->R;
-  o->world_size = c->G;
-  o->rank = c->rank;
+  o->world_size = c->world;
+  o->rank = c->world_rank;
   o->peers_attached = c->peers_attached;
   o->io_rings = c->io.rings;
   o->ring_depth = c->io.depth;
   o->direct_io = c->io.direct ? 1 : 0;
   o->io_reads = c->io.reads.load();
   o->staged_rows = stager_rows(c);
+  o->io_sms = c->green_sms;
   return HELIOS_OK;
 }
 
@@ -450,6 +451,13 @@ helios_status helios_plan_create(helios_graph* g, helios_cache* c, const helios_
 #endif
   p->link = c && c->S > 0 && !p->intra && !p->serial_gather && (d->flags & HELIOS_PLAN_LINK_STREAM);
   HCHECK(!p->intra || p->graphs, HELIOS_E_INVALID, "HELIOS_PLAN_INTRA_BATCH needs CUDA graphs");
+  p->G = d->group > 0 ? d->group : 1;
+  if (p->G < 1 || p->G > kMaxGroup || (p->G > 1 && (p->intra || p->link || p->trace))) {
+    const int G = p->G;
+    delete p;
+    return fail(HELIOS_E_INVALID, "plan group %d (need 1..%d, and 1 with INTRA_BATCH / LINK_STREAM / TRACE)", G,
+                kMaxGroup);
+  }
   helios_status st = plan_create_impl(p);
   if (st != HELIOS_OK) {
     std::string keep = helios_last_error();

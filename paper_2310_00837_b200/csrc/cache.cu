@@ -177,6 +177,48 @@ static helios_status fill_tier_from_file(helios_cache* c, const int32_t* h_ids, 
   return HELIOS_OK;
 }
 
+// HBM tier fill from the (unregistered) canonical host table: host threads gather the rows of ids
+// into one of two pinned chunks while the other chunk's copy to the GPU is in flight.
+static helios_status fill_hbm_from_table(helios_cache* c, const int32_t* h_ids, int64_t n, char* dst) {
+  const int64_t chunk_rows = std::max<int64_t>(1, (64ll << 20) / c->R);
+  char* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaStream_t st = nullptr;
+  helios_status s = HELIOS_OK;
+  auto run = [&]() -> helios_status {
+    for (int b = 0; b < 2; b++) {
+      HCUDA(cudaHostAlloc(&buf[b], chunk_rows * (int64_t)c->R, cudaHostAllocDefault));
+      HCUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+    }
+    HCUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    const int T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    for (int64_t k = 0, i0 = 0; i0 < n; k++, i0 += chunk_rows) {
+      const int b = (int)(k & 1);
+      const int64_t m = std::min(chunk_rows, n - i0);
+      HCUDA(cudaEventSynchronize(ev[b]));  // the copy that last read this chunk is done
+      std::vector<std::thread> th;
+      for (int t = 0; t < T; t++)
+        th.emplace_back([&, t]() {
+          for (int64_t j = m * t / T; j < m * (t + 1) / T; j++)
+            memcpy(buf[b] + j * c->R, (const char*)c->host_table + (int64_t)h_ids[i0 + j] * c->R, c->R);
+        });
+      for (auto& x : th) x.join();
+      HCUDA(cudaMemcpyAsync(dst + i0 * (int64_t)c->R, buf[b], m * (int64_t)c->R, cudaMemcpyHostToDevice, st));
+      HCUDA(cudaEventRecord(ev[b], st));
+    }
+    HCUDA(cudaStreamSynchronize(st));
+    return HELIOS_OK;
+  };
+  s = run();
+  if (st) cudaStreamSynchronize(st);
+  for (int b = 0; b < 2; b++) {
+    if (ev[b]) cudaEventDestroy(ev[b]);
+    if (buf[b]) cudaFreeHost(buf[b]);
+  }
+  if (st) cudaStreamDestroy(st);
+  return s;
+}
+
 helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, helios_cache* c) {
   c->g = g;
   c->device = g->device;
@@ -185,6 +227,12 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
   c->R = d->row_bytes;
   c->G = d->world_size;
   c->rank = d->rank;
+  c->world = d->world_size;
+  c->world_rank = d->rank;
+  if (d->flags & HELIOS_CACHE_HBM_REPLICATED) {  // C5-rep: every rank holds the same hottest H rows, so
+    c->G = 1;                                     // the directory is the single-GPU one (no peers)
+    c->rank = 0;
+  }
   c->H = d->hbm_rows;
   c->S = d->host_rows;
   c->flags = d->flags;
@@ -223,7 +271,11 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
   }
   // register the canonical host table (zero-copy source for fills and, with ALIAS, the host tier)
   char* table_dev = nullptr;
-  if (c->host_table) {
+  // The canonical table is registered (pinned + mapped) only when the GPU reads it zero-copy, i.e. when
+  // the host tier aliases it (HOST_ALIAS) or the caller mapped it already (TABLE_MAPPED).  Otherwise
+  // the HBM shard is filled by host threads gathering its rows into pinned chunks copied to the GPU,
+  // so a rank never pins the whole table (57 GB at C3) just to read its 1/G share of the hottest rows.
+  if (c->host_table && (alias || (c->flags & HELIOS_CACHE_TABLE_MAPPED))) {
     if (!(c->flags & HELIOS_CACHE_TABLE_MAPPED)) {
       cudaError_t e = cudaHostRegister((void*)c->host_table, (size_t)V * c->R,
                                        cudaHostRegisterMapped | cudaHostRegisterReadOnly);
@@ -252,6 +304,10 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
     k_shard_ids<<<c->sms * 4, 256>>>(d_order, H_eff, c->G, c->rank, d_ids);
     if (table_dev) {
       st = gather_rows_by_id(table_dev, c->R, d_ids, H_eff, c->hbm, c->sms, 0);
+    } else if (c->host_table) {
+      std::vector<int32_t> h_ids(H_eff);
+      HCUDA(cudaMemcpy(h_ids.data(), d_ids, H_eff * 4, cudaMemcpyDeviceToHost));
+      st = fill_hbm_from_table(c, h_ids.data(), H_eff, c->hbm);
     } else {
       std::vector<int32_t> h_ids(H_eff);
       HCUDA(cudaMemcpy(h_ids.data(), d_ids, H_eff * 4, cudaMemcpyDeviceToHost));
@@ -335,7 +391,14 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
   // streams / events for the IO kernels
   int lo, hi;
   HCUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  HCUDA(cudaStreamCreateWithPriority(&c->s_submit, cudaStreamNonBlocking, hi));
+  if (d->io_sms > 0 && c->has_file) {  // IO kernels confined to an SM partition (green context)
+    int dev = 0;
+    HCUDA(cudaGetDevice(&dev));
+    st = green_io_start(c, dev, d->io_sms, hi);
+    if (st != HELIOS_OK) return st;
+  } else {
+    HCUDA(cudaStreamCreateWithPriority(&c->s_submit, cudaStreamNonBlocking, hi));
+  }
   HCUDA(cudaEventCreateWithFlags(&c->ev_lookup, cudaEventDisableTiming));
   HCUDA(cudaEventCreateWithFlags(&c->ev_submit, cudaEventDisableTiming));
   HCUDA(cudaEventCreateWithFlags(&c->ev_io_done, cudaEventDisableTiming));
@@ -350,6 +413,7 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
     int per_sm = 1;
     if (const char* e = getenv("HELIOS_GATHER_CTAS_PER_SM")) per_sm = std::max(1, std::min(atoi(e), 4));
     if (const char* e = getenv("HELIOS_GATHER_BULK")) c->gather_bulk = atoi(e) != 0;
+    if (const char* e = getenv("HELIOS_GATHER_VU")) c->gather_vu = atoi(e) == 16 ? 16 : 8;
     if (c->gather_bulk) per_sm = 1;  // 192 KB of shared memory per CTA
     c->gather_ctas = c->sms * per_sm;
   }
@@ -378,6 +442,7 @@ void cache_free_impl(helios_cache* c) {
   if (c->dir) cudaFree(c->dir);
   if (c->d_peers) cudaFree(c->d_peers);
   if (c->d_err) cudaFree(c->d_err);
+  if (c->green) green_io_stop(c);
   if (c->s_submit) cudaStreamDestroy(c->s_submit);
   if (c->ev_lookup) cudaEventDestroy(c->ev_lookup);
   if (c->ev_submit) cudaEventDestroy(c->ev_submit);

@@ -80,31 +80,35 @@ __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
   asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+__device__ __forceinline__ uint4 ld_volatile_v4u32(const void* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
 
-// Open-addressing (linear probing) insert-or-find of key u; returns the slot, *fresh = created here.
-__device__ __forceinline__ uint32_t table_insert(TableSlot* tab, uint32_t mask, uint32_t u, bool* fresh) {
+// Open-addressing (linear probing) insert-or-find of key u at edge position e: returns the slot,
+// *fresh = created here (with minpos = e); an existing slot's minpos is lowered to e if larger.
+__device__ __forceinline__ uint32_t table_insert(TableSlot* tab, uint32_t mask, uint32_t u, uint32_t e, bool* fresh) {
+  const unsigned long long want = ((unsigned long long)u << 32) | e;
   uint32_t s = hash32(u) & mask;
   for (;;) {
-    uint32_t k = ld_volatile_u32(&tab[s].key);
-    if (k == u) {
-      *fresh = false;
-      return s;
-    }
-    if (k == kEmpty) {
-      uint32_t prev = atomicCAS(&tab[s].key, kEmpty, u);
-      if (prev == kEmpty) {
+    unsigned long long w = ld_volatile_u64(&tab[s].km);
+    if ((uint32_t)(w >> 32) == kEmpty) {
+      w = atomicCAS(&tab[s].km, kEmptyKM, want);
+      if (w == kEmptyKM) {
         *fresh = true;
         return s;
       }
-      if (prev == u) {
-        *fresh = false;
-        return s;
-      }
+    }
+    if ((uint32_t)(w >> 32) == u) {
+      if ((uint32_t)w > e) atomicMin(&tab[s].km, want);
+      *fresh = false;
+      return s;
     }
     s = (s + 1) & mask;
   }

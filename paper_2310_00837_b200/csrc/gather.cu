@@ -38,17 +38,38 @@ struct ListPtrs {
 // K3: one thread per row of N_L: dir[v] -> tier list (local HBM / peer HBM / host / file), appended
 // with warp-aggregated atomics.  The list counts are the per-tier row counts.
 // Rows [*lo, *hi) of N_L (lo = NULL: from 0); the intra-batch pipeline runs one pass per node range.
-__global__ void __launch_bounds__(256) k_lookup(const int64_t* __restrict__ nodes, const int64_t* __restrict__ lo_ptr,
-                                                const int64_t* __restrict__ n_nodes,
-                                                const int64_t* __restrict__ dir, int64_t V, int32_t rank, ListPtrs L,
-                                                unsigned long long* ctl, int* err, const int64_t* trace_params,
-                                                int trace_idx) {
+struct LookupArgs {
+  const int64_t* nodes;
+  const int64_t* lo_ptr;
+  const int64_t* n_nodes;
+  const int64_t* dir;
+  int64_t V;
+  int32_t rank;
+  ListPtrs L;
+  unsigned long long* ctl;
+  int* err;
+  const int64_t* trace_params;
+  int trace_idx;
+};
+struct LookupGroup {  // the batches of one launch (gridDim.y), as SampleGroup
+  LookupArgs a[kMaxGroup];
+};
+__global__ void __launch_bounds__(256) k_lookup(const __grid_constant__ LookupGroup P) {
+  const LookupArgs& A = P.a[blockIdx.y];
+  const int64_t* __restrict__ nodes = A.nodes;
+  const int64_t* __restrict__ dir = A.dir;
+  const int64_t* lo_ptr = A.lo_ptr;
+  const ListPtrs& L = A.L;
+  unsigned long long* ctl = A.ctl;
+  const int64_t V = A.V;
+  const int32_t rank = A.rank;
+  int* err = A.err;
   pdl_wait();  // N_L is final once the sampling chain's last kernel has completed
   pdl_trigger();
-  TraceScope ts(trace_params, trace_idx);
+  TraceScope ts(A.trace_params, A.trace_idx);
   const int lane = threadIdx.x & 31;
   const int64_t lo = lo_ptr ? *lo_ptr : 0;
-  const int64_t n = *n_nodes - lo;
+  const int64_t n = *A.n_nodes - lo;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < n; base += stride) {
     const int64_t i = lo + base + lane;
@@ -90,7 +111,15 @@ __device__ __forceinline__ void st_release_sys_u32_(uint32_t* p, uint32_t v) {
 // Staged mode (dynamic split): post the batch's mailbox {seq, n_host} (release,
 // system scope) for the host stagers, which then claim 64-row chunks of the host list from its END
 // while the GPU's host-row warps take rows from its FRONT (host_rows_dyn).
-__global__ void k_stage_publish(unsigned long long* ctl, uint32_t* seq_ctr, uint32_t* mail) {
+struct PublishGroup {
+  unsigned long long* ctl[kMaxGroup];
+  uint32_t* seq[kMaxGroup];
+  uint32_t* mail[kMaxGroup];
+};
+__global__ void k_stage_publish(const __grid_constant__ PublishGroup P) {
+  unsigned long long* ctl = P.ctl[blockIdx.y];
+  uint32_t* seq_ctr = P.seq[blockIdx.y];
+  uint32_t* mail = P.mail[blockIdx.y];
   pdl_wait();
   pdl_trigger();
   const int64_t n_host = (int64_t)ctl[kListHost];
@@ -116,6 +145,7 @@ struct GatherArgs {
   unsigned long long* hint; // device alias of the pinned front hint ((seq << 32) | chunk the GPU reached)
   float stage_reserve;      // share of the batch's chunks (from the list's end) left to the stagers
   int64_t stage_max_chunks; // chunks the staging buffer holds (the stagers never claim more)
+  bool vu16;                // HBM / peer rows: 16 (else 8) 16-byte loads in flight per lane
   int* err;
   const char* hbm;          // this rank's shard
   char* const* peers;       // device [G]
@@ -447,8 +477,14 @@ __device__ __forceinline__ void host_rows_dyn(const GatherArgs& a, int64_t n_hos
 
 // HOST = false: the instantiation for caches without a host tier (no host-row code, so the HBM copy
 // loop alone sets the register budget).
-template <int VPL, int UH, bool BULK, bool HOST>
-__global__ void __launch_bounds__(256, 2) k_gather_lists(GatherArgs a) {
+struct GatherGroup {  // the batches of one launch (gridDim.y), as SampleGroup
+  GatherArgs a[kMaxGroup];
+};
+// VU: 16-byte loads in flight per lane for HBM / peer rows (8: 2 CTAs per SM fit the register file;
+// 16: HELIOS_GATHER_VU=16, one CTA per SM).
+template <int VPL, int UH, bool BULK, bool HOST, int VU>
+__global__ void __launch_bounds__(256, VU > 8 ? 1 : 2) k_gather_lists(const __grid_constant__ GatherGroup P) {
+  const GatherArgs& a = P.a[blockIdx.y];
   pdl_wait();
   pdl_trigger();
   TraceScope ts(a.part == kPartHost ? nullptr : a.trace_params, a.trace_idx);
@@ -503,8 +539,8 @@ __global__ void __launch_bounds__(256, 2) k_gather_lists(GatherArgs a) {
     bulk_rows(a, kListLocal, n_local, dw, n_dw, lane, stage0, bars[wi], phase);
     bulk_wait0();  // this lane's row stores are complete before the kernel ends
   } else {
-    flat_rows<8>(a, kListPeer, n_peer, dw, n_dw, lane, nvec);
-    flat_rows<8>(a, kListLocal, n_local, dw, n_dw, lane, nvec);
+    flat_rows<VU>(a, kListPeer, n_peer, dw, n_dw, lane, nvec);
+    flat_rows<VU>(a, kListLocal, n_local, dw, n_dw, lane, nvec);
   }
 }
 
@@ -763,32 +799,40 @@ helios_status io_preload_kernels() {
 constexpr int kBulkSmem = 8 * 2 * kBulkWarpBytes;
 
 template <int VPL, int UH, bool HOST>
-static void launch_gather(const GatherArgs& a, int grid, bool bulk, cudaStream_t st) {
+static void launch_gather(const GatherGroup& P, int n, int grid, bool bulk, cudaStream_t st) {
   if (bulk) {
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_gather_lists<VPL, UH, true, HOST>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
+      cudaFuncSetAttribute(k_gather_lists<VPL, UH, true, HOST, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kBulkSmem);
       attr = true;
     }
-    launch_pdl_smem(k_gather_lists<VPL, UH, true, HOST>, dim3(grid), dim3(256), kBulkSmem, st, a);
+    launch_pdl_smem(k_gather_lists<VPL, UH, true, HOST, 8>, dim3(grid, n), dim3(256), kBulkSmem, st, P);
+  } else if (P.a[0].vu16) {
+    launch_pdl(k_gather_lists<VPL, UH, false, HOST, 16>, dim3(grid, n), dim3(256), st, P);
   } else {
-    launch_pdl(k_gather_lists<VPL, UH, false, HOST>, dim3(grid), dim3(256), st, a);
+    launch_pdl(k_gather_lists<VPL, UH, false, HOST, 8>, dim3(grid, n), dim3(256), st, P);
   }
 }
 
 template <bool HOST>
-static void launch_gather_rows(const GatherArgs& a, int grid, bool bulk, cudaStream_t st) {
-  const int nvec = a.R / 16;
-  if (nvec <= 32) launch_gather<1, 8, HOST>(a, grid, bulk, st);
-  else if (nvec <= 64) launch_gather<2, 4, HOST>(a, grid, bulk, st);
-  else if (nvec <= 128) launch_gather<4, 2, HOST>(a, grid, bulk, st);
-  else launch_gather<8, 1, HOST>(a, grid, bulk, st);
+static void launch_gather_rows(const GatherGroup& P, int n, int grid, bool bulk, cudaStream_t st) {
+  const int nvec = P.a[0].R / 16;
+  if (nvec <= 32) launch_gather<1, 8, HOST>(P, n, grid, bulk, st);
+  else if (nvec <= 64) launch_gather<2, 4, HOST>(P, n, grid, bulk, st);
+  else if (nvec <= 128) launch_gather<4, 2, HOST>(P, n, grid, bulk, st);
+  else launch_gather<8, 1, HOST>(P, n, grid, bulk, st);
 }
 
 // host: the cache has a host tier (else the lean HBM-only instantiation)
+static void launch_gather_any(const GatherGroup& P, int n, int grid, bool bulk, bool host, cudaStream_t st) {
+  if (host) launch_gather_rows<true>(P, n, grid, bulk, st);
+  else launch_gather_rows<false>(P, n, grid, bulk, st);
+}
 static void launch_gather_any(const GatherArgs& a, int grid, bool bulk, bool host, cudaStream_t st) {
-  if (host) launch_gather_rows<true>(a, grid, bulk, st);
-  else launch_gather_rows<false>(a, grid, bulk, st);
+  GatherGroup P{};
+  P.a[0] = a;
+  launch_gather_any(P, 1, grid, bulk, host, st);
 }
 
 void gws_free(GatherWS& w) {
@@ -862,6 +906,7 @@ static GatherArgs make_args(helios_cache* c, GatherWS& w, void* out, helios_gath
   a.hint = w.d_hint;
   a.stage_reserve = c->stage_reserve;
   a.stage_max_chunks = w.stage_rows / kStageChunk;
+  a.vu16 = c->gather_vu == 16;
   a.err = c->d_err;
   a.hbm = c->hbm;
   a.peers = c->d_peers;
@@ -872,27 +917,65 @@ static GatherArgs make_args(helios_cache* c, GatherWS& w, void* out, helios_gath
   return a;
 }
 
-// One lookup + gather pass over rows [*lo, *n_nodes) (lo = NULL: all).  first: reset every count;
-// otherwise (later intra-batch passes) only the per-pass tier counts and row tickets are reset, so
-// the file list and the stats accumulate over the passes of a batch.
+// One lookup + gather pass over rows [*lo, *n_nodes) (lo = NULL: all) of each of the n batches of a
+// group (one launch of each kernel, gridDim.y = n).  first: reset every count; otherwise (later
+// intra-batch passes, n = 1) only the per-pass tier counts and row tickets are reset, so the file
+// list and the stats accumulate over the passes of a batch.
+static helios_status gather_pass_group(helios_cache* c, GatherWS* const* ws, const int64_t* const* nodes,
+                                       const int64_t* lo, const int64_t* const* n_nodes, int n, int64_t max_rows,
+                                       void* const* out, helios_gather_stats* const* stats, bool first, bool accumulate,
+                                       int part, cudaStream_t st) {
+  HCHECK(!c->broken, HELIOS_E_STATE, "cache unusable after an IO / staging watchdog timeout");
+  HCHECK(n >= 1 && n <= kMaxGroup, HELIOS_E_INVALID, "group of %d batches (1..%d)", n, kMaxGroup);
+  LookupGroup LP{};
+  GatherGroup GP{};
+  PublishGroup PP{};
+  bool staged = false;
+  for (int b = 0; b < n; b++) {
+    GatherWS& w = *ws[b];
+    if (first) {
+      if (!w.ctl_preset) HCUDA(cudaMemsetAsync(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long), st));
+    } else {
+      HCUDA(cudaMemsetAsync(w.d_ctl, 0, kListFile * sizeof(unsigned long long), st));
+      HCUDA(cudaMemsetAsync(w.d_ctl + kCtlHostTicket, 0, sizeof(unsigned long long), st));
+    }
+    GP.a[b] = make_args(c, w, out[b], stats[b], accumulate, part);
+    LP.a[b] = LookupArgs{nodes[b], lo, n_nodes[b], (const int64_t*)c->dir, c->V, c->rank, GP.a[b].L, w.d_ctl,
+                         c->d_err, w.trace_params, w.trace_idx};
+    PP.ctl[b] = w.d_ctl;
+    PP.seq[b] = w.d_seq;
+    PP.mail[b] = w.d_mail;
+    staged = GP.a[b].staged;
+  }
+  const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_rows + 255) / 256), (int64_t)c->sms * 2);
+  launch_pdl(k_lookup, dim3(lg, n), dim3(256), st, LP);
+  if (staged) launch_pdl(k_stage_publish, dim3(1, n), dim3(1), st, PP);
+  launch_gather_any(GP, n, c->gather_ctas, c->gather_bulk, c->S > 0, st);
+  HCUDA(cudaGetLastError());
+  return HELIOS_OK;
+}
+
 static helios_status gather_pass(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* lo,
                                  const int64_t* n_nodes, int64_t max_rows, void* out, helios_gather_stats* stats,
                                  bool first, bool accumulate, int part, cudaStream_t st) {
-  HCHECK(!c->broken, HELIOS_E_STATE, "cache unusable after an IO / staging watchdog timeout");
-  if (first) {
-    if (!w.ctl_preset) HCUDA(cudaMemsetAsync(w.d_ctl, 0, kCtlWords * sizeof(unsigned long long), st));
-  } else {
-    HCUDA(cudaMemsetAsync(w.d_ctl, 0, kListFile * sizeof(unsigned long long), st));
-    HCUDA(cudaMemsetAsync(w.d_ctl + kCtlHostTicket, 0, sizeof(unsigned long long), st));
+  GatherWS* ws[1] = {&w};
+  const int64_t* nd[1] = {nodes};
+  const int64_t* nn[1] = {n_nodes};
+  void* o[1] = {out};
+  helios_gather_stats* sts[1] = {stats};
+  return gather_pass_group(c, ws, nd, lo, nn, 1, max_rows, o, sts, first, accumulate, part, st);
+}
+
+helios_status gather_launch_group(helios_cache* c, GatherWS* const* ws, const int64_t* const* nodes,
+                                  const int64_t* const* n_nodes, int n, int64_t max_nodes, void* const* out,
+                                  helios_gather_stats* const* stats, cudaStream_t st) {
+  HCHECK(c->G == 1 || c->peers_attached, HELIOS_E_STATE, "world_size %d but peers not attached", c->G);
+  for (int b = 0; b < n; b++) {
+    HCHECK(nodes[b] && n_nodes[b] && (out[b] || max_nodes == 0), HELIOS_E_INVALID, "null gather argument");
+    HCHECK(ws[b]->d_ctl && max_nodes <= ws[b]->cap, HELIOS_E_CAPACITY, "max_nodes %lld > gather list cap %lld",
+           (long long)max_nodes, (long long)ws[b]->cap);
   }
-  GatherArgs a = make_args(c, w, out, stats, accumulate, part);
-  const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_rows + 255) / 256), (int64_t)c->sms * 2);
-  launch_pdl(k_lookup, dim3(lg), dim3(256), st, nodes, lo, n_nodes, (const int64_t*)c->dir, c->V, c->rank, a.L, w.d_ctl,
-             c->d_err, w.trace_params, w.trace_idx);
-  if (a.staged) launch_pdl(k_stage_publish, dim3(1), dim3(1), st, w.d_ctl, w.d_seq, w.d_mail);
-  launch_gather_any(a, c->gather_ctas, c->gather_bulk, c->S > 0, st);
-  HCUDA(cudaGetLastError());
-  return HELIOS_OK;
+  return gather_pass_group(c, ws, nodes, nullptr, n_nodes, n, max_nodes, out, stats, true, false, kPartAll, st);
 }
 
 helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes,

@@ -82,6 +82,7 @@ inline cudaError_t launch_pdl_smem(void (*kernel)(KArgs...), dim3 grid, dim3 blo
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+constexpr int kMaxGroup = 4;                // batches per plan-slot group (one launch of each kernel)
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // empty hash key / unassigned local id / no minpos
 constexpr int kScanBlock = 256;
 constexpr int kScanItems = 4;
@@ -95,12 +96,17 @@ struct ScanState {
 
 // One slot of the per-batch open-addressing table (array of structs: an insert, its atomicMin and
 // the later local-id reads all touch one 16 B slot, i.e. one 32 B sector, not three arrays).
+// key and minpos share one 64-bit word (key in the high half): the insert's CAS claims a free slot
+// with the edge position already in it, and a later occurrence lowers minpos with one 64-bit
+// atomicMin (same key, so the word order is the position order) issued only when the word it read
+// holds a larger position -- no separate read of `local` on the insert path.
 struct alignas(16) TableSlot {
-  uint32_t key;     // vertex id, kEmpty = free
-  uint32_t minpos;  // first edge position of an id new at this hop (atomicMin)
-  uint32_t local;   // local id in N_L once assigned, kEmpty = not yet
+  unsigned long long km;  // (key << 32) | minpos; all-ones = free.  minpos: first edge position of an
+                          // id new at this hop (meaningless once `local` is set)
+  uint32_t local;         // local id in N_L once assigned, kEmpty = not yet
   uint32_t pad;
 };
+constexpr unsigned long long kEmptyKM = ~0ull;
 
 // Sampling workspace: one per sampling context (the graph's default context, and one per plan
 // slot so that consecutive batches can be in flight concurrently).
@@ -258,8 +264,10 @@ struct helios_cache {
   int* d_err = nullptr;           // device latched error
   std::string path;
   int64_t header = 0, stride = 0;
+  int world = 1, world_rank = 0;    // the caller's world size / rank (G, rank: the directory's)
   int io_ctas = 32;
   int gather_ctas = 148;            // K4 grid (one CTA per SM with a host tier, more for HBM-only caches)
+  int gather_vu = 8;                // HBM / peer rows: 16-byte loads in flight per lane (HELIOS_GATHER_VU)
   bool gather_bulk = false;         // HELIOS_GATHER_BULK=1: HBM rows by cp.async.bulk (ablation)
   bool io_sync = false;            // HELIOS_CACHE_IO_SYNC ablation
   bool broken = false;             // a ring / staging watchdog fired: ring state is no longer consistent
@@ -273,6 +281,8 @@ struct helios_cache {
   helios::Stager* stager = nullptr;
   helios::GatherWS gws;            // default gather context (helios_gather / helios_batch_prepare)
   cudaStream_t s_submit = nullptr;  // IO stream: k_io of successive batches, serialised (ring sequences)
+  void* green = nullptr;            // CUgreenCtx of the IO SM partition (io_sms > 0), s_submit belongs to it
+  int green_sms = 0;                // SMs actually provisioned for it
   cudaEvent_t ev_lookup = nullptr, ev_submit = nullptr, ev_io_done = nullptr;
   bool io_pending = false;         // ev_io_done recorded at least once
 };
@@ -305,6 +315,10 @@ struct PlanSlot {
   int64_t count = 0;              // batches submitted to this slot
   int64_t tcount = 0;             // timed batches submitted to this slot
   bool submitted = false;
+  // plan groups (desc.group G > 1): every position has its own workspaces and outputs (above); the
+  // group's first position (the leader) owns the stream, graphs and events used for all G.
+  bool staged = false;            // parameters uploaded, group not launched yet
+  bool rb_req = false;            // readback requested by this position's pending submit
 };
 
 }  // namespace helios
@@ -331,6 +345,7 @@ struct helios_plan {
   cudaEvent_t ev_ref = nullptr;           // helios_plan_mark: origin of the t_* timings
   bool marked = false;
   bool gather_chained = false;
+  int G = 1;                              // batches per slot (desc.group); slots = depth x G positions
   std::vector<helios::PlanSlot> slots;
 };
 
@@ -353,6 +368,10 @@ helios_status ws_upload_params(SampleWS& w, uint64_t key, int64_t B, const int64
 helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const int32_t* fanouts, int32_t L,
                             const helios_blocks* out, cudaStream_t st,
                             const std::function<helios_status(int)>* stage_hook = nullptr);
+// n batches (1..kMaxGroup) in one launch of each kernel (gridDim.y = n); ws[b] / outs[b] per batch.
+helios_status sample_launch_group(helios_graph* g, SampleWS* const* ws, const helios_blocks* const* outs, int n,
+                                  int64_t B_max, const int32_t* fanouts, int32_t L, cudaStream_t st,
+                                  const std::function<helios_status(int)>* hook = nullptr);
 helios_status hot_count_enqueue(const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes, int64_t V, uint64_t* hot,
                                 int sms, cudaStream_t st);
 helios_status gws_ensure(helios_cache* c, GatherWS& w, int64_t max_nodes);
@@ -361,6 +380,10 @@ void gws_free(GatherWS& w);
 // file list for io_launch.
 helios_status gather_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* n_nodes, int64_t max_nodes,
                             void* out, helios_gather_stats* stats, cudaStream_t st);
+// The same for the n batches of a plan-slot group (one launch of each kernel, gridDim.y = n).
+helios_status gather_launch_group(helios_cache* c, GatherWS* const* ws, const int64_t* const* nodes,
+                                  const int64_t* const* n_nodes, int n, int64_t max_nodes, void* const* out,
+                                  helios_gather_stats* const* stats, cudaStream_t st);
 // Link mode, first half (slot stream): K3 lookup + K4 over the HBM tiers only (stats written).
 helios_status gather_hbm_launch(helios_cache* c, GatherWS& w, const int64_t* nodes, const int64_t* n_nodes,
                                 int64_t max_nodes, void* out, helios_gather_stats* stats, cudaStream_t st);
@@ -388,6 +411,8 @@ helios_status io_start(helios_cache* c, const helios_cache_desc* d);
 void io_worker(helios_cache* c, int ring);  // host IO worker draining SQ ring `ring` (io_workers.cu)
 helios_status io_preload_kernels();
 void io_stop(helios_cache* c);
+helios_status green_io_start(helios_cache* c, int device, int io_sms, int priority);  // green.cu
+void green_io_stop(helios_cache* c);
 helios_status stager_start(helios_cache* c);
 void stager_stop(helios_cache* c);
 int64_t stager_rows(const helios_cache* c);  // rows the stagers copied since build (0 without stagers)

@@ -74,7 +74,8 @@ helios_status plan_create_impl(helios_plan* p) {
   int64_t lvl[HELIOS_MAX_HOPS + 1], edg[HELIOS_MAX_HOPS];
   helios_status s = sample_bounds(d.max_seeds, d.fanouts, d.L, g->V, g->E, &p->maxn, lvl, edg);
   if (s != HELIOS_OK) return s;
-  p->slots.resize(d.depth);
+  const int G = p->G;
+  p->slots.resize((size_t)d.depth * G);
   HCUDA(cudaEventCreateWithFlags(&p->ev_gather_chain, cudaEventDisableTiming));
   HCUDA(cudaEventCreate(&p->ev_ref));
   if (p->link) {
@@ -83,7 +84,7 @@ helios_status plan_create_impl(helios_plan* p) {
     if (const char* e = getenv("HELIOS_PLAN_LINKS")) p->n_links = std::max(1, std::min(atoi(e), helios_plan::kMaxLinks));
     for (int i = 0; i < p->n_links; i++) HCUDA(cudaStreamCreateWithPriority(&p->s_link[i], cudaStreamNonBlocking, greatest));
   }
-  for (int k = 0; k < d.depth; k++) {
+  for (int k = 0; k < d.depth * G; k++) {  // per position: workspaces and outputs
     PlanSlot& sl = p->slots[k];
     // output blocks: one allocation
     size_t bytes = p->maxn * 8 + (d.L + 1) * 8 + HELIOS_MAX_HOPS * 8 + 256;
@@ -116,8 +117,28 @@ helios_status plan_create_impl(helios_plan* p) {
     }
     s = ws_ensure(g, sl.ws, d.max_seeds, d.fanouts, d.L);
     if (s != HELIOS_OK) return s;
-    HCUDA(cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking));
     HCUDA(cudaHostAlloc(&sl.h_rb, (HELIOS_MAX_HOPS + 1 + 4) * sizeof(int64_t), cudaHostAllocDefault));
+  }
+  for (int k = 0; k < d.depth * G; k += G) {  // per slot (group leader): stream, events, graphs
+    PlanSlot& sl = p->slots[k];
+    SampleWS* gws_s[kMaxGroup];
+    const helios_blocks* gblk[kMaxGroup];
+    GatherWS* ggw[kMaxGroup];
+    const int64_t* gnodes[kMaxGroup];
+    const int64_t* gnn[kMaxGroup];
+    void* gfeat[kMaxGroup];
+    helios_gather_stats* gst[kMaxGroup];
+    for (int j = 0; j < G; j++) {
+      PlanSlot& m = p->slots[k + j];
+      gws_s[j] = &m.ws;
+      gblk[j] = &m.blocks;
+      ggw[j] = &m.gws;
+      gnodes[j] = m.blocks.nodes;
+      gnn[j] = m.blocks.level_counts + d.L;
+      gfeat[j] = m.feats;
+      gst[j] = m.stats;
+    }
+    HCUDA(cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking));
     if (p->trace) {
       const size_t row = (size_t)(3 * d.L + 4) * 16;
       HCUDA(cudaMalloc(&sl.d_trace, PlanSlot::kTraceRing * row));
@@ -136,12 +157,16 @@ helios_status plan_create_impl(helios_plan* p) {
     if (p->graphs) {
       auto sample_ops = [&]() -> helios_status {
         // the gather's control words are zeroed at the batch start, off the sampling -> lookup edge
-        if (sl.gws.ctl_preset) HCUDA(cudaMemsetAsync(sl.gws.d_ctl, 0, kCtlWords * sizeof(unsigned long long), sl.stream));
-        return sample_launch(g, sl.ws, d.max_seeds, d.fanouts, d.L, &sl.blocks, sl.stream);
+        for (int j = 0; j < G; j++)
+          if (ggw[j]->ctl_preset)
+            HCUDA(cudaMemsetAsync(ggw[j]->d_ctl, 0, kCtlWords * sizeof(unsigned long long), sl.stream));
+        return sample_launch_group(g, gws_s, gblk, G, d.max_seeds, d.fanouts, d.L, sl.stream);
       };
       auto gather_ops = [&]() {  // link mode: lookup + HBM rows only (host rows: link stream)
-        return (p->link ? gather_hbm_launch : gather_launch)(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + d.L,
-                                                             sl.blocks.nodes_cap, sl.feats, sl.stats, sl.stream);
+        if (p->link)
+          return gather_hbm_launch(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + d.L, sl.blocks.nodes_cap,
+                                   sl.feats, sl.stats, sl.stream);
+        return gather_launch_group(p->c, ggw, gnodes, gnn, G, sl.blocks.nodes_cap, gfeat, gst, sl.stream);
       };
       s = capture(sl.stream, &sl.g_sample, sample_ops);
       if (s != HELIOS_OK) return s;
@@ -182,25 +207,20 @@ helios_status plan_create_impl(helios_plan* p) {
   return HELIOS_OK;
 }
 
-helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seeds, int64_t n, uint64_t key, uint32_t flags,
-                               cudaStream_t caller) {
-  HCHECK(slot >= 0 && slot < (int32_t)p->slots.size(), HELIOS_E_INVALID, "slot %d of %zu", slot, p->slots.size());
-  HCHECK(n >= 0 && n <= p->d.max_seeds, HELIOS_E_CAPACITY, "n_seeds %lld > plan capacity %lld", (long long)n,
-         (long long)p->d.max_seeds);
-  HCHECK(n == 0 || seeds, HELIOS_E_INVALID, "null seeds");
-  HCHECK(!p->c || !p->c->broken, HELIOS_E_STATE, "cache unusable after an IO / staging watchdog timeout");
-  PlanSlot& sl = p->slots[slot];
-  HCUDA(cudaEventRecord(sl.ev_caller, caller));
-  HCUDA(cudaStreamWaitEvent(sl.stream, sl.ev_caller, 0));
-  void* trace_row = nullptr;
-  if (p->trace) {
-    const size_t row = (size_t)(3 * p->d.L + 4) * 16;
-    trace_row = (char*)sl.d_trace + (sl.count % PlanSlot::kTraceRing) * row;
-    HCUDA(cudaMemsetAsync(trace_row, 0xFF, row, sl.stream));
+// Launches slot gi's group (G positions, leader gi*G) with the parameters already uploaded; positions
+// not submitted since the last launch run as empty batches.
+static helios_status launch_group(helios_plan* p, int gi, uint32_t flags) {
+  const int G = p->G;
+  PlanSlot& sl = p->slots[(size_t)gi * G];
+  helios_status s = HELIOS_OK;
+  for (int j = 0; j < G; j++) {
+    PlanSlot& m = p->slots[(size_t)gi * G + j];
+    if (!m.staged) {
+      s = ws_upload_params(m.ws, 0, 0, nullptr, false, sl.stream, nullptr);
+      if (s != HELIOS_OK) return s;
+      m.rb_req = false;
+    }
   }
-  helios_status s = ws_upload_params(sl.ws, key, n, seeds, (flags & HELIOS_SUBMIT_SEEDS_HOST) != 0, sl.stream,
-                                     trace_row);
-  if (s != HELIOS_OK) return s;
   const bool timed = (flags & HELIOS_SUBMIT_TIMING) != 0;
   cudaEvent_t* ev = &sl.ring[PlanSlot::kEv * (sl.tcount % PlanSlot::kRing)];
   if (timed) HCUDA(cudaEventRecord(ev[0], sl.stream));
@@ -211,11 +231,30 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
   } else if (p->graphs && !timed && !chain) {
     HCUDA(cudaGraphLaunch(sl.g_all, sl.stream));
   } else {
+    SampleWS* gws_s[kMaxGroup];
+    const helios_blocks* gblk[kMaxGroup];
+    GatherWS* ggw[kMaxGroup];
+    const int64_t* gnodes[kMaxGroup];
+    const int64_t* gnn[kMaxGroup];
+    void* gfeat[kMaxGroup];
+    helios_gather_stats* gst[kMaxGroup];
+    for (int j = 0; j < G; j++) {
+      PlanSlot& m = p->slots[(size_t)gi * G + j];
+      gws_s[j] = &m.ws;
+      gblk[j] = &m.blocks;
+      ggw[j] = &m.gws;
+      gnodes[j] = m.blocks.nodes;
+      gnn[j] = m.blocks.level_counts + p->d.L;
+      gfeat[j] = m.feats;
+      gst[j] = m.stats;
+    }
     if (p->graphs) {
       HCUDA(cudaGraphLaunch(sl.g_sample, sl.stream));
     } else {
-      if (sl.gws.ctl_preset) HCUDA(cudaMemsetAsync(sl.gws.d_ctl, 0, kCtlWords * sizeof(unsigned long long), sl.stream));
-      s = sample_launch(p->g, sl.ws, p->d.max_seeds, p->d.fanouts, p->d.L, &sl.blocks, sl.stream);
+      for (int j = 0; j < G; j++)
+        if (ggw[j]->ctl_preset)
+          HCUDA(cudaMemsetAsync(ggw[j]->d_ctl, 0, kCtlWords * sizeof(unsigned long long), sl.stream));
+      s = sample_launch_group(p->g, gws_s, gblk, G, p->d.max_seeds, p->d.fanouts, p->d.L, sl.stream);
       if (s != HELIOS_OK) return s;
     }
     if (chain && p->gather_chained) HCUDA(cudaStreamWaitEvent(sl.stream, p->ev_gather_chain, 0));
@@ -223,9 +262,12 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
     if (p->c) {
       if (p->graphs) {
         HCUDA(cudaGraphLaunch(sl.g_gather, sl.stream));
+      } else if (p->link) {
+        s = gather_hbm_launch(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + p->d.L, sl.blocks.nodes_cap,
+                              sl.feats, sl.stats, sl.stream);
+        if (s != HELIOS_OK) return s;
       } else {
-        s = (p->link ? gather_hbm_launch : gather_launch)(p->c, sl.gws, sl.blocks.nodes, sl.blocks.level_counts + p->d.L,
-                                                          sl.blocks.nodes_cap, sl.feats, sl.stats, sl.stream);
+        s = gather_launch_group(p->c, ggw, gnodes, gnn, G, sl.blocks.nodes_cap, gfeat, gst, sl.stream);
         if (s != HELIOS_OK) return s;
       }
     }
@@ -242,8 +284,11 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
     HCUDA(cudaStreamWaitEvent(sl.stream, sl.ev_host, 0));
   }
   if (p->c) {
-    s = io_launch(p->c, sl.gws, sl.feats, sl.stream);
-    if (s != HELIOS_OK) return s;
+    for (int j = 0; j < G; j++) {
+      PlanSlot& m = p->slots[(size_t)gi * G + j];
+      s = io_launch(p->c, m.gws, m.feats, sl.stream);
+      if (s != HELIOS_OK) return s;
+    }
   }
   if (chain) {
     HCUDA(cudaEventRecord(p->ev_gather_chain, sl.stream));
@@ -253,22 +298,68 @@ helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seed
     HCUDA(cudaEventRecord(ev[2], sl.stream));
     sl.tcount++;
   }
-  sl.rb_valid = (flags & HELIOS_SUBMIT_READBACK) != 0;
-  if (sl.rb_valid) {
-    const int L = p->d.L;
-    HCUDA(cudaMemcpyAsync(sl.h_rb, sl.blocks.level_counts, (L + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, sl.stream));
-    if (p->c) HCUDA(cudaMemcpyAsync(sl.h_rb + L + 1, sl.stats, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, sl.stream));
+  const int L = p->d.L;
+  for (int j = 0; j < G; j++) {
+    PlanSlot& m = p->slots[(size_t)gi * G + j];
+    m.rb_valid = m.rb_req;
+    if (m.rb_valid) {
+      HCUDA(cudaMemcpyAsync(m.h_rb, m.blocks.level_counts, (L + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, sl.stream));
+      if (p->c) HCUDA(cudaMemcpyAsync(m.h_rb + L + 1, m.stats, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, sl.stream));
+    }
+    m.staged = false;
+    m.submitted = true;
   }
   HCUDA(cudaEventRecord(sl.ev_end, sl.stream));
   sl.count++;
-  sl.submitted = true;
   return HELIOS_OK;
+}
+
+// Stages one batch at position `slot` (uploads its parameters on the group's stream) and launches
+// the group when the position is the group's last one (or on HELIOS_SUBMIT_FLUSH); G = 1: every
+// submit launches.
+helios_status plan_submit_impl(helios_plan* p, int32_t slot, const int64_t* seeds, int64_t n, uint64_t key, uint32_t flags,
+                               cudaStream_t caller) {
+  HCHECK(slot >= 0 && slot < (int32_t)p->slots.size(), HELIOS_E_INVALID, "slot %d of %zu", slot, p->slots.size());
+  HCHECK(n >= 0 && n <= p->d.max_seeds, HELIOS_E_CAPACITY, "n_seeds %lld > plan capacity %lld", (long long)n,
+         (long long)p->d.max_seeds);
+  HCHECK(n == 0 || seeds, HELIOS_E_INVALID, "null seeds");
+  HCHECK(!p->c || !p->c->broken, HELIOS_E_STATE, "cache unusable after an IO / staging watchdog timeout");
+  const int G = p->G;
+  const int gi = slot / G;
+  PlanSlot& sl = p->slots[(size_t)gi * G];  // the group's leader: stream, graphs, events
+  PlanSlot& me = p->slots[slot];
+  HCHECK(!me.staged, HELIOS_E_STATE, "position %d already holds a batch that was not launched", slot);
+  HCUDA(cudaEventRecord(sl.ev_caller, caller));
+  HCUDA(cudaStreamWaitEvent(sl.stream, sl.ev_caller, 0));
+  void* trace_row = nullptr;
+  if (p->trace) {
+    const size_t row = (size_t)(3 * p->d.L + 4) * 16;
+    trace_row = (char*)sl.d_trace + (sl.count % PlanSlot::kTraceRing) * row;
+    HCUDA(cudaMemsetAsync(trace_row, 0xFF, row, sl.stream));
+  }
+  helios_status s = ws_upload_params(me.ws, key, n, seeds, (flags & HELIOS_SUBMIT_SEEDS_HOST) != 0, sl.stream,
+                                     trace_row);
+  if (s != HELIOS_OK) return s;
+  me.staged = true;
+  me.rb_req = (flags & HELIOS_SUBMIT_READBACK) != 0;
+  if (slot % G == G - 1 || (flags & HELIOS_SUBMIT_FLUSH)) return launch_group(p, gi, flags);
+  return HELIOS_OK;
+}
+
+// The group of position `slot` is launched first if that position holds a staged (not yet launched)
+// batch; otherwise the position's last batch belongs to the group's last launch, which is what the
+// caller waits for (batches staged at the group's other positions stay staged).
+static helios_status flush_group(helios_plan* p, int32_t slot) {
+  if (!p->slots[slot].staged) return HELIOS_OK;
+  return launch_group(p, slot / p->G, 0);
 }
 
 helios_status plan_wait_impl(helios_plan* p, int32_t slot, cudaStream_t st) {
   HCHECK(slot >= 0 && slot < (int32_t)p->slots.size(), HELIOS_E_INVALID, "slot %d of %zu", slot, p->slots.size());
-  PlanSlot& sl = p->slots[slot];
-  if (!sl.submitted) return HELIOS_OK;
+  helios_status s = flush_group(p, slot);
+  if (s != HELIOS_OK) return s;
+  PlanSlot& sl = p->slots[(size_t)(slot / p->G) * p->G];
+  if (!p->slots[slot].submitted) return HELIOS_OK;
   HCUDA(cudaStreamWaitEvent(st, sl.ev_end, 0));
   return HELIOS_OK;
 }
@@ -276,9 +367,11 @@ helios_status plan_wait_impl(helios_plan* p, int32_t slot, cudaStream_t st) {
 helios_status plan_readback_impl(helios_plan* p, int32_t slot, int64_t* out) {
   HCHECK(slot >= 0 && slot < (int32_t)p->slots.size(), HELIOS_E_INVALID, "slot %d of %zu", slot, p->slots.size());
   HCHECK(out, HELIOS_E_INVALID, "null readback output");
+  helios_status s = flush_group(p, slot);
+  if (s != HELIOS_OK) return s;
   PlanSlot& sl = p->slots[slot];
   HCHECK(sl.submitted && sl.rb_valid, HELIOS_E_STATE, "slot %d: last batch not submitted with HELIOS_SUBMIT_READBACK", slot);
-  HCUDA(cudaEventSynchronize(sl.ev_end));
+  HCUDA(cudaEventSynchronize(p->slots[(size_t)(slot / p->G) * p->G].ev_end));
   const int L = p->d.L;
   memcpy(out, sl.h_rb, (L + 1) * sizeof(int64_t));
   for (int q = 0; q < 4; q++) out[L + 1 + q] = p->c ? sl.h_rb[L + 1 + q] : 0;
@@ -288,7 +381,7 @@ helios_status plan_readback_impl(helios_plan* p, int32_t slot, int64_t* out) {
 helios_status plan_timing_impl(helios_plan* p, int32_t slot, int32_t back, helios_batch_timing* out) {
   HCHECK(slot >= 0 && slot < (int32_t)p->slots.size(), HELIOS_E_INVALID, "slot %d of %zu", slot, p->slots.size());
   HCHECK(out, HELIOS_E_INVALID, "null timing output");
-  PlanSlot& sl = p->slots[slot];
+  PlanSlot& sl = p->slots[(size_t)(slot / p->G) * p->G];  // timing is per group (its leader's events)
   HCHECK(back >= 0 && back < PlanSlot::kRing && back < sl.tcount, HELIOS_E_RANGE,
          "slot %d: timed batch -%d not recorded", slot, back);
   cudaEvent_t* ev = &sl.ring[PlanSlot::kEv * ((sl.tcount - 1 - back) % PlanSlot::kRing)];

@@ -70,6 +70,13 @@ struct SampleCtx {
   unsigned* bar;  // grid barrier {arrivals, generation} (reset with the scan state every batch)
 };
 
+// The batches of one launch (a plan slot's group): the chain's kernels run with
+// gridDim.y = n and CTA row y works on batch y; every batch keeps its own table, scan state and
+// outputs, so a group is exactly n independent batches sharing each kernel launch.
+struct SampleGroup {
+  SampleCtx c[kMaxGroup];
+};
+
 // N_0 = seeds: copy into nodes, insert into the table with local id = position.  Duplicate or
 // out-of-range seeds are latched (reading 7).
 __device__ __forceinline__ void insert_seed(const SampleCtx& c, int64_t i, const int64_t* __restrict__ seeds) {
@@ -81,7 +88,7 @@ __device__ __forceinline__ void insert_seed(const SampleCtx& c, int64_t i, const
     return;
   }
   bool fresh;
-  const uint32_t s = table_insert(c.tab, c.mask, (uint32_t)u, &fresh);
+  const uint32_t s = table_insert(c.tab, c.mask, (uint32_t)u, kEmpty, &fresh);
   c.node_slot[i] = s;
   if (!fresh) {
     latch(c.err, HELIOS_E_INVALID);
@@ -156,9 +163,7 @@ __device__ __forceinline__ void dev_count_scan(const SampleCtx& c, int h) {
 
 __device__ __forceinline__ void insert_edge(const SampleCtx& c, int64_t e, uint32_t u) {
   bool fresh;
-  const uint32_t s = table_insert(c.tab, c.mask, u, &fresh);
-  c.slot_of[e] = s;
-  if (fresh || ld_volatile_u32(&c.tab[s].local) == kEmpty) atomicMin(&c.tab[s].minpos, (uint32_t)e);
+  c.slot_of[e] = table_insert(c.tab, c.mask, u, (uint32_t)e, &fresh);
 }
 
 // Hop h fill: one G-lane group per frontier row (G = power of two >= min(f, 32), >= 4).  Copy the
@@ -251,7 +256,8 @@ __device__ __forceinline__ void dev_assign(const SampleCtx& c, int h) {
       slot[q] = 0;
       if (e < eh) {
         slot[q] = c.slot_of[e];
-        flag[q] = (ld_volatile_u32(&c.tab[slot[q]].local) == kEmpty && c.tab[slot[q]].minpos == (uint32_t)e) ? 1 : 0;
+        const uint4 t = ld_volatile_v4u32(&c.tab[slot[q]]);  // {minpos, key, local, pad}
+        flag[q] = (t.z == kEmpty && t.x == (uint32_t)e) ? 1 : 0;
       }
       sum += flag[q];
     }
@@ -263,7 +269,7 @@ __device__ __forceinline__ void dev_assign(const SampleCtx& c, int h) {
     for (int q = 0; q < kScanItems; q++) {
       if (flag[q]) {
         const int64_t id = nh + run;
-        c.nodes[id] = (int64_t)c.tab[slot[q]].key;
+        c.nodes[id] = (int64_t)(c.tab[slot[q]].km >> 32);
         c.node_slot[id] = slot[q];
         c.tab[slot[q]].local = (uint32_t)id;
         run++;
@@ -303,38 +309,46 @@ __device__ __forceinline__ void dev_insert_seeds(const SampleCtx& c) {  // L = 0
 }
 
 // ---- multi-kernel path: one kernel per phase, chained with programmatic dependent launch ----
-__global__ void __launch_bounds__(kScanBlock) k_count_scan(SampleCtx c, int h) {
+// blockIdx.y selects the batch of the group.
+__global__ void __launch_bounds__(kScanBlock) k_count_scan(const __grid_constant__ SampleGroup P, int h) {
+  const SampleCtx& c = P.c[blockIdx.y];
   if (h > 0) pdl_wait();
   pdl_trigger();
   TraceScope ts(c.params, 3 * h);
   dev_count_scan<kScanBlock>(c, h);
 }
 template <int G>
-__global__ void __launch_bounds__(256) k_fill_insert(SampleCtx c, int h) {
+__global__ void __launch_bounds__(256) k_fill_insert(const __grid_constant__ SampleGroup P, int h) {
+  const SampleCtx& c = P.c[blockIdx.y];
   pdl_wait();
   pdl_trigger();
   TraceScope ts(c.params, 3 * h + 1);
   dev_fill_insert<G>(c, h);
 }
-__global__ void __launch_bounds__(kScanBlock) k_dedup_assign(SampleCtx c, int h) {
+__global__ void __launch_bounds__(kScanBlock) k_dedup_assign(const __grid_constant__ SampleGroup P, int h) {
+  const SampleCtx& c = P.c[blockIdx.y];
   pdl_wait();
   pdl_trigger();
   TraceScope ts(c.params, 3 * h + 2);
   dev_assign<kScanBlock>(c, h);
 }
-__global__ void __launch_bounds__(256) k_relabel(SampleCtx c, int h) {
+__global__ void __launch_bounds__(256) k_relabel(const __grid_constant__ SampleGroup P, int h) {
+  const SampleCtx& c = P.c[blockIdx.y];
   pdl_wait();
   pdl_trigger();
   TraceScope ts(c.params, 3 * c.L);
   dev_relabel(c, h);
 }
-__global__ void __launch_bounds__(256) k_table_clear(SampleCtx c) {
+__global__ void __launch_bounds__(256) k_table_clear(const __grid_constant__ SampleGroup P) {
+  const SampleCtx& c = P.c[blockIdx.y];
   pdl_wait();
   pdl_trigger();
   TraceScope ts(c.params, 3 * c.L + 1);
   dev_table_clear(c);
 }
-__global__ void __launch_bounds__(256) k_insert_seeds(SampleCtx c) { dev_insert_seeds(c); }
+__global__ void __launch_bounds__(256) k_insert_seeds(const __grid_constant__ SampleGroup P) {
+  dev_insert_seeds(P.c[blockIdx.y]);
+}
 
 // ---- persistent path: the whole batch in one cooperative kernel, phases separated by a grid
 // barrier (3 per hop + 1), so a batch costs one launch instead of 2 + 3L ----
@@ -678,10 +692,10 @@ static SampleCtx make_ctx(const helios_graph* g, const SampleWS& w, const int32_
 }
 
 template <int G>
-static void launch_fill(const helios_graph* g, const SampleCtx& c, int h, int64_t rows, cudaStream_t st) {
+static void launch_fill(const helios_graph* g, const SampleGroup& P, int n, int h, int64_t rows, cudaStream_t st) {
   const int64_t threads = std::max<int64_t>(rows, 1) * G;
   const int grid = (int)std::min<int64_t>((threads + 255) / 256, (int64_t)g->sms * 4);
-  launch_pdl(k_fill_insert<G>, dim3(grid), dim3(256), st, c, h);
+  launch_pdl(k_fill_insert<G>, dim3(grid, n), dim3(256), st, P, h);
 }
 
 static int persistent_grid(int sms) {
@@ -727,20 +741,28 @@ static bool cluster_fits(int cl) {
   return n > 0;
 }
 
-helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const int32_t* fanouts, int32_t L,
-                            const helios_blocks* out, cudaStream_t st, const std::function<helios_status(int)>* hook) {
+helios_status sample_launch_group(helios_graph* g, SampleWS* const* ws, const helios_blocks* const* outs, int n,
+                                  int64_t B_max, const int32_t* fanouts, int32_t L, cudaStream_t st,
+                                  const std::function<helios_status(int)>* hook) {
   int64_t maxn, lvl[HELIOS_MAX_HOPS + 1], edg[HELIOS_MAX_HOPS];
   helios_status s = sample_bounds(B_max, fanouts, L, g->V, g->E, &maxn, lvl, edg);
   if (s != HELIOS_OK) return s;
-  const SampleCtx c = make_ctx(g, w, fanouts, L, out);
-  HCUDA(cudaMemsetAsync(w.scan_base, 0xFF, w.scan_bytes, st));
-  if (w.cluster && !hook) {  // the whole batch: one cluster, one launch
+  HCHECK(n >= 1 && n <= kMaxGroup, HELIOS_E_INVALID, "group of %d batches (1..%d)", n, kMaxGroup);
+  HCHECK(n == 1 || !hook, HELIOS_E_INVALID, "stage hooks need a group of one batch");
+  SampleGroup P{};
+  for (int b = 0; b < n; b++) {
+    P.c[b] = make_ctx(g, *ws[b], fanouts, L, outs[b]);
+    HCUDA(cudaMemsetAsync(ws[b]->scan_base, 0xFF, ws[b]->scan_bytes, st));
+  }
+  const SampleCtx& c = P.c[0];
+  SampleWS& w = *ws[0];
+  if (n == 1 && w.cluster && !hook) {  // the whole batch: one cluster, one launch
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t cfg = cluster_cfg(w.cluster, st, attr);
     HCUDA(cudaLaunchKernelEx(&cfg, k_sample_cluster<kClusterBlock>, c));
     return HELIOS_OK;
   }
-  if (w.persistent && !hook) {
+  if (n == 1 && w.persistent && !hook) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(persistent_grid(g->sms));
     cfg.blockDim = dim3(256);
@@ -754,27 +776,28 @@ helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const i
     return HELIOS_OK;
   }
   if (L == 0)
-    k_insert_seeds<<<(int)std::max<int64_t>(1, (B_max + 255) / 256), 256, 0, st>>>(c);
+    k_insert_seeds<<<dim3((unsigned)std::max<int64_t>(1, (B_max + 255) / 256), n), 256, 0, st>>>(P);
   for (int h = 0; h < L; h++) {
     const int32_t f = fanouts[h];
     // persistent tile loops: a grid of at most one CTA per SM, tiles taken by ticket
     const int rt = (int)std::min<int64_t>(std::max<int64_t>(1, (lvl[h] + kScanTile - 1) / kScanTile), g->sms);
     // hop 0: enough CTAs for one seed insert per thread (the scan itself uses ceil(B/tile) tiles)
     if (h == 0) {
-      k_count_scan<<<std::max<int>(rt, (int)std::min<int64_t>((B_max + 255) / 256, g->sms)), kScanBlock, 0, st>>>(c, 0);
+      const int g0 = std::max<int>(rt, (int)std::min<int64_t>((B_max + 255) / 256, g->sms));
+      k_count_scan<<<dim3(g0, n), kScanBlock, 0, st>>>(P, 0);
       if (hook) {
         helios_status hs = (*hook)(0);
         if (hs != HELIOS_OK) return hs;
       }
     } else {
-      launch_pdl(k_count_scan, dim3(rt), dim3(kScanBlock), st, c, h);
+      launch_pdl(k_count_scan, dim3(rt, n), dim3(kScanBlock), st, P, h);
     }
-    if (f < 0 || f > 16) launch_fill<32>(g, c, h, lvl[h], st);
-    else if (f > 8) launch_fill<16>(g, c, h, lvl[h], st);
-    else if (f > 4) launch_fill<8>(g, c, h, lvl[h], st);
-    else launch_fill<4>(g, c, h, lvl[h], st);
+    if (f < 0 || f > 16) launch_fill<32>(g, P, n, h, lvl[h], st);
+    else if (f > 8) launch_fill<16>(g, P, n, h, lvl[h], st);
+    else if (f > 4) launch_fill<8>(g, P, n, h, lvl[h], st);
+    else launch_fill<4>(g, P, n, h, lvl[h], st);
     const int et = (int)std::min<int64_t>(std::max<int64_t>(1, (edg[h] + kScanTile - 1) / kScanTile), g->sms);
-    launch_pdl(k_dedup_assign, dim3(et), dim3(kScanBlock), st, c, h);
+    launch_pdl(k_dedup_assign, dim3(et, n), dim3(kScanBlock), st, P, h);
     if (hook) {
       helios_status hs = (*hook)(h + 1);
       if (hs != HELIOS_OK) return hs;
@@ -782,12 +805,19 @@ helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const i
   }
   if (L > 0) {
     const int ge = (int)std::min<int64_t>(std::max<int64_t>(1, (edg[L - 1] + 255) / 256), (int64_t)g->sms * 2);
-    launch_pdl(k_relabel, dim3(ge), dim3(256), st, c, L - 1);
+    launch_pdl(k_relabel, dim3(ge, n), dim3(256), st, P, L - 1);
   }
   const int gc = (int)std::min<int64_t>(std::max<int64_t>(1, (maxn + 255) / 256), (int64_t)g->sms * 2);
-  launch_pdl(k_table_clear, dim3(gc), dim3(256), st, c);
+  launch_pdl(k_table_clear, dim3(gc, n), dim3(256), st, P);
   HCUDA(cudaGetLastError());
   return HELIOS_OK;
+}
+
+helios_status sample_launch(helios_graph* g, SampleWS& w, int64_t B_max, const int32_t* fanouts, int32_t L,
+                            const helios_blocks* out, cudaStream_t st, const std::function<helios_status(int)>* hook) {
+  SampleWS* ws[1] = {&w};
+  const helios_blocks* outs[1] = {out};
+  return sample_launch_group(g, ws, outs, 1, B_max, fanouts, L, st, hook);
 }
 
 }  // namespace helios

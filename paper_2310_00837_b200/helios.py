@@ -30,8 +30,9 @@ MAX_RANKS = 64
 STATUS = ["OK", "E_INVALID", "E_RANGE", "E_CAPACITY", "E_NOMEM", "E_CUDA", "E_IO", "E_TIMEOUT", "E_STATE"]
 HOST_ALIAS, TABLE_MAPPED, NO_DIRECT_IO, IO_FAULT_AT = 0x1, 0x2, 0x4, 0x100
 HOST_FILL, HOST_TIER_MAPPED, HOST_STAGED, IO_SYNC = 0x8, 0x10, 0x20, 0x40
+HBM_REPLICATED = 0x200
 PLAN_NO_GRAPH, PLAN_SERIAL_GATHER, PLAN_INTRA_BATCH, PLAN_LINK_STREAM, PLAN_TRACE = 0x1, 0x2, 0x4, 0x8, 0x10
-SUBMIT_SEEDS_HOST, SUBMIT_TIMING, SUBMIT_READBACK = 0x1, 0x2, 0x4
+SUBMIT_SEEDS_HOST, SUBMIT_TIMING, SUBMIT_READBACK, SUBMIT_FLUSH = 0x1, 0x2, 0x4, 0x8
 
 i64, i32, u32, u64, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p
 
@@ -47,11 +48,12 @@ class helios_cache_desc(ctypes.Structure):
                 ("hotness", vp), ("host_table", vp), ("feature_path", ctypes.c_char_p), ("header_bytes", i64),
                 ("file_stride", i64), ("io_rings", i32), ("ring_depth", i32), ("io_ctas", i32),
                 ("io_fault_at", i32), ("flags", u32), ("host_tier", vp), ("stage_workers", i32),
-                ("stage_frac", ctypes.c_float), ("stage_reserve", ctypes.c_float)]
+                ("stage_frac", ctypes.c_float), ("stage_reserve", ctypes.c_float), ("io_sms", i32)]
 
 
 class helios_plan_desc(ctypes.Structure):
-    _fields_ = [("max_seeds", i64), ("L", i32), ("fanouts", i32 * MAX_HOPS), ("depth", i32), ("flags", u32)]
+    _fields_ = [("max_seeds", i64), ("L", i32), ("fanouts", i32 * MAX_HOPS), ("depth", i32), ("flags", u32),
+                ("group", i32)]
 
 
 class helios_batch_timing(ctypes.Structure):
@@ -62,7 +64,7 @@ class helios_batch_timing(ctypes.Structure):
 class helios_cache_info(ctypes.Structure):
     _fields_ = [("dir", vp), ("hbm_tier", vp), ("host_tier", vp), ("V", i64), ("hbm_rows", i64), ("host_rows", i64),
                 ("file_rows", i64), ("row_bytes", i32), ("world_size", i32), ("rank", i32), ("peers_attached", i32),
-                ("io_rings", i32), ("ring_depth", i32), ("direct_io", i32), ("io_reads", i64), ("staged_rows", i64)]
+                ("io_rings", i32), ("ring_depth", i32), ("direct_io", i32), ("io_reads", i64), ("staged_rows", i64), ("io_sms", i32)]
 
 
 _sig = {
@@ -305,7 +307,7 @@ def helios_cache_build(g: Graph, hotness: torch.Tensor, row_bytes: int, hbm_rows
                        file_stride: int = 0, world_size: int = 1, rank: int = 0, io_rings: int = 4,
                        ring_depth: int = 256, io_ctas: int = 32, flags: int = 0, io_fault_at: int = 0,
                        host_tier=None, stage_workers: int = 0, stage_frac: float = 0.0,
-                       stage_reserve: float = 0.0) -> Cache:
+                       stage_reserve: float = 0.0, io_sms: int = 0) -> Cache:
     d = helios_cache_desc()
     d.row_bytes, d.world_size, d.rank = row_bytes, world_size, rank
     d.hbm_rows, d.host_rows = hbm_rows, host_rows
@@ -317,6 +319,7 @@ def helios_cache_build(g: Graph, hotness: torch.Tensor, row_bytes: int, hbm_rows
     d.io_rings, d.ring_depth, d.io_ctas, d.io_fault_at, d.flags = io_rings, ring_depth, io_ctas, io_fault_at, flags
     d.host_tier = _ptr(host_tier)
     d.stage_workers, d.stage_frac, d.stage_reserve = stage_workers, stage_frac, stage_reserve
+    d.io_sms = io_sms
     h = vp()
     _check(_lib.helios_cache_build(g.handle, ctypes.byref(d), ctypes.byref(h)), "helios_cache_build")
     return Cache(h.value, g, (host_table, path, host_tier))
@@ -395,14 +398,17 @@ def device_view(ptr: int, n: int, dtype=torch.int64) -> torch.Tensor:
 # ---- execution plan ------------------------------------------------------------------------------
 
 class Plan:
-    """A helios_plan: `depth` in-flight batch slots, each replaying a CUDA graph of the whole batch.
-    Slot outputs are plan-owned device buffers exposed as zero-copy torch views."""
+    """A helios_plan: `depth` in-flight batch slots of `group` batches each, each slot replaying a CUDA
+    graph of its whole group.  `positions` = depth * group; every plan call takes a position.
+    Position outputs are plan-owned device buffers exposed as zero-copy torch views."""
 
-    def __init__(self, handle: int, graph: Graph, cache: Cache | None, B: int, fanouts, depth: int):
+    def __init__(self, handle: int, graph: Graph, cache: Cache | None, B: int, fanouts, depth: int, group: int = 1):
         self.handle, self.graph, self.cache, self.B, self.fanouts, self.depth = handle, graph, cache, B, list(fanouts), depth
+        self.group = group
+        self.positions = depth * group
         L = len(self.fanouts)
         self.outputs = []
-        for k in range(depth):
+        for k in range(self.positions):
             blk, fp, sp = helios_blocks(), vp(), vp()
             _check(_lib.helios_plan_outputs(handle, k, ctypes.byref(blk), ctypes.byref(fp), ctypes.byref(sp)),
                    "helios_plan_outputs")
@@ -432,15 +438,16 @@ class Plan:
             pass
 
 
-def helios_plan_create(g: Graph, c: Cache | None, B: int, fanouts, depth: int = 2, flags: int = 0) -> Plan:
+def helios_plan_create(g: Graph, c: Cache | None, B: int, fanouts, depth: int = 2, flags: int = 0,
+                       group: int = 1) -> Plan:
     d = helios_plan_desc()
-    d.max_seeds, d.L, d.depth, d.flags = B, len(fanouts), depth, flags
+    d.max_seeds, d.L, d.depth, d.flags, d.group = B, len(fanouts), depth, flags, group
     for h, f in enumerate(fanouts):
         d.fanouts[h] = f
     h = vp()
     _check(_lib.helios_plan_create(g.handle, c.handle if c is not None else None, ctypes.byref(d), ctypes.byref(h)),
            "helios_plan_create")
-    p = Plan(h.value, g, c, B, fanouts, depth)
+    p = Plan(h.value, g, c, B, fanouts, depth, group)
     # host rows go through the plan's link stream (see helios.h, HELIOS_PLAN_LINK_STREAM)
     p.link = (c is not None and c.info().host_rows > 0 and bool(flags & PLAN_LINK_STREAM)
               and not flags & (PLAN_SERIAL_GATHER | PLAN_INTRA_BATCH))
@@ -448,7 +455,7 @@ def helios_plan_create(g: Graph, c: Cache | None, B: int, fanouts, depth: int = 
 
 
 def helios_plan_submit(p: Plan, slot: int, seeds, key: int, stream=None, timing: bool = False,
-                       readback: bool = False) -> None:
+                       readback: bool = False, flush: bool = False) -> None:
     if isinstance(seeds, torch.Tensor) and seeds.is_cuda and seeds.dtype == torch.int64 and seeds.is_contiguous():
         # the plan reads them later on its slot stream: the caller keeps them alive until the batch
         # completes (helios.h, helios_plan_submit)
@@ -464,6 +471,8 @@ def helios_plan_submit(p: Plan, slot: int, seeds, key: int, stream=None, timing:
         fl |= SUBMIT_TIMING
     if readback:
         fl |= SUBMIT_READBACK
+    if flush:
+        fl |= SUBMIT_FLUSH
     _check(_lib.helios_plan_submit(p.handle, slot, ptr, n, key & (2**64 - 1), fl, _stream(stream)),
            "helios_plan_submit")
 

@@ -10,10 +10,14 @@
 // stager threads claim chunks from the back.  Every output row is compared with its source row, so a
 // lost, duplicated-into-the-wrong-place or stale chunk fails; built with -fsanitize=thread it also
 // checks the protocol's memory ordering.  Prints one JSON line.
-//   stager_harness <contexts> <batches> <n_host> <stage_workers> <gpu_threads> <frac> [steal_us]
+// The reservation rule (stage_reserve > 0: the last chunks wait a bounded time for a stager before
+// the GPU takes them) is mirrored too.
+//   stager_harness <contexts> <batches> <n_host> <stage_workers> <gpu_threads> <frac> [steal_us] [reserve]
+//                  [reserve_us]
 #include "../../paper_2310_00837_b200/csrc/staging.cu"
 
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <random>
@@ -28,6 +32,8 @@ int main(int argc, char** argv) {
   const int gpu_threads = argc > 5 ? atoi(argv[5]) : 4;
   const float frac = argc > 6 ? (float)atof(argv[6]) : 1.0f;
   const int steal_us = argc > 7 ? atoi(argv[7]) : 100;   // the GPU's kStageStealNs (0: never wait)
+  const float reserve = argc > 8 ? (float)atof(argv[8]) : 0.0f;  // stage_reserve
+  const int reserve_us = argc > 9 ? atoi(argv[9]) : 200;  // the GPU's kStageReserveNs
   const int32_t R = 64;        // row bytes (the protocol is independent of R)
   const int64_t S = 20000;     // host-tier rows
   std::vector<char> tier((size_t)S * R);
@@ -84,6 +90,9 @@ int main(int argc, char** argv) {
         __atomic_store_n(&x.mail[0], seq, __ATOMIC_RELEASE);
         std::atomic<int64_t> ticket{0};
         const int64_t n_chunks = (n + kStageChunk - 1) / kStageChunk;
+        const int64_t n_res = std::min<int64_t>(std::min<int64_t>(n_chunks, x.w.stage_rows / kStageChunk),
+                                                (int64_t)std::ceil(reserve * (float)n_chunks));
+        const int64_t c_res = n_chunks - n_res;
         std::vector<std::thread> warps;
         for (int t = 0; t < gpu_threads; t++)
           warps.emplace_back([&]() {
@@ -91,11 +100,20 @@ int main(int argc, char** argv) {
               const int64_t j0 = ticket.fetch_add(kStageChunk);
               if (j0 >= n) break;
               const int64_t cc = j0 / kStageChunk;
-              __atomic_store_n(&x.hint, ((unsigned long long)seq << 32) | (unsigned long long)cc, __ATOMIC_RELAXED);
               const int64_t j1 = std::min<int64_t>(n, j0 + kStageChunk);
               const unsigned long long claimed = ((unsigned long long)seq << 2) | kChunkClaimed;
               const unsigned long long done = ((unsigned long long)seq << 2) | kChunkDone;
               unsigned long long st = __atomic_load_n(&x.chunk[cc], __ATOMIC_ACQUIRE);
+              if (cc >= c_res && st != claimed && st != done) {  // reserved: wait for a stager to claim it
+                auto w0 = std::chrono::steady_clock::now();
+                while (st != claimed && st != done &&
+                       std::chrono::steady_clock::now() - w0 < std::chrono::microseconds(reserve_us)) {
+                  std::this_thread::yield();
+                  st = __atomic_load_n(&x.chunk[cc], __ATOMIC_ACQUIRE);
+                }
+              }
+              if (st != claimed && st != done)  // this "warp" copies the chunk: stagers stop at the front
+                __atomic_store_n(&x.hint, ((unsigned long long)seq << 32) | (unsigned long long)cc, __ATOMIC_RELAXED);
               if (st == claimed) {  // bounded wait, then take the chunk back (as host_rows_dyn)
                 auto w0 = std::chrono::steady_clock::now();
                 while (st == claimed && std::chrono::steady_clock::now() - w0 < std::chrono::microseconds(steal_us)) {

@@ -37,18 +37,18 @@ def setup(H, cfg, flags=0):
     return inp, g, c, dref
 
 
-def check_batches(H, inp, g, c, dref, n_batches, depth=8, order=None):
+def check_batches(H, inp, g, c, dref, n_batches, depth=8, order=None, group=1):
     cfg = inp.cfg
     keys = workloads.batch_keys(0, len(inp.batches))
     full = [b for b in range(len(inp.batches)) if len(inp.batches[b]) == cfg.B][:n_batches]
     if order == "reversed":
         full = full[::-1]
-    p = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=depth)
+    p = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=depth, group=group)
     stream = torch.cuda.current_stream()
     seeds = {b: torch.as_tensor(inp.batches[b]).cuda() for b in full}
     got = {}
-    for start in range(0, len(full), depth):
-        idx = full[start:start + depth]
+    for start in range(0, len(full), p.positions):
+        idx = full[start:start + p.positions]
         for k, b in enumerate(idx):
             H.helios_plan_submit(p, k, seeds[b], keys[b], stream)
         for k, b in enumerate(idx):
@@ -85,6 +85,10 @@ def test_c2_full_size_plan(H):
     b = check_batches(H, inp, g, c, dref, 20, depth=5, order="reversed")
     for k in a:
         assert np.array_equal(a[k][1], b[k][1])
+    # and through plan groups of 4 (one launch of each kernel for 4 batches), as the bench runs C2
+    b = check_batches(H, inp, g, c, dref, 20, depth=3, group=4)
+    for k in a:
+        assert np.array_equal(a[k][1], b[k][1])
     c.free()
     g.free()
 
@@ -110,6 +114,9 @@ def test_c3_full_size_plan(H):
         pytest.skip(f"needs ~125 GB of host RAM for the table + packed host tier, {avail / 1e9:.0f} GB available")
     inp, g, c, dref = setup(H, cfg, flags=H.HOST_STAGED)
     got = check_batches(H, inp, g, c, dref, 24, depth=12)
+    got2 = check_batches(H, inp, g, c, dref, 16, depth=4, group=4)   # plan groups (bench --group)
+    for k in got2:
+        assert np.array_equal(got[k][1], got2[k][1])
     assert sum(int(v[2][2]) for v in got.values()) > 0
     c.free()
     g.free()

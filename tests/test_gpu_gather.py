@@ -130,6 +130,38 @@ def test_io_ring_wraparound_and_fault(H, c1, c1_hot, sync):
     c.free()
 
 
+@pytest.mark.parametrize("io_sms,sync", [(8, False), (16, False), (48, True)])
+def test_io_green_context(H, c1, c1_hot, io_sms, sync):
+    """NEXT-3: the IO kernel confined to a green-context SM partition (the analog of the paper's MPS
+    cap): three-tier gathers stay bit-exact, the provisioned SM count is
+    reported, and a plan of C1 batches (sampling + gather on the primary context, IO on the partition)
+    completes."""
+    g, hot = c1_hot
+    cfg = c1.cfg
+    Hr, S = workloads.tier_rows(cfg)
+    c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=c1.table, feature_path=c1.feature_path,
+                             header_bytes=c1.header, file_stride=c1.stride, io_ctas=4, io_sms=io_sms,
+                             flags=H.IO_SYNC if sync else 0)
+    got = c.info().io_sms
+    assert io_sms <= got < 148, got
+    dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S)
+    rng = np.random.default_rng(io_sms)
+    for n in (1, 1000, cfg.V):
+        nodes = rng.permutation(cfg.V)[:n]
+        gather_and_check(H, c, c1, nodes, oracle.lookup_counts(dref, nodes))
+    reads0 = c.info().io_reads
+    p = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=3)
+    keys = workloads.batch_keys(0, len(c1.batches))
+    for i, b in enumerate(c1.batches[:12]):
+        H.helios_plan_submit(p, i % 3, torch.as_tensor(b).cuda(), keys[i])
+    for k in range(3):
+        H.helios_plan_wait(p, k)
+    H.helios_sync(c)
+    assert c.info().io_reads > reads0
+    p.free()
+    c.free()
+
+
 def test_batch_prepare_c1_epoch(H, c1, c1_hot):
     g, hot = c1_hot
     cfg = c1.cfg

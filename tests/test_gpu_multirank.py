@@ -2,7 +2,9 @@
 the same device), gloo for the setup collectives.  Each rank builds its HBM shard (G=2), the packed
 host tier is one /dev/shm mapping filled by rank 0, blobs are all-gathered and peer shards attached;
 every rank's batches (b = rank mod 2) must equal the oracle bit for bit, and its per-tier counts
-(local / peer / host / file) must equal the oracle's lookup_counts for that rank."""
+(local / peer / host / file) must equal the oracle's lookup_counts for that rank.  The C5-rep ablation
+(HELIOS_CACHE_HBM_REPLICATED: every rank holds the same hottest rows) runs the same checks against the
+single-GPU directory and must read no peer rows."""
 import os
 import socket
 import sys
@@ -24,7 +26,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, tag, q):
+def _worker(rank, world, port, tag, q, replicated):
     import faulthandler
     faulthandler.dump_traceback_later(100, exit=True)
     sys.path.insert(0, ROOT)
@@ -51,21 +53,25 @@ def _worker(rank, world, port, tag, q):
         hd.allreduce_hotness(hot_cpu)
         hot.copy_(hot_cpu)
         Hr = int(0.1 * cfg.V)
-        S = cfg.V - world * Hr
+        G = 1 if replicated else world   # the directory's world size
+        S = cfg.V - G * Hr
+        rf = H.HBM_REPLICATED if replicated else 0
         name = f"helios_mr_{tag}"
         if rank == 0:   # creator first, then the others map it (after the barrier)
             tier, m = hd.shared_array(name, (S * cfg.R,), np.uint8, create=True)
             c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=inp.table, world_size=world, rank=rank,
-                                     host_tier=tier, flags=H.HOST_FILL)
+                                     host_tier=tier, flags=H.HOST_FILL | rf)
         dist.barrier()
         if rank != 0:
             tier, m = hd.shared_array(name, (S * cfg.R,), np.uint8, create=False)
             c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=inp.table, world_size=world, rank=rank,
-                                     host_tier=tier)
+                                     host_tier=tier, flags=rf)
+        info = c.info()
+        assert info.world_size == world and info.rank == rank
         print(f"[rank {rank}] cache built", file=sys.stderr, flush=True)
         hd.attach_peers(H, c)
         print(f"[rank {rank}] peers attached", file=sys.stderr, flush=True)
-        dref, _ = oracle.cache_dir(hot_cpu.numpy().astype(np.uint64), world, Hr, S)
+        dref, _ = oracle.cache_dir(hot_cpu.numpy().astype(np.uint64), G, Hr, S)
         p = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=2)
         keys = workloads.batch_keys(0, len(inp.batches))
         mine = hd.rank_batches(len(inp.batches), rank, world)
@@ -82,7 +88,7 @@ def _worker(rank, world, port, tag, q):
             ok &= np.array_equal(got["nodes"], orc.nodes)
             ok &= np.array_equal(feats[: len(orc.nodes)].cpu().numpy(), oracle.gather(orc.nodes, cfg.R, table=inp.table))
             st = stats.cpu().tolist()
-            ok &= st == oracle.lookup_counts(dref, orc.nodes, rank).tolist()
+            ok &= st == oracle.lookup_counts(dref, orc.nodes, 0 if replicated else rank).tolist()
             peer_rows += st[1]
         print(f"[rank {rank}] batches done", file=sys.stderr, flush=True)
         dist.barrier()
@@ -96,13 +102,14 @@ def _worker(rank, world, port, tag, q):
         dist.destroy_process_group()
 
 
-def test_two_ranks_one_gpu():
+@pytest.mark.parametrize("replicated", [False, True], ids=["sharded", "replicated"])
+def test_two_ranks_one_gpu(replicated):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     tag = f"{os.getpid()}_{port}"
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, tag, q)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, tag, q, replicated)) for r in range(2)]
     for p in ps:
         p.start()
     res = [q.get(timeout=150) for _ in ps]
@@ -111,4 +118,8 @@ def test_two_ranks_one_gpu():
         assert p.exitcode == 0
     for rank, ok, peer_rows, nb in res:
         assert ok, f"rank {rank} differs from the oracle"
-        assert peer_rows > 0 and nb > 0, f"rank {rank} read no peer rows"
+        assert nb > 0
+        if replicated:
+            assert peer_rows == 0, f"rank {rank} read peer rows from a replicated HBM tier"
+        else:
+            assert peer_rows > 0, f"rank {rank} read no peer rows"

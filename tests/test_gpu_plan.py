@@ -91,6 +91,56 @@ def test_plan_c1_epoch(H, c1, depth, flags, host_seeds, staged):
     c.free()
 
 
+@pytest.mark.parametrize("depth,group,flags,host_seeds,staged,partial",
+                         [(2, 2, 0, False, False, False), (2, 4, 0, True, False, False), (3, 3, 1, False, False, False),
+                          (2, 4, 0, False, True, False), (1, 4, 2, True, False, False), (2, 3, 0, False, False, True),
+                          (1, 2, 1, True, True, True)])
+def test_plan_groups_c1_epoch(H, c1, depth, group, flags, host_seeds, staged, partial):
+    """Plan groups (desc.group): each kernel of a slot's chain launched once for `group` batches
+    (gridDim.y).  Every batch of the C1 epoch, at every position, equals the oracle (sampling, three-
+    tier gather incl. the IO rings, tier counts); per-position readback; partial groups launched by
+    helios_plan_wait (partial=True: only some positions of a group are submitted, the others run as
+    empty batches and keep nothing of their previous batch visible through readback)."""
+    cfg = c1.cfg
+    Hr, S = workloads.tier_rows(cfg)
+    g, hot, c = build(H, c1, Hr, S, flags=H.HOST_ALIAS | (H.HOST_STAGED if staged else 0))
+    dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S, host_slot_is_id=True)
+    p = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=depth, flags=flags, group=group)
+    assert p.positions == depth * group
+    keys = workloads.batch_keys(0, len(c1.batches))
+    stream = torch.cuda.current_stream()
+    nb = len(c1.batches)
+    P = p.positions
+    rnd = 0
+    for start in range(0, nb, P):
+        idx = list(range(start, min(nb, start + P)))
+        if partial and rnd % 2 == 1:
+            idx = idx[: max(1, group - 1)]   # the first group is left incomplete
+        rnd += 1
+        live = []
+        for k, b in enumerate(idx):
+            seeds = c1.batches[b] if host_seeds else torch.as_tensor(c1.batches[b]).cuda()
+            live.append(seeds)
+            H.helios_plan_submit(p, k, seeds, keys[b], stream, timing=(b % 2 == 0), readback=True)
+        for k, b in enumerate(idx):
+            H.helios_plan_wait(p, k, stream)
+        H.helios_sync(c)
+        for k, b in enumerate(idx):
+            check_slot(p, k, c1, c1.batches[b], keys[b], dref)
+            rb = H.helios_plan_readback(p, k)
+            orc_n = p.outputs[k][0].level_counts.cpu().numpy()
+            assert rb[: len(cfg.fanouts) + 1].tolist() == orc_n.tolist()
+            assert rb[len(cfg.fanouts) + 1:].tolist() == p.outputs[k][2].cpu().tolist()
+        if partial and len(idx) < group:   # positions of the group not submitted ran as empty batches
+            for k in range(len(idx), group):
+                assert int(p.outputs[k][0].level_counts[0].item()) == 0
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=2, group=5)
+    assert e.value.name == "E_INVALID"
+    p.free()
+    c.free()
+
+
 def test_plan_sample_only_medium(H):
     gr = synth.graph(400_000, 8_000_000, seed=33)
     g = H.helios_graph_load(gr.indptr, gr.indices)

@@ -37,16 +37,18 @@ def stager(request):
     return _build("stager_harness.cpp", "stager_harness", request.param), request.param
 
 
-@pytest.mark.parametrize("ctx,batches,n_host,workers,gpu,frac,steal",
-                         [(3, 40, 5000, 4, 4, 1.0, 100), (4, 30, 3000, 6, 2, 0.5, 100), (2, 60, 700, 3, 3, 1.0, 0),
-                          (1, 50, 64, 2, 1, 1.0, 1000), (3, 20, 20000, 8, 6, 0.6, 20)])
-def test_stager_chunk_protocol(stager, ctx, batches, n_host, workers, gpu, frac, steal):
+@pytest.mark.parametrize("ctx,batches,n_host,workers,gpu,frac,steal,reserve,reserve_us",
+                         [(3, 40, 5000, 4, 4, 1.0, 100, 0, 0), (4, 30, 3000, 6, 2, 0.5, 100, 0, 0),
+                          (2, 60, 700, 3, 3, 1.0, 0, 0, 0), (1, 50, 64, 2, 1, 1.0, 1000, 0, 0),
+                          (3, 20, 20000, 8, 6, 0.6, 20, 0, 0), (3, 30, 5000, 4, 4, 1.0, 100, 0.7, 200),
+                          (2, 30, 3000, 1, 4, 0.7, 50, 0.7, 5), (4, 20, 8000, 6, 3, 0.8, 100, 0.8, 1000)])
+def test_stager_chunk_protocol(stager, ctx, batches, n_host, workers, gpu, frac, steal, reserve, reserve_us):
     """Every host-list row of every batch reaches the output exactly as its source row, whatever
     mix of zero-copy and staged chunks the race produced; staged chunks were used."""
     exe, tsan = stager
     if tsan:
         batches = max(5, batches // 3)
-    r = _run(exe, ctx, batches, n_host, workers, gpu, frac, steal)
+    r = _run(exe, ctx, batches, n_host, workers, gpu, frac, steal, reserve, reserve_us)
     assert r["bad_rows"] == 0
     assert r["rows_gpu"] + r["rows_staged_used"] > 0
     assert r["rows_staged_by_cpu"] >= r["rows_staged_used"]
