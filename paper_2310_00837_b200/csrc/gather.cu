@@ -19,6 +19,9 @@
 
 namespace helios {
 
+__device__ __forceinline__ void st_global_v4(int4* p, int4 v) {  // STG, not a generic ST (shuffled pointers)
+  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
 __device__ __forceinline__ int4 ld_stream(const int4* p) {
   int4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
@@ -244,7 +247,7 @@ __device__ __forceinline__ void flat_rows(const GatherArgs& a, int q, int64_t cn
         const int f = b0 + lane + 32 * k;
         const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
         char* dst = (char*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)dp, row);
-        if (f < nv) ((int4*)dst)[f - row * nvec] = r[k];
+        if (f < nv) st_global_v4((int4*)dst + (f - row * nvec), r[k]);
       }
     }
     sp = sp_n;

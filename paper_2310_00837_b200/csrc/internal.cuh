@@ -130,6 +130,10 @@ struct SampleWS {
   unsigned* bar = nullptr;      // persistent-sampler grid barrier {arrivals, generation} (in the scan region)
   int cluster = 0;              // > 0: the whole batch in one launch of a cluster of this many CTAs
                                 // (HELIOS_SAMPLE_MODE=cluster|cluster16|chain)
+  // shared-memory tile dedup (HELIOS_SAMPLE_DEDUP=smem|global): hop h runs tiled when tile_rows[h] > 0
+  int32_t tile_rows[HELIOS_MAX_HOPS] = {};
+  uint2* elist = nullptr;        // [cap_edges] per-tile distinct entries {global slot, tile minpos}
+  uint32_t* ndist = nullptr;     // [tiles] distinct ids per tile
   bool persistent = false;      // one cooperative kernel per batch instead of the 2+3L-kernel chain
                                 // (HELIOS_SAMPLE_PERSISTENT=1; measured slower)
   // per-batch parameters, read by the kernels from device memory so that a captured CUDA graph

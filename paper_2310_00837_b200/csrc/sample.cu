@@ -68,6 +68,11 @@ struct SampleCtx {
   int32_t fan[HELIOS_MAX_HOPS];
   int32_t L;
   unsigned* bar;  // grid barrier {arrivals, generation} (reset with the scan state every batch)
+  // shared-memory tile dedup: tile_rows[h] > 0 = hop h runs the tiled fill / assign /
+  // relabel; elist[E0 + j] = {global slot, tile minpos} of the tile's j-th distinct id, ndist[t] = count
+  int32_t tile_rows[HELIOS_MAX_HOPS];
+  uint2* elist;
+  uint32_t* ndist;
 };
 
 // The batches of one launch (a plan slot's group): the chain's kernels run with
@@ -95,6 +100,57 @@ __device__ __forceinline__ void insert_seed(const SampleCtx& c, int64_t i, const
     return;
   }
   c.tab[s].local = (uint32_t)i;
+}
+
+// ---- shared-memory tile dedup (north_star: "warp-cooperative dedup/relabel via a shared-memory hash
+// plus radix compaction") ----------------------------------------------------------------------------
+// Hop h's frontier rows are cut into tiles of tile_rows[h] consecutive rows, so a tile's sampled
+// edges are the consecutive positions [E0, E1) = [bp[r0], bp[r1]) (at most kTileEdges).  The fill
+// dedups a tile's ids in a shared-memory hash first (key, tile-minimum position) and touches the
+// global table once per DISTINCT id of the tile (insert + minpos lowering) instead of once per
+// edge; every edge keeps the index of its tile-distinct entry (slot_of[e] = E0 + j).  The assign
+// reads the tile's distinct entries (not its edges), marks the first occurrences of ids new at this
+// hop in a shared bitmap over the tile's edge positions, ranks them by popcount prefix (the radix
+// compaction: rank = position order within the tile) and takes the tile's offset from a decoupled
+// look-back over tiles in order, so new ids are numbered exactly in first-occurrence order (the
+// oracle's).  The relabel reads the local ids of a tile's distinct entries into shared memory once
+// and writes the tile's block indices from there.
+constexpr int kTileEdges = 1024;            // sampled edges per tile at most (tile_rows * f_h)
+constexpr int kTileSlots = 2 * kTileEdges;  // shared hash slots (load <= 0.5)
+
+__device__ __forceinline__ int64_t tile_count(const SampleCtx& c, int h) {
+  const int64_t n = c.level_counts[h];
+  return (n + c.tile_rows[h] - 1) / c.tile_rows[h];
+}
+
+// Relabel of hop h, tiled: block indices from the local ids of each tile's distinct entries.
+__device__ __forceinline__ void dev_relabel_tile(const SampleCtx& c, int h) {
+  __shared__ uint32_t s_loc[kTileEdges];
+  const int TR = c.tile_rows[h];
+  const int64_t n = c.level_counts[h];
+  const int64_t nt = tile_count(c, h);
+  const int32_t* __restrict__ bp = c.bp[h];
+  int32_t* __restrict__ bi = c.bi[h];
+  for (int64_t t = blockIdx.x; t < nt; t += gridDim.x) {
+    const int64_t r0 = t * TR;
+    const int64_t E0 = bp[r0], E1 = bp[min(n, r0 + TR)];
+    const uint32_t nd = c.ndist[t];
+    for (uint32_t j = threadIdx.x; j < nd; j += blockDim.x) s_loc[j] = c.tab[c.elist[E0 + j].x].local;
+    __syncthreads();
+    for (int64_t e = E0 + threadIdx.x; e < E1; e += blockDim.x) bi[e] = (int32_t)s_loc[c.slot_of[e] - (uint32_t)E0];
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void dev_relabel_any(const SampleCtx& c, int h) {
+  if (c.tile_rows[h] > 0) {
+    dev_relabel_tile(c, h);
+    return;
+  }
+  const int64_t ep = c.edge_counts[h];
+  int32_t* __restrict__ bi = c.bi[h];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ep; e += (int64_t)gridDim.x * blockDim.x)
+    bi[e] = (int32_t)c.tab[c.slot_of[e]].local;
 }
 
 // Hop h degree scan: k_i = min(deg(N_h[i]), f_h), block_indptr[h] = exclusive scan (persistent tile
@@ -153,12 +209,7 @@ __device__ __forceinline__ void dev_count_scan(const SampleCtx& c, int h) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
       insert_seed(c, i, seeds);
   }
-  if (h > 0) {  // side job: hop h-1's local ids are final (its dedup_assign has completed)
-    const int64_t ep = c.edge_counts[h - 1];
-    int32_t* __restrict__ prev = c.bi[h - 1];
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ep; e += (int64_t)gridDim.x * blockDim.x)
-      prev[e] = (int32_t)c.tab[c.slot_of[e]].local;
-  }
+  if (h > 0) dev_relabel_any(c, h - 1);  // side job: hop h-1's local ids are final (its assign has completed)
 }
 
 __device__ __forceinline__ void insert_edge(const SampleCtx& c, int64_t e, uint32_t u) {
@@ -227,6 +278,176 @@ __device__ __forceinline__ void dev_fill_insert(const SampleCtx& c, int h) {
   }
 }
 
+// Tiled fill of hop h (see the tile dedup comment above): the sampling of every row is that of
+// dev_fill_insert (same draws, same positions); only the table insert differs.
+template <int G>
+__device__ __forceinline__ void dev_fill_tile(const SampleCtx& c, int h) {
+  __shared__ uint32_t s_key[kTileSlots], s_min[kTileSlots], s_li[kTileSlots];
+  __shared__ uint16_t s_eslot[kTileEdges];
+  __shared__ uint32_t s_cnt;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const unsigned gmask = (G == 32) ? 0xFFFFFFFFu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  const int32_t f = c.fan[h];
+  const uint64_t key = (uint64_t)c.params[0];
+  const int TR = c.tile_rows[h];
+  const int64_t n = c.level_counts[h];
+  const int64_t nt = tile_count(c, h);
+  const int32_t* __restrict__ bp = c.bp[h];
+  int32_t* scratch = c.bi[h];
+  for (int p = threadIdx.x; p < kTileSlots; p += blockDim.x) {
+    s_key[p] = kEmpty;
+    s_min[p] = kEmpty;
+  }
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const int grp = threadIdx.x / G, ngrp = blockDim.x / G;
+  for (int64_t t = blockIdx.x; t < nt; t += gridDim.x) {
+    const int64_t r0 = t * TR, r1 = min(n, r0 + TR);
+    const int64_t E0 = bp[r0], E1 = bp[r1];
+    auto ins = [&](int64_t e, uint32_t u) {  // shared-memory insert-or-find, tile-minimum position
+      uint32_t q = hash32(u) & (kTileSlots - 1);
+      for (;;) {
+        const uint32_t k = atomicCAS(&s_key[q], kEmpty, u);
+        if (k == kEmpty || k == u) break;
+        q = (q + 1) & (kTileSlots - 1);
+      }
+      atomicMin(&s_min[q], (uint32_t)e);
+      s_eslot[e - E0] = (uint16_t)q;
+    };
+    for (int64_t i = r0 + grp; i < r1; i += ngrp) {
+      const int64_t v = c.nodes[i];
+      int64_t base = 0, d = 0;
+      if ((uint64_t)v < (uint64_t)c.V) {
+        base = c.indptr[v];
+        d = c.indptr[v + 1] - base;
+      }
+      const int64_t off = bp[i];
+      const int64_t k = min(d, (int64_t)f);
+      if (k == d) {
+        for (int64_t p = gl; p < d; p += G) ins(off + p, (uint32_t)c.indices[base + p]);
+      } else if (k <= G) {
+        uint32_t tt = 0, m = 0;
+        if (gl < k) {
+          m = (uint32_t)(d - k + gl + 1);
+          tt = __umulhi(philox_word(key, (uint32_t)h, (uint64_t)v, (uint32_t)gl), m);
+        }
+        uint32_t P = 0;
+        for (int j = 0; j < (int)k; j++) {
+          const uint32_t tj = __shfl_sync(gmask, tt, j, G);
+          const unsigned hit = __ballot_sync(gmask, gl < j && P == tj);
+          if (gl == j) P = hit ? (m - 1) : tj;
+        }
+        if (gl < k) ins(off + gl, (uint32_t)c.indices[base + P]);
+      } else {  // k > G: serial Floyd in the scratch row (as dev_fill_insert)
+        if (gl == 0) {
+          for (int64_t j = 0; j < k; j++) {
+            const uint32_t m = (uint32_t)(d - k + j + 1);
+            const uint32_t tj = __umulhi(philox_word(key, (uint32_t)h, (uint64_t)v, (uint32_t)j), m);
+            bool seen = false;
+            for (int64_t q = 0; q < j; q++)
+              if ((uint32_t)scratch[off + q] == tj) {
+                seen = true;
+                break;
+              }
+            scratch[off + j] = (int32_t)(seen ? m - 1 : tj);
+          }
+        }
+        __syncwarp(gmask);
+        for (int64_t j = gl; j < k; j += G) ins(off + j, (uint32_t)c.indices[base + scratch[off + j]]);
+        __syncwarp(gmask);
+      }
+    }
+    __syncthreads();
+    // one global insert per distinct id of the tile, with the tile's first position of it
+    for (int q = threadIdx.x; q < kTileSlots; q += blockDim.x) {
+      const uint32_t u = s_key[q];
+      if (u != kEmpty) {
+        bool fresh;
+        const uint32_t mp = s_min[q];
+        const uint32_t gs = table_insert(c.tab, c.mask, u, mp, &fresh);
+        const uint32_t j = atomicAdd(&s_cnt, 1u);
+        c.elist[E0 + j] = make_uint2(gs, mp);
+        s_li[q] = j;
+        s_key[q] = kEmpty;
+        s_min[q] = kEmpty;
+      }
+    }
+    __syncthreads();
+    for (int64_t e = E0 + threadIdx.x; e < E1; e += blockDim.x) c.slot_of[e] = (uint32_t)E0 + s_li[s_eslot[e - E0]];
+    if (threadIdx.x == 0) {
+      c.ndist[t] = s_cnt;
+      s_cnt = 0;
+    }
+    __syncthreads();
+  }
+}
+
+// Tiled assign of hop h: tiles in ticket (= edge position) order; first occurrences of new ids are
+// ranked inside the tile by a popcount prefix over a shared bitmap of the tile's edge positions.
+template <int BLK>
+__device__ __forceinline__ void dev_assign_tile(const SampleCtx& c, int h) {
+  constexpr int kWords = kTileEdges / 32;
+  __shared__ uint32_t s_bits[kWords], s_wpre[kWords];
+  __shared__ uint32_t s_total;
+  __shared__ unsigned s_tile;
+  __shared__ long long s_prefix;
+  const int TR = c.tile_rows[h];
+  const int64_t n = c.level_counts[h];
+  const int64_t nt = tile_count(c, h);
+  const int64_t nh = n;
+  const int32_t* __restrict__ bp = c.bp[h];
+  const ScanState& ss = c.edge_scan[h];
+  if (threadIdx.x < kWords) s_bits[threadIdx.x] = 0;
+  __syncthreads();
+  for (;;) {
+    const unsigned tile = tile_ticket(ss, &s_tile);
+    if (tile > 0 && (int64_t)tile >= nt) break;
+    const bool real = (int64_t)tile < nt;
+    const int64_t E0 = real ? bp[(int64_t)tile * TR] : 0;
+    const uint32_t nd = real ? c.ndist[tile] : 0;
+    for (uint32_t j = threadIdx.x; j < nd; j += BLK) {
+      const uint2 ent = c.elist[E0 + j];
+      const uint4 t = ld_volatile_v4u32(&c.tab[ent.x]);  // {minpos, key, local, pad}
+      if (t.z == kEmpty && t.x == ent.y) {
+        const uint32_t r = ent.y - (uint32_t)E0;
+        atomicOr(&s_bits[r >> 5], 1u << (r & 31));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // word prefix of the popcounts (kWords == 32)
+      const uint32_t v = __popc(s_bits[threadIdx.x]);
+      uint32_t incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if ((int)threadIdx.x >= o) incl += y;
+      }
+      s_wpre[threadIdx.x] = incl - v;
+      if (threadIdx.x == 31) s_total = incl;
+    }
+    __syncthreads();
+    const long long prefix = tile_lookback(ss, tile, (long long)s_total, &s_prefix);
+    for (uint32_t j = threadIdx.x; j < nd; j += BLK) {
+      const uint2 ent = c.elist[E0 + j];
+      const uint32_t r = ent.y - (uint32_t)E0;
+      if (r < (uint32_t)kTileEdges) {
+        const uint32_t w = s_bits[r >> 5];
+        if ((w >> (r & 31)) & 1u) {  // this entry holds the first occurrence of an id new at hop h
+          const int64_t id = nh + prefix + s_wpre[r >> 5] + __popc(w & ((1u << (r & 31)) - 1u));
+          c.nodes[id] = (int64_t)(c.tab[ent.x].km >> 32);
+          c.node_slot[id] = ent.x;
+          c.tab[ent.x].local = (uint32_t)id;
+        }
+      }
+    }
+    if (threadIdx.x == 0 && ((nt == 0 && tile == 0) || (int64_t)tile == nt - 1)) c.level_counts[h + 1] = nh + prefix + s_total;
+    __syncthreads();
+    if (threadIdx.x < kWords) s_bits[threadIdx.x] = 0;
+    __syncthreads();
+  }
+}
+
 __device__ __forceinline__ int fill_group(int32_t f) { return (f < 0 || f > 16) ? 32 : (f > 8 ? 16 : (f > 4 ? 8 : 4)); }
 
 // Hop h dedup/relabel: flag = "this edge is the first occurrence of an id new at this hop"; the
@@ -281,12 +502,7 @@ __device__ __forceinline__ void dev_assign(const SampleCtx& c, int h) {
   }
 }
 
-__device__ __forceinline__ void dev_relabel(const SampleCtx& c, int h) {
-  const int64_t eh = c.edge_counts[h];
-  int32_t* __restrict__ bi = c.bi[h];
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < eh; e += (int64_t)gridDim.x * blockDim.x)
-    bi[e] = (int32_t)c.tab[c.slot_of[e]].local;
-}
+__device__ __forceinline__ void dev_relabel(const SampleCtx& c, int h) { dev_relabel_any(c, h); }
 
 // Returns the batch hash table to all-EMPTY by clearing exactly the slots of the batch's nodes
 // (every occupied slot belongs to one node of N_L).
@@ -324,6 +540,21 @@ __global__ void __launch_bounds__(256) k_fill_insert(const __grid_constant__ Sam
   pdl_trigger();
   TraceScope ts(c.params, 3 * h + 1);
   dev_fill_insert<G>(c, h);
+}
+template <int G>
+__global__ void __launch_bounds__(256) k_fill_tile(const __grid_constant__ SampleGroup P, int h) {
+  const SampleCtx& c = P.c[blockIdx.y];
+  pdl_wait();
+  pdl_trigger();
+  TraceScope ts(c.params, 3 * h + 1);
+  dev_fill_tile<G>(c, h);
+}
+__global__ void __launch_bounds__(kScanBlock) k_assign_tile(const __grid_constant__ SampleGroup P, int h) {
+  const SampleCtx& c = P.c[blockIdx.y];
+  pdl_wait();
+  pdl_trigger();
+  TraceScope ts(c.params, 3 * h + 2);
+  dev_assign_tile<kScanBlock>(c, h);
 }
 __global__ void __launch_bounds__(kScanBlock) k_dedup_assign(const __grid_constant__ SampleGroup P, int h) {
   const SampleCtx& c = P.c[blockIdx.y];
@@ -562,6 +793,8 @@ void ws_free(SampleWS& w) {
   if (w.reset_base) cudaFree(w.reset_base);
   if (w.slot_of) cudaFree(w.slot_of);
   if (w.node_slot) cudaFree(w.node_slot);
+  if (w.elist) cudaFree(w.elist);
+  if (w.ndist) cudaFree(w.ndist);
   if (w.d_params) cudaFree(w.d_params);
   if (w.h_params) cudaFreeHost(w.h_params);
   if (w.params_ev) cudaEventDestroy(w.params_ev);
@@ -574,12 +807,21 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
   int64_t maxn, lvl[HELIOS_MAX_HOPS + 1], edg[HELIOS_MAX_HOPS];
   helios_status s = sample_bounds(B, fanouts, L, g->V, g->E, &maxn, lvl, edg);
   if (s != HELIOS_OK) return s;
-  int64_t max_e = 1, tiles_r = 1, tiles_e = 1;
+  // shared-memory tile dedup for hops with a bounded fanout (HELIOS_SAMPLE_DEDUP=smem)
+  bool tiled = false;
+  if (const char* e = getenv("HELIOS_SAMPLE_DEDUP")) tiled = !strcmp(e, "smem");
+  int32_t trows[HELIOS_MAX_HOPS] = {};
+  int64_t max_e = 1, tiles_r = 1, tiles_e = 1, tiles_t = 1;
   for (int h = 0; h < L; h++) {
     max_e = std::max(max_e, edg[h]);
     tiles_r = std::max(tiles_r, (lvl[h] + kScanTile - 1) / kScanTile);
     tiles_e = std::max(tiles_e, (edg[h] + kScanTile - 1) / kScanTile);
+    if (tiled && fanouts[h] > 0 && fanouts[h] <= kTileEdges) {
+      trows[h] = kTileEdges / fanouts[h];
+      tiles_t = std::max(tiles_t, (lvl[h] + trows[h] - 1) / trows[h]);
+    }
   }
+  tiles_e = std::max(tiles_e, tiles_t);  // the tiled assign's look-back uses the edge scan state
   // worst-case load <= 0.8 (n_L bound / table); the typical batch fills a few percent of it
   const uint64_t T64 = pow2_at_least(std::min<int64_t>(g->V, std::max<int64_t>(maxn, 1)) * 5 / 4);
   // slots are u32-indexed with kEmpty = 2^32-1 reserved: at most 2^31 slots
@@ -588,8 +830,10 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
   const uint32_t T = (uint32_t)T64;
   const int64_t max_nodes = std::max<int64_t>(maxn, 1);
   if (w.reset_base && T <= w.table_size && max_e <= w.cap_edges && tiles_r <= w.cap_tiles_rows &&
-      tiles_e <= w.cap_tiles_edges && max_nodes <= w.cap_nodes && B <= w.cap_seeds)
+      tiles_e <= w.cap_tiles_edges && max_nodes <= w.cap_nodes && B <= w.cap_seeds && (!tiled || w.elist)) {
+    for (int h = 0; h < HELIOS_MAX_HOPS; h++) w.tile_rows[h] = h < L ? trows[h] : 0;
     return HELIOS_OK;
+  }
   HCUDA(cudaDeviceSynchronize());
   ws_free(w);
   const size_t table_bytes = (size_t)T * sizeof(TableSlot);
@@ -599,6 +843,11 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
   HCUDA(cudaMalloc(&w.reset_base, w.reset_bytes));
   HCUDA(cudaMalloc(&w.slot_of, (size_t)max_e * 4));
   HCUDA(cudaMalloc(&w.node_slot, (size_t)max_nodes * 4));
+  if (tiled) {
+    HCUDA(cudaMalloc(&w.elist, (size_t)max_e * sizeof(uint2)));
+    HCUDA(cudaMalloc(&w.ndist, (size_t)tiles_e * 4));
+  }
+  for (int h = 0; h < HELIOS_MAX_HOPS; h++) w.tile_rows[h] = h < L ? trows[h] : 0;
   w.cap_nodes = max_nodes;
   w.cap_seeds = std::max<int64_t>(B, 1);
   HCUDA(cudaMalloc(&w.d_params, (4 + w.cap_seeds) * sizeof(int64_t)));
@@ -688,11 +937,21 @@ static SampleCtx make_ctx(const helios_graph* g, const SampleWS& w, const int32_
   }
   c.L = L;
   c.bar = w.bar;
+  const bool chain = !w.cluster && !w.persistent;  // the one-launch samplers run the global-table phases
+  for (int h = 0; h < HELIOS_MAX_HOPS; h++) c.tile_rows[h] = (chain && h < L) ? w.tile_rows[h] : 0;
+  c.elist = w.elist;
+  c.ndist = w.ndist;
   return c;
 }
 
 template <int G>
 static void launch_fill(const helios_graph* g, const SampleGroup& P, int n, int h, int64_t rows, cudaStream_t st) {
+  const int TR = P.c[0].tile_rows[h];
+  if (TR > 0) {  // tiled: one CTA per tile (tiles taken grid-stride)
+    const int grid = (int)std::min<int64_t>(std::max<int64_t>(1, (rows + TR - 1) / TR), (int64_t)g->sms * 4);
+    launch_pdl(k_fill_tile<G>, dim3(grid, n), dim3(256), st, P, h);
+    return;
+  }
   const int64_t threads = std::max<int64_t>(rows, 1) * G;
   const int grid = (int)std::min<int64_t>((threads + 255) / 256, (int64_t)g->sms * 4);
   launch_pdl(k_fill_insert<G>, dim3(grid, n), dim3(256), st, P, h);
@@ -796,8 +1055,14 @@ helios_status sample_launch_group(helios_graph* g, SampleWS* const* ws, const he
     else if (f > 8) launch_fill<16>(g, P, n, h, lvl[h], st);
     else if (f > 4) launch_fill<8>(g, P, n, h, lvl[h], st);
     else launch_fill<4>(g, P, n, h, lvl[h], st);
-    const int et = (int)std::min<int64_t>(std::max<int64_t>(1, (edg[h] + kScanTile - 1) / kScanTile), g->sms);
-    launch_pdl(k_dedup_assign, dim3(et, n), dim3(kScanBlock), st, P, h);
+    if (c.tile_rows[h] > 0) {
+      const int TR = c.tile_rows[h];
+      const int at = (int)std::min<int64_t>(std::max<int64_t>(1, (lvl[h] + TR - 1) / TR), g->sms);
+      launch_pdl(k_assign_tile, dim3(at, n), dim3(kScanBlock), st, P, h);
+    } else {
+      const int et = (int)std::min<int64_t>(std::max<int64_t>(1, (edg[h] + kScanTile - 1) / kScanTile), g->sms);
+      launch_pdl(k_dedup_assign, dim3(et, n), dim3(kScanBlock), st, P, h);
+    }
     if (hook) {
       helios_status hs = (*hook)(h + 1);
       if (hs != HELIOS_OK) return hs;

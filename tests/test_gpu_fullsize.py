@@ -78,15 +78,20 @@ def H():
     return helios
 
 
-def test_c2_full_size_plan(H):
+def test_c2_full_size_plan(H, monkeypatch):
     inp, g, c, dref = setup(H, workloads.CONFIGS["C2"])
     a = check_batches(H, inp, g, c, dref, 20)
     # the same batches through other slots, reversed: identical bytes (no state leaks across slots)
     b = check_batches(H, inp, g, c, dref, 20, depth=5, order="reversed")
     for k in a:
         assert np.array_equal(a[k][1], b[k][1])
-    # and through plan groups of 4 (one launch of each kernel for 4 batches), as the bench runs C2
+    # and through plan groups of 4 (one launch of each kernel for 4 batches)
     b = check_batches(H, inp, g, c, dref, 20, depth=3, group=4)
+    for k in a:
+        assert np.array_equal(a[k][1], b[k][1])
+    # and with the shared-memory tile dedup (HELIOS_SAMPLE_DEDUP=smem, read at plan creation)
+    monkeypatch.setenv("HELIOS_SAMPLE_DEDUP", "smem")
+    b = check_batches(H, inp, g, c, dref, 20, depth=12)
     for k in a:
         assert np.array_equal(a[k][1], b[k][1])
     c.free()

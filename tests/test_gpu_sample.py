@@ -40,12 +40,14 @@ def assert_same(gpu, orc, L):
         assert np.array_equal(gpu["block_indices"][h], orc.block_indices[h]), f"hop {h} indices"
 
 
-@pytest.fixture(params=["chain", "cluster", "cluster16"])
+@pytest.fixture(params=["chain", "cluster", "cluster16", "tiled"])
 def mode(request, monkeypatch):
     """Sampler launch mode (HELIOS_SAMPLE_MODE, read when a graph's workspace is allocated): the chain of
     2 + 3L kernels, or the whole batch in one launch of an 8- or 16-CTA cluster.  Same device code,
-    so the same bits."""
-    monkeypatch.setenv("HELIOS_SAMPLE_MODE", request.param)
+    so the same bits.  "tiled": the chain with the shared-memory tile dedup (HELIOS_SAMPLE_DEDUP=smem:
+    per-tile shared hash, bitmap ranking, tiled relabel) for every hop with a bounded fanout."""
+    monkeypatch.setenv("HELIOS_SAMPLE_MODE", "chain" if request.param == "tiled" else request.param)
+    monkeypatch.setenv("HELIOS_SAMPLE_DEDUP", "smem" if request.param == "tiled" else "global")
     return request.param
 
 
@@ -95,7 +97,9 @@ def test_hub_and_isolated(H, mode):
             assert_same(gpu, orc, len(fan))
 
 
-def test_zero_seeds(H, c1):
+@pytest.mark.parametrize("dedup", ["global", "smem"])
+def test_zero_seeds(H, c1, dedup, monkeypatch):
+    monkeypatch.setenv("HELIOS_SAMPLE_DEDUP", dedup)
     g = H.helios_graph_load(c1.graph.indptr, c1.graph.indices)
     gpu = run_gpu(H, g, [], [10, 5], 1)
     assert gpu["level_counts"].tolist() == [0, 0, 0] and len(gpu["nodes"]) == 0

@@ -67,7 +67,7 @@ ms = a.elapsed_time(e) / (reps * len(blks))
 n_local, n_host = rows[0] / len(blks), rows[2] / len(blks)
 nLm = nL / len(blks)
 hbm_bytes = cfg.R * n_local + cfg.R * nLm + 16 * nLm
-print(json.dumps({"config": cfg.name, "variant": {k: os.environ.get(k) for k in ("HELIOS_GATHER_CTAS_PER_SM", "HELIOS_GATHER_BULK")},
+print(json.dumps({"config": cfg.name, "variant": {k: os.environ.get(k) for k in ("HELIOS_GATHER_CTAS_PER_SM", "HELIOS_GATHER_BULK", "HELIOS_GATHER_VU")},
                   "n_L": round(nLm, 1), "rows_local": round(n_local, 1), "rows_host": round(n_host, 1),
                   "hbm_bytes_per_launch": round(hbm_bytes), "ms_per_gather_k3k4": round(ms, 5),
                   "hbm_gbs_k3k4": round(hbm_bytes / ms / 1e6, 1), "parity": ok}), flush=True)
