@@ -547,6 +547,25 @@ __global__ void __launch_bounds__(256, VU > 8 ? 1 : 2) k_gather_lists(const __gr
   }
 }
 
+// Split host part (HELIOS_GATHER_SPLIT_HOST=1): the host-tier rows of a batch in their
+// own small kernel (64-thread CTAs, host-row code only) launched right behind the HBM part
+// (k_gather_lists, kPartHbm) on the same stream.  A host-row warp spends most of its life waiting on
+// PCIe reads and on the stagers; in the combined kernel it keeps a whole 256-thread CTA (and its
+// registers) resident after the data warps are done, which takes SM slots from the other batches'
+// sampling.  No griddepcontrol.wait: this grid is launched as the HBM part's programmatic dependent,
+// whose CTAs trigger only after their own wait on the lookup / publish kernels has returned, so the
+// lists, counts and mailbox it reads are complete.
+template <int VPL, int UH>
+__global__ void __launch_bounds__(64) k_gather_host(const __grid_constant__ GatherGroup P) {
+  const GatherArgs& a = P.a[blockIdx.y];
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const int nvec = a.R >> 4;
+  const int64_t n_host = (int64_t)a.ctl[kListHost];
+  if (a.staged) host_rows_dyn<VPL, UH>(a, n_host, lane, nvec);
+  else host_rows<VPL, UH>(a, n_host, lane, nvec);
+}
+
 // Plain row copy by id (setup: HBM-tier fill from a mapped host table).
 __global__ void k_rows_by_id(const char* __restrict__ src, int32_t R, const int32_t* __restrict__ ids, int64_t n,
                              char* __restrict__ dst) {
@@ -678,12 +697,16 @@ __device__ __forceinline__ void io_complete_warp(const IoArgs& a, int lane) {
     const int64_t idx = (int64_t)r * a.depth + slot;
     bool ok = true;
     const uint64_t t0 = globaltimer();
-    while (ld_acquire_sys_u32(&a.cq[idx].seq) != seq) {  // every lane polls (one coalesced request)
+    // every lane polls (one coalesced 32 B system-memory read per poll); the backoff grows to 8 us, far
+    // below a storage read's latency, so polls do not eat PCIe read bandwidth (profiles/r02/ncu_io_summary.json)
+    unsigned backoff = 256;
+    while (ld_acquire_sys_u32(&a.cq[idx].seq) != seq) {
       if (globaltimer() - t0 > kWatchdogNs) {
         ok = false;
         break;
       }
-      __nanosleep(128);
+      __nanosleep(backoff);
+      backoff = min(backoff * 2u, 8192u);
     }
     ok = __all_sync(0xFFFFFFFFu, ok);
     if (!ok) {
@@ -832,6 +855,13 @@ static void launch_gather_any(const GatherGroup& P, int n, int grid, bool bulk, 
   if (host) launch_gather_rows<true>(P, n, grid, bulk, st);
   else launch_gather_rows<false>(P, n, grid, bulk, st);
 }
+static void launch_gather_host(const GatherGroup& P, int n, int grid, cudaStream_t st) {
+  const int nvec = P.a[0].R / 16;
+  if (nvec <= 32) launch_pdl(k_gather_host<1, 8>, dim3(grid, n), dim3(64), st, P);
+  else if (nvec <= 64) launch_pdl(k_gather_host<2, 4>, dim3(grid, n), dim3(64), st, P);
+  else if (nvec <= 128) launch_pdl(k_gather_host<4, 2>, dim3(grid, n), dim3(64), st, P);
+  else launch_pdl(k_gather_host<8, 1>, dim3(grid, n), dim3(64), st, P);
+}
 static void launch_gather_any(const GatherArgs& a, int grid, bool bulk, bool host, cudaStream_t st) {
   GatherGroup P{};
   P.a[0] = a;
@@ -953,7 +983,14 @@ static helios_status gather_pass_group(helios_cache* c, GatherWS* const* ws, con
   const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_rows + 255) / 256), (int64_t)c->sms * 2);
   launch_pdl(k_lookup, dim3(lg, n), dim3(256), st, LP);
   if (staged) launch_pdl(k_stage_publish, dim3(1, n), dim3(1), st, PP);
-  launch_gather_any(GP, n, c->gather_ctas, c->gather_bulk, c->S > 0, st);
+  if (c->split_host && c->S > 0 && part == kPartAll) {  // HBM part, then the host part in its own small kernel
+    for (int b = 0; b < n; b++) GP.a[b].part = kPartHbm;
+    launch_gather_any(GP, n, c->gather_ctas, c->gather_bulk, false, st);
+    for (int b = 0; b < n; b++) GP.a[b].part = kPartHost;
+    launch_gather_host(GP, n, c->sms, st);
+  } else {
+    launch_gather_any(GP, n, c->gather_ctas, c->gather_bulk, c->S > 0, st);
+  }
   HCUDA(cudaGetLastError());
   return HELIOS_OK;
 }

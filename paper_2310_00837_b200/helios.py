@@ -406,6 +406,9 @@ class Plan:
         self.handle, self.graph, self.cache, self.B, self.fanouts, self.depth = handle, graph, cache, B, list(fanouts), depth
         self.group = group
         self.positions = depth * group
+        # device seeds of each position's last submit: kept referenced until that position is reused, so
+        # PyTorch's caching allocator cannot hand the memory out while the plan may still read it
+        self._seeds_ref = [None] * self.positions
         L = len(self.fanouts)
         self.outputs = []
         for k in range(self.positions):
@@ -457,16 +460,16 @@ def helios_plan_create(g: Graph, c: Cache | None, B: int, fanouts, depth: int = 
 def helios_plan_submit(p: Plan, slot: int, seeds, key: int, stream=None, timing: bool = False,
                        readback: bool = False, flush: bool = False) -> None:
     if isinstance(seeds, torch.Tensor) and seeds.is_cuda and seeds.dtype == torch.int64 and seeds.is_contiguous():
-        # the plan reads them later on its slot stream: the caller keeps them alive until the batch
-        # completes (helios.h, helios_plan_submit)
-        ptr, n, fl = seeds.data_ptr(), seeds.numel(), 0
+        # the plan reads them later on its slot stream (helios.h, helios_plan_submit): the binding keeps a
+        # reference until the position's next submit, so they stay allocated while the batch can run
+        ptr, n, fl, keep = seeds.data_ptr(), seeds.numel(), 0, seeds
     else:
         # host seeds, or device seeds needing a conversion: copied into the submit's parameter block
         # (no temporary device buffer whose lifetime the plan would have to track)
         if isinstance(seeds, torch.Tensor):
             seeds = seeds.detach().to("cpu", torch.int64).numpy()
         arr = np.ascontiguousarray(seeds, dtype=np.int64)
-        ptr, n, fl = _ptr(arr), len(arr), SUBMIT_SEEDS_HOST
+        ptr, n, fl, keep = _ptr(arr), len(arr), SUBMIT_SEEDS_HOST, None
     if timing:
         fl |= SUBMIT_TIMING
     if readback:
@@ -475,6 +478,7 @@ def helios_plan_submit(p: Plan, slot: int, seeds, key: int, stream=None, timing:
         fl |= SUBMIT_FLUSH
     _check(_lib.helios_plan_submit(p.handle, slot, ptr, n, key & (2**64 - 1), fl, _stream(stream)),
            "helios_plan_submit")
+    p._seeds_ref[slot] = keep
 
 
 def helios_plan_readback(p: Plan, slot: int, out: np.ndarray | None = None) -> np.ndarray:

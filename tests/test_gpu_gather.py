@@ -130,6 +130,42 @@ def test_io_ring_wraparound_and_fault(H, c1, c1_hot, sync):
     c.free()
 
 
+@pytest.mark.parametrize("staged,reserve", [(False, 0), (True, 0), (True, 0.7)])
+def test_split_host_kernel(H, c1, c1_hot, staged, reserve, monkeypatch):
+    """HELIOS_GATHER_SPLIT_HOST=1: the host-tier rows in their own 64-thread kernel behind the HBM part
+    (zero-copy, dynamic staged and reserved staged): three-tier gathers and a C1 plan stay bit-exact."""
+    monkeypatch.setenv("HELIOS_GATHER_SPLIT_HOST", "1")
+    g, hot = c1_hot
+    cfg = c1.cfg
+    Hr, S = workloads.tier_rows(cfg)
+    c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=c1.table, feature_path=c1.feature_path,
+                             header_bytes=c1.header, file_stride=c1.stride,
+                             flags=H.HOST_STAGED if staged else 0, stage_workers=3, stage_reserve=reserve)
+    dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, Hr, S)
+    rng = np.random.default_rng(5)
+    for n in (1, 999, cfg.V, cfg.V):
+        nodes = rng.permutation(cfg.V)[:n]
+        gather_and_check(H, c, c1, nodes, oracle.lookup_counts(dref, nodes))
+    p = H.helios_plan_create(g, c, cfg.B, cfg.fanouts, depth=3)
+    keys = workloads.batch_keys(0, len(c1.batches))
+    live = [torch.as_tensor(b).cuda() for b in c1.batches[:9]]
+    for i in range(9):
+        H.helios_plan_submit(p, i % 3, live[i], keys[i])
+        if i % 3 == 2:
+            for k in range(3):
+                H.helios_plan_wait(p, k)
+            H.helios_sync(c)
+            for k in range(3):
+                b = i - 2 + k
+                blocks, feats, stats = p.outputs[k]
+                orc = oracle.sample(c1.graph.indptr, c1.graph.indices, c1.batches[b], cfg.fanouts, keys[b])
+                assert np.array_equal(blocks.to_host()["nodes"], orc.nodes)
+                assert np.array_equal(feats[: len(orc.nodes)].cpu().numpy(), oracle.gather(orc.nodes, cfg.R, table=c1.table))
+                assert stats.cpu().tolist() == oracle.lookup_counts(dref, orc.nodes).tolist()
+    p.free()
+    c.free()
+
+
 @pytest.mark.parametrize("io_sms,sync", [(8, False), (16, False), (48, True)])
 def test_io_green_context(H, c1, c1_hot, io_sms, sync):
     """NEXT-3: the IO kernel confined to a green-context SM partition (the analog of the paper's MPS
