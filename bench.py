@@ -312,7 +312,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--parity-batches", type=int, default=2)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no baseline, no parity")
-    ap.add_argument("--depth", type=int, default=12, help="plan slots (groups in flight)")
+    ap.add_argument("--depth", type=int, default=0,
+                    help="plan slots (groups in flight); 0 = 24 with a host tier (its gathers wait on PCIe and the "
+                         "stagers, so more batches in flight pay), else 12")
     ap.add_argument("--group", type=int, default=1,
                     help="batches per plan slot: each kernel of a slot's chain launches once for its whole group "
                          "(gridDim.y); batches in flight = depth x group")
@@ -334,8 +336,8 @@ def main():
     ap.add_argument("--stage-reserve", type=float, default=0.7,
                     help="HOST_STAGED: share of each batch's host-row chunks (from the list's end) the GPU leaves to "
                          "the stagers, waiting a bounded time before copying them itself (0 = pure dynamic split)")
-    ap.add_argument("--stage-workers", type=int, default=14,
-                    help="host stager threads (HOST_STAGED); 14 of the GPU box's 16 cores measured best")
+    ap.add_argument("--stage-workers", type=int, default=0,
+                    help="host stager threads per rank (HOST_STAGED); 0 = min(14, host cores / local ranks - 2) (14 of the GPU box's 16 cores measured best)")
     ap.add_argument("--ring-depth", type=int, default=256)
     ap.add_argument("--io-ctas", type=int, default=32, help="CTA budget of each IO kernel (PAPER.md:244)")
     ap.add_argument("--io-sync", action="store_true", help="ablation: GIDS-style coupled IO (one warp per request)")
@@ -346,6 +348,10 @@ def main():
     args = ap.parse_args()
     if args.zero_copy:
         args.host_staged = 0.0
+    if args.stage_workers <= 0:   # 14 of a 16-core host measured best; per rank, the host's cores / ranks - 2
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")))
+        cores = len(os.sched_getaffinity(0)) // max(1, local_world)
+        args.stage_workers = max(2, min(14, cores - 2))
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -486,7 +492,7 @@ def main():
     seq = [my_batches[i % len(my_batches)] for i in range(need)]
     seed_of = {b: torch.as_tensor(inp.batches[b]).cuda() for b in sorted(set(seq))}
     stream = torch.cuda.current_stream()
-    depth = args.depth
+    depth = args.depth if args.depth > 0 else (24 if S > 0 else 12)
     pflags = ((H.PLAN_NO_GRAPH if args.no_graph else 0) | (H.PLAN_SERIAL_GATHER if args.serial_gather else 0)
               | (H.PLAN_INTRA_BATCH if args.intra else 0) | (H.PLAN_LINK_STREAM if args.link_stream else 0))
     G = args.group
@@ -608,15 +614,15 @@ def main():
             if file_cfg:   # CPU-managed cache: FILE-tier rows by pread, the rest from memory
                 dir_host = H.device_view(c.info().dir, cfg.V, torch.int64).cpu().numpy()
             r = run_oracle_baseline(inp, keys, args.cpu_budget, dir_=dir_host)
-            P = len(os.sched_getaffinity(0))
-            rP = run_oracle_baseline(inp, keys, args.cpu_budget, dir_=dir_host, threads=P)
+            ncpu = len(os.sched_getaffinity(0))
+            rP = run_oracle_baseline(inp, keys, args.cpu_budget, dir_=dir_host, threads=ncpu)
             cpu = {"value": round(r["value"], 4), "unit": "batches/s", "cores": 1, "kind": "oracle",
                    "sample": f"{r['batches']} batches of {cfg.name} (first of epoch 0), single-threaded C++ oracle "
                              f"sample+gather ({'FILE-tier rows by buffered pread, ' if file_cfg else ''}"
                              f"{'other rows from the canonical host table' if table is not None else 'rows by pread from the feature file'}), "
-                             f"{r['seconds']:.1f}s; P-core leg: the same oracle on {P} threads, one independent batch "
+                             f"{r['seconds']:.1f}s; P-core leg: the same oracle on {ncpu} threads, one independent batch "
                              f"per thread at a time, {rP['batches']} batches in {rP['seconds']:.1f}s",
-                   "feature_gbs": round(r["gbs"], 3), "cores_P": P, "value_P": round(rP["value"], 4),
+                   "feature_gbs": round(r["gbs"], 3), "cores_P": ncpu, "value_P": round(rP["value"], 4),
                    "feature_gbs_P": round(rP["gbs"], 3), "cpu_model": cpu_model()}
 
     # ---- roofline of the dominant kernel (lookup+gather, K3/K4) ----
@@ -773,6 +779,8 @@ def main():
                       f"host stager threads from its end (cap {args.host_staged:.0%}, last "
                       f"{min(args.stage_reserve, args.host_staged):.0%} reserved for the stagers)"
                       if args.host_staged > 0 else "; GPU zero-copy reads only (ablation)"),
+                   "host_rows_kernel": ("combined (2 host warps per 8 in K4)" if os.environ.get("HELIOS_GATHER_SPLIT_HOST") == "0"
+                                        else "split (own 64-thread kernel behind the HBM part)") if S > 0 else None,
                    "batches_in_flight": P, "plan_slots": depth, "batches_per_launch": G, "cuda_graphs": not args.no_graph, "serial_gather": bool(args.serial_gather),
                    "link_stream": bool(plan.link),
                    "intra_batch_pipeline": bool(args.intra),

@@ -1,4 +1,4 @@
-/* helios.h — C ABI v1 of libhelios.so: the B200 mini-batch preparation hot path of Helios
+/* helios.h — C ABI v2 of libhelios.so: the B200 mini-batch preparation hot path of Helios
  * (arXiv 2310.00837): multi-hop uniform neighbour sampling over a CSR graph, dedup/relabel into
  * per-hop block CSRs, and feature extraction through a GPU-managed heterogeneous cache
  * (HBM tier, pinned-host tier read zero-copy, file tier served by GPU-initiated IO rings).
@@ -36,7 +36,8 @@
 extern "C" {
 #endif
 
-#define HELIOS_ABI_VERSION 1
+#define HELIOS_ABI_VERSION 2  /* 2: round 2 appended stage_reserve and io_sms to helios_cache_desc, io_sms to
+                                  helios_cache_info and group to helios_plan_desc */
 #define HELIOS_MAX_HOPS 8
 #define HELIOS_MAX_RANKS 64
 
@@ -272,7 +273,7 @@ helios_status helios_batch_prepare(helios_graph* g, helios_cache* c, const int64
  * batches is serialised on the cache's IO streams.
  *   desc.max_seeds   B: capacity of every slot (n_seeds <= B per submit).
  *   desc.L, fanouts  hops and fanouts (as helios_sample).
- *   desc.depth       number of slots, 1..16.
+ *   desc.depth       number of slots, 1..32 (with CUDA_DEVICE_MAX_CONNECTIONS=32 every slot stream gets its own hardware queue).
  *   desc.flags       HELIOS_PLAN_NO_GRAPH: launch the kernels directly on every submit;
  *                    HELIOS_PLAN_SERIAL_GATHER: chain the gathers of successive submits;
  *                    HELIOS_PLAN_INTRA_BATCH: per-hop gather passes overlapping the sampling;

@@ -432,7 +432,7 @@ helios_status helios_plan_create(helios_graph* g, helios_cache* c, const helios_
   HCHECK(g && d && out, HELIOS_E_INVALID, "null argument");
   *out = nullptr;
   HCHECK(!c || c->g == g, HELIOS_E_INVALID, "cache was built on another graph");
-  HCHECK(d->depth >= 1 && d->depth <= 16, HELIOS_E_INVALID, "plan depth %d not in [1,16]", d->depth);
+  HCHECK(d->depth >= 1 && d->depth <= 32, HELIOS_E_INVALID, "plan depth %d not in [1,32]", d->depth);
   HCHECK(d->max_seeds >= 0, HELIOS_E_INVALID, "max_seeds < 0");
   DeviceGuard dg(g->device);
   helios_plan* p = new helios_plan();

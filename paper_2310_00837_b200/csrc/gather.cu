@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(256, VU > 8 ? 1 : 2) k_gather_lists(const __gr
   }
 }
 
-// Split host part (HELIOS_GATHER_SPLIT_HOST=1): the host-tier rows of a batch in their
+// Split host part (the default; HELIOS_GATHER_SPLIT_HOST=0 = combined kernel): the host-tier rows of a batch in their
 // own small kernel (64-thread CTAs, host-row code only) launched right behind the HBM part
 // (k_gather_lists, kPartHbm) on the same stream.  A host-row warp spends most of its life waiting on
 // PCIe reads and on the stagers; in the combined kernel it keeps a whole 256-thread CTA (and its

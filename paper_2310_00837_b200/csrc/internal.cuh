@@ -271,7 +271,8 @@ struct helios_cache {
   int world = 1, world_rank = 0;    // the caller's world size / rank (G, rank: the directory's)
   int io_ctas = 32;
   int gather_ctas = 148;            // K4 grid (one CTA per SM with a host tier, more for HBM-only caches)
-  bool split_host = false;          // host-tier rows in their own small kernel (HELIOS_GATHER_SPLIT_HOST)
+  bool split_host = true;           // host-tier rows in their own small kernel (HELIOS_GATHER_SPLIT_HOST=0: the
+                                    // combined kernel, 2 host warps per 8)
   int gather_vu = 8;                // HBM / peer rows: 16-byte loads in flight per lane (HELIOS_GATHER_VU)
   bool gather_bulk = false;         // HELIOS_GATHER_BULK=1: HBM rows by cp.async.bulk (ablation)
   bool io_sync = false;            // HELIOS_CACHE_IO_SYNC ablation

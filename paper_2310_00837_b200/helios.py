@@ -1,4 +1,4 @@
-"""Thin ctypes binding of libhelios.so (C ABI v1, include/helios.h) — argument marshalling only.
+"""Thin ctypes binding of libhelios.so (C ABI v2, include/helios.h) — argument marshalling only.
 
 Every step of the hot path runs in the library's CUDA kernels; this module only turns torch tensors
 into device pointers, torch streams into cudaStream_t handles, and statuses into exceptions.  There

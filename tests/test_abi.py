@@ -38,7 +38,7 @@ def test_sm100a_cubin(so):
 def test_binding_names_match_header(so):
     from paper_2310_00837_b200 import helios as H
     assert sorted(H.ABI_SYMBOLS) == declared_symbols()
-    assert H.helios_abi_version() == 1
+    assert H.helios_abi_version() == 2
 
 
 def test_host_side_bounds_and_validation(so):

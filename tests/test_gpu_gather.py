@@ -130,11 +130,13 @@ def test_io_ring_wraparound_and_fault(H, c1, c1_hot, sync):
     c.free()
 
 
+@pytest.mark.parametrize("split", ["1", "0"])
 @pytest.mark.parametrize("staged,reserve", [(False, 0), (True, 0), (True, 0.7)])
-def test_split_host_kernel(H, c1, c1_hot, staged, reserve, monkeypatch):
-    """HELIOS_GATHER_SPLIT_HOST=1: the host-tier rows in their own 64-thread kernel behind the HBM part
-    (zero-copy, dynamic staged and reserved staged): three-tier gathers and a C1 plan stay bit-exact."""
-    monkeypatch.setenv("HELIOS_GATHER_SPLIT_HOST", "1")
+def test_split_host_kernel(H, c1, c1_hot, staged, reserve, split, monkeypatch):
+    """Host-tier rows in their own 64-thread kernel behind the HBM part (the default, split = 1) and in
+    the combined kernel (HELIOS_GATHER_SPLIT_HOST=0, 2 host warps per 8), zero-copy, dynamic staged and
+    reserved staged: three-tier gathers and a C1 plan stay bit-exact."""
+    monkeypatch.setenv("HELIOS_GATHER_SPLIT_HOST", split)
     g, hot = c1_hot
     cfg = c1.cfg
     Hr, S = workloads.tier_rows(cfg)
