@@ -452,6 +452,7 @@ helios_status helios_plan_create(helios_graph* g, helios_cache* c, const helios_
   p->link = c && c->S > 0 && !p->intra && !p->serial_gather && (d->flags & HELIOS_PLAN_LINK_STREAM);
   HCHECK(!p->intra || p->graphs, HELIOS_E_INVALID, "HELIOS_PLAN_INTRA_BATCH needs CUDA graphs");
   p->G = d->group > 0 ? d->group : 1;
+  if (const char* e = getenv("HELIOS_PLAN_TWO_GRAPHS")) p->two_graphs = atoi(e) != 0;
   if (p->G < 1 || p->G > kMaxGroup || (p->G > 1 && (p->intra || p->link || p->trace))) {
     const int G = p->G;
     delete p;

@@ -352,6 +352,8 @@ struct helios_plan {
   bool marked = false;
   bool gather_chained = false;
   int G = 1;                              // batches per slot (desc.group); slots = depth x G positions
+  bool two_graphs = false;                // HELIOS_PLAN_TWO_GRAPHS=1: untimed submits also launch the sampling
+                                          // and gather graphs separately (as timed submits do)
   std::vector<helios::PlanSlot> slots;
 };
 

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <vector>
+#include <unistd.h>
 
 #include "internal.cuh"
 
@@ -228,7 +229,7 @@ static helios_status launch_group(helios_plan* p, int gi, uint32_t flags) {
   if (p->graphs && p->intra && p->c) {  // one graph; timed submits time the whole overlapped batch
     HCUDA(cudaGraphLaunch(sl.g_all, sl.stream));
     if (timed) HCUDA(cudaEventRecord(ev[1], sl.stream));
-  } else if (p->graphs && !timed && !chain) {
+  } else if (p->graphs && !timed && !chain && !p->two_graphs) {
     HCUDA(cudaGraphLaunch(sl.g_all, sl.stream));
   } else {
     SampleWS* gws_s[kMaxGroup];
@@ -371,7 +372,15 @@ helios_status plan_readback_impl(helios_plan* p, int32_t slot, int64_t* out) {
   if (s != HELIOS_OK) return s;
   PlanSlot& sl = p->slots[slot];
   HCHECK(sl.submitted && sl.rb_valid, HELIOS_E_STATE, "slot %d: last batch not submitted with HELIOS_SUBMIT_READBACK", slot);
-  HCUDA(cudaEventSynchronize(p->slots[(size_t)(slot / p->G) * p->G].ev_end));
+  // wait by polling with short sleeps rather than cudaEventSynchronize's spin: the host stager threads
+  // (HOST_STAGED) share these cores, and a spinning waiter takes one from them
+  cudaEvent_t ev = p->slots[(size_t)(slot / p->G) * p->G].ev_end;
+  for (unsigned us = 2;; us = std::min(us * 2, 50u)) {
+    const cudaError_t e = cudaEventQuery(ev);
+    if (e == cudaSuccess) break;
+    if (e != cudaErrorNotReady) return fail(HELIOS_E_CUDA, "helios_plan_readback: %s", cudaGetErrorString(e));
+    usleep(us);
+  }
   const int L = p->d.L;
   memcpy(out, sl.h_rb, (L + 1) * sizeof(int64_t));
   for (int q = 0; q < 4; q++) out[L + 1 + q] = p->c ? sl.h_rb[L + 1 + q] : 0;
