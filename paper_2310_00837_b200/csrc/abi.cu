@@ -12,13 +12,18 @@ static thread_local std::string g_last_error;
 
 void set_error(const std::string& s) { g_last_error = s; }
 
+// Programmatic dependent launch: on unless HELIOS_NO_PDL=1; a scope (PdlScope) can turn it off for the
+// launches it encloses (plans whose cache has a host tier).
+static thread_local int g_pdl_scope = -1;
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("HELIOS_NO_PDL");
     return !(e && atoi(e) != 0);
   }();
-  return on;
+  return on && g_pdl_scope != 0;
 }
+PdlScope::PdlScope(bool enable) : prev(g_pdl_scope) { g_pdl_scope = enable ? 1 : 0; }
+PdlScope::~PdlScope() { g_pdl_scope = prev; }
 
 helios_status fail(helios_status st, const char* fmt, ...) {
   char buf[1024];

@@ -52,6 +52,11 @@ struct DeviceGuard {
 // predecessor's results.  Captured into CUDA graphs as programmatic edges.
 // HELIOS_NO_PDL=1 (read once): plain stream-ordered launches instead (ablation).
 bool pdl_enabled();
+struct PdlScope {  // launches inside the scope use PDL iff `enable` (and HELIOS_NO_PDL is not set)
+  explicit PdlScope(bool enable);
+  ~PdlScope();
+  int prev;
+};
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg = {};

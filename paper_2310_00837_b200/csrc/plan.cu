@@ -69,7 +69,18 @@ static helios_status capture(cudaStream_t st, cudaGraphExec_t* out, F&& body) {
   return HELIOS_OK;
 }
 
+// PDL for a plan's kernels: on, except when the cache has a host tier.  There the gathers wait on
+// PCIe and the stagers for most of a batch, and dependents launched early (programmatic launch) sit in
+// griddepcontrol.wait holding SM slots that the other slots' kernels need: C3 at 24 slots 6,845-6,895
+// batches/s without vs 6,672-6,722 with; C2 (HBM only) 29.8 k with vs 29.2 k without
+// (profiles/r02/pdl_on_off.jsonl).  HELIOS_PLAN_PDL=1 / 0 forces it.
+static bool plan_pdl(const helios_plan* p) {
+  if (const char* e = getenv("HELIOS_PLAN_PDL")) return atoi(e) != 0;
+  return !(p->c && p->c->S > 0);
+}
+
 helios_status plan_create_impl(helios_plan* p) {
+  PdlScope pdl_scope(plan_pdl(p));
   helios_graph* g = p->g;
   const helios_plan_desc& d = p->d;
   int64_t lvl[HELIOS_MAX_HOPS + 1], edg[HELIOS_MAX_HOPS];
@@ -211,6 +222,7 @@ helios_status plan_create_impl(helios_plan* p) {
 // Launches slot gi's group (G positions, leader gi*G) with the parameters already uploaded; positions
 // not submitted since the last launch run as empty batches.
 static helios_status launch_group(helios_plan* p, int gi, uint32_t flags) {
+  PdlScope pdl_scope(plan_pdl(p));
   const int G = p->G;
   PlanSlot& sl = p->slots[(size_t)gi * G];
   helios_status s = HELIOS_OK;
