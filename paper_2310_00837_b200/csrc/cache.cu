@@ -413,7 +413,10 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
     int per_sm = 1;
     if (const char* e = getenv("HELIOS_GATHER_CTAS_PER_SM")) per_sm = std::max(1, std::min(atoi(e), 4));
     if (const char* e = getenv("HELIOS_GATHER_BULK")) c->gather_bulk = atoi(e) != 0;
-    if (const char* e = getenv("HELIOS_GATHER_VU")) c->gather_vu = atoi(e) == 16 ? 16 : 8;
+    if (const char* e = getenv("HELIOS_GATHER_VU")) {
+      const int v = atoi(e);
+      c->gather_vu = (v == 16 || v == 4 || v == 2) ? v : 8;
+    }
     if (const char* e = getenv("HELIOS_GATHER_SPLIT_HOST")) c->split_host = atoi(e) != 0;
     if (c->gather_bulk) per_sm = 1;  // 192 KB of shared memory per CTA
     c->gather_ctas = c->sms * per_sm;

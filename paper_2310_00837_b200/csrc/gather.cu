@@ -149,6 +149,8 @@ struct GatherArgs {
   float stage_reserve;      // share of the batch's chunks (from the list's end) left to the stagers
   int64_t stage_max_chunks; // chunks the staging buffer holds (the stagers never claim more)
   bool vu16;                // HBM / peer rows: 16 (else 8) 16-byte loads in flight per lane
+  bool vu4;                 // HBM / peer rows: 4 loads in flight per lane (smaller register footprint)
+  bool vu2;                 // HBM / peer rows: 2 loads in flight per lane
   int* err;
   const char* hbm;          // this rank's shard
   char* const* peers;       // device [G]
@@ -483,10 +485,12 @@ __device__ __forceinline__ void host_rows_dyn(const GatherArgs& a, int64_t n_hos
 struct GatherGroup {  // the batches of one launch (gridDim.y), as SampleGroup
   GatherArgs a[kMaxGroup];
 };
-// VU: 16-byte loads in flight per lane for HBM / peer rows (8: 2 CTAs per SM fit the register file;
-// 16: HELIOS_GATHER_VU=16, one CTA per SM).
+// VU: 16-byte loads in flight per lane for HBM / peer rows.  The default 4 (80 registers) is slower
+// than 8 (113 registers) for K4 alone but faster in the pipeline, where K4's register footprint decides
+// how many of the other batches' sampler CTAs fit beside it; 2, 8 and 16
+// (HELIOS_GATHER_VU) are the measured alternatives.
 template <int VPL, int UH, bool BULK, bool HOST, int VU>
-__global__ void __launch_bounds__(256, VU > 8 ? 1 : 2) k_gather_lists(const __grid_constant__ GatherGroup P) {
+__global__ void __launch_bounds__(256, VU > 8 ? 1 : (VU == 4 ? 3 : (VU == 2 ? 4 : 2))) k_gather_lists(const __grid_constant__ GatherGroup P) {
   const GatherArgs& a = P.a[blockIdx.y];
   pdl_wait();
   pdl_trigger();
@@ -836,6 +840,10 @@ static void launch_gather(const GatherGroup& P, int n, int grid, bool bulk, cuda
     launch_pdl_smem(k_gather_lists<VPL, UH, true, HOST, 8>, dim3(grid, n), dim3(256), kBulkSmem, st, P);
   } else if (P.a[0].vu16) {
     launch_pdl(k_gather_lists<VPL, UH, false, HOST, 16>, dim3(grid, n), dim3(256), st, P);
+  } else if (P.a[0].vu4) {
+    launch_pdl(k_gather_lists<VPL, UH, false, HOST, 4>, dim3(grid, n), dim3(256), st, P);
+  } else if (P.a[0].vu2) {
+    launch_pdl(k_gather_lists<VPL, UH, false, HOST, 2>, dim3(grid, n), dim3(256), st, P);
   } else {
     launch_pdl(k_gather_lists<VPL, UH, false, HOST, 8>, dim3(grid, n), dim3(256), st, P);
   }
@@ -940,6 +948,8 @@ static GatherArgs make_args(helios_cache* c, GatherWS& w, void* out, helios_gath
   a.stage_reserve = c->stage_reserve;
   a.stage_max_chunks = w.stage_rows / kStageChunk;
   a.vu16 = c->gather_vu == 16;
+  a.vu4 = c->gather_vu == 4;
+  a.vu2 = c->gather_vu == 2;
   a.err = c->d_err;
   a.hbm = c->hbm;
   a.peers = c->d_peers;

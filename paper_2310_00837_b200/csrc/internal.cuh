@@ -278,7 +278,8 @@ struct helios_cache {
   int gather_ctas = 148;            // K4 grid (one CTA per SM with a host tier, more for HBM-only caches)
   bool split_host = true;           // host-tier rows in their own small kernel (HELIOS_GATHER_SPLIT_HOST=0: the
                                     // combined kernel, 2 host warps per 8)
-  int gather_vu = 8;                // HBM / peer rows: 16-byte loads in flight per lane (HELIOS_GATHER_VU)
+  int gather_vu = 4;                // HBM / peer rows: 16-byte loads in flight per lane (HELIOS_GATHER_VU = 2/4/8/16;
+                                    // 4: 80 registers, the footprint that leaves the sampler most room)
   bool gather_bulk = false;         // HELIOS_GATHER_BULK=1: HBM rows by cp.async.bulk (ablation)
   bool io_sync = false;            // HELIOS_CACHE_IO_SYNC ablation
   bool broken = false;             // a ring / staging watchdog fired: ring state is no longer consistent

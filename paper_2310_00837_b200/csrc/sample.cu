@@ -952,8 +952,12 @@ static void launch_fill(const helios_graph* g, const SampleGroup& P, int n, int 
     launch_pdl(k_fill_tile<G>, dim3(grid, n), dim3(256), st, P, h);
     return;
   }
+  static const int per_sm = [] {  // fill CTAs per SM at most (HELIOS_FILL_CTAS_PER_SM, default 2: leaves SM
+    const char* e = getenv("HELIOS_FILL_CTAS_PER_SM");  // slots to the other batches' kernels)
+    return e ? std::max(1, std::min(atoi(e), 8)) : 2;
+  }();
   const int64_t threads = std::max<int64_t>(rows, 1) * G;
-  const int grid = (int)std::min<int64_t>((threads + 255) / 256, (int64_t)g->sms * 4);
+  const int grid = (int)std::min<int64_t>((threads + 255) / 256, (int64_t)g->sms * per_sm);
   launch_pdl(k_fill_insert<G>, dim3(grid, n), dim3(256), st, P, h);
 }
 
