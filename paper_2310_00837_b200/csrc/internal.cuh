@@ -139,6 +139,7 @@ struct SampleWS {
   int32_t tile_rows[HELIOS_MAX_HOPS] = {};
   uint2* elist = nullptr;        // [cap_edges] per-tile distinct entries {global slot, tile minpos}
   uint32_t* ndist = nullptr;     // [tiles] distinct ids per tile
+  bool fill_seg = true;         // fill with f-lane segments (HELIOS_FILL_SEG=0: power-of-two lane groups)
   bool persistent = false;      // one cooperative kernel per batch instead of the 2+3L-kernel chain
                                 // (HELIOS_SAMPLE_PERSISTENT=1; measured slower)
   // per-batch parameters, read by the kernels from device memory so that a captured CUDA graph

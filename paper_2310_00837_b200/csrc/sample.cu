@@ -73,6 +73,7 @@ struct SampleCtx {
   int32_t tile_rows[HELIOS_MAX_HOPS];
   uint2* elist;
   uint32_t* ndist;
+  int32_t fill_seg;  // fill with f-lane segments (default; HELIOS_FILL_SEG=0: power-of-two groups)
 };
 
 // The batches of one launch (a plan slot's group): the chain's kernels run with
@@ -448,6 +449,54 @@ __device__ __forceinline__ void dev_assign_tile(const SampleCtx& c, int h) {
   }
 }
 
+// Hop h fill with S-lane segments, S = f_h (1 <= f_h <= 32; the default, HELIOS_FILL_SEG=0 disables): a warp samples
+// floor(32 / S) rows at once instead of 32 / G with G the power of two >= f (f = 5: 6 rows on 30 busy
+// lanes instead of 4 rows on 20; f = 10: 3 instead of 2), so the same rows hold a third fewer warp
+// slots.  Same draws, positions and inserts as dev_fill_insert (k <= f = S, so the serial path never
+// applies); shuffles and ballots use the segment's lane mask with explicit source lanes.
+__device__ __forceinline__ void dev_fill_seg(const SampleCtx& c, int h) {
+  const int lane = threadIdx.x & 31;
+  const int32_t f = c.fan[h];
+  const int S = f;
+  const int rpw = 32 / S;
+  const int seg = lane / S;
+  if (seg >= rpw) return;  // spare lanes (32 mod S of them); they take part in no shuffle
+  const int sl = lane - seg * S;
+  const int bl = seg * S;
+  const unsigned smask = (S == 32) ? 0xFFFFFFFFu : (((1u << S) - 1u) << bl);
+  const uint64_t key = (uint64_t)c.params[0];
+  const int64_t n = c.level_counts[h];
+  const int32_t* __restrict__ bp = c.bp[h];
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp * rpw + seg; i < n; i += nwarps * rpw) {
+    const int64_t v = c.nodes[i];
+    int64_t base = 0, d = 0;
+    if ((uint64_t)v < (uint64_t)c.V) {
+      base = c.indptr[v];
+      d = c.indptr[v + 1] - base;
+    }
+    const int64_t off = bp[i];
+    const int64_t k = min(d, (int64_t)f);
+    if (k == d) {  // every neighbour, CSR order, no RNG consumed
+      for (int64_t p = sl; p < d; p += S) insert_edge(c, off + p, (uint32_t)c.indices[base + p]);
+    } else {  // Floyd's k-subset, lane sl owning draw sl
+      uint32_t t = 0, m = 0;
+      if (sl < k) {
+        m = (uint32_t)(d - k + sl + 1);
+        t = __umulhi(philox_word(key, (uint32_t)h, (uint64_t)v, (uint32_t)sl), m);
+      }
+      uint32_t P = 0;
+      for (int j = 0; j < (int)k; j++) {
+        const uint32_t tj = __shfl_sync(smask, t, bl + j);
+        const unsigned hit = __ballot_sync(smask, sl < j && P == tj);
+        if (sl == j) P = hit ? (m - 1) : tj;
+      }
+      if (sl < k) insert_edge(c, off + sl, (uint32_t)c.indices[base + P]);
+    }
+  }
+}
+
 __device__ __forceinline__ int fill_group(int32_t f) { return (f < 0 || f > 16) ? 32 : (f > 8 ? 16 : (f > 4 ? 8 : 4)); }
 
 // Hop h dedup/relabel: flag = "this edge is the first occurrence of an id new at this hop"; the
@@ -548,6 +597,13 @@ __global__ void __launch_bounds__(256) k_fill_tile(const __grid_constant__ Sampl
   pdl_trigger();
   TraceScope ts(c.params, 3 * h + 1);
   dev_fill_tile<G>(c, h);
+}
+__global__ void __launch_bounds__(256) k_fill_seg(const __grid_constant__ SampleGroup P, int h) {
+  const SampleCtx& c = P.c[blockIdx.y];
+  pdl_wait();
+  pdl_trigger();
+  TraceScope ts(c.params, 3 * h + 1);
+  dev_fill_seg(c, h);
 }
 __global__ void __launch_bounds__(kScanBlock) k_assign_tile(const __grid_constant__ SampleGroup P, int h) {
   const SampleCtx& c = P.c[blockIdx.y];
@@ -877,6 +933,7 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
   p += 8;
   w.scan_bytes = (size_t)(p - w.scan_base);
   if (const char* e = getenv("HELIOS_SAMPLE_PERSISTENT")) w.persistent = atoi(e) != 0;
+  if (const char* e = getenv("HELIOS_FILL_SEG")) w.fill_seg = atoi(e) != 0;
   if (const char* e = getenv("HELIOS_SAMPLE_MODE")) {
     if (!strcmp(e, "cluster")) w.cluster = 8;
     else if (!strcmp(e, "cluster16")) w.cluster = 16;
@@ -941,6 +998,7 @@ static SampleCtx make_ctx(const helios_graph* g, const SampleWS& w, const int32_
   for (int h = 0; h < HELIOS_MAX_HOPS; h++) c.tile_rows[h] = (chain && h < L) ? w.tile_rows[h] : 0;
   c.elist = w.elist;
   c.ndist = w.ndist;
+  c.fill_seg = w.fill_seg ? 1 : 0;
   return c;
 }
 
@@ -956,6 +1014,13 @@ static void launch_fill(const helios_graph* g, const SampleGroup& P, int n, int 
     const char* e = getenv("HELIOS_FILL_CTAS_PER_SM");  // slots to the other batches' kernels)
     return e ? std::max(1, std::min(atoi(e), 8)) : 2;
   }();
+  const int32_t f = P.c[0].fan[h];
+  if (P.c[0].fill_seg && f >= 1 && f <= 32) {  // S-lane segments, floor(32 / f) rows per warp
+    const int64_t warps = (std::max<int64_t>(rows, 1) + 32 / f - 1) / (32 / f);
+    const int grid = (int)std::min<int64_t>((warps * 32 + 255) / 256, (int64_t)g->sms * per_sm);
+    launch_pdl(k_fill_seg, dim3(grid, n), dim3(256), st, P, h);
+    return;
+  }
   const int64_t threads = std::max<int64_t>(rows, 1) * G;
   const int grid = (int)std::min<int64_t>((threads + 255) / 256, (int64_t)g->sms * per_sm);
   launch_pdl(k_fill_insert<G>, dim3(grid, n), dim3(256), st, P, h);

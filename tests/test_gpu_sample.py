@@ -40,14 +40,17 @@ def assert_same(gpu, orc, L):
         assert np.array_equal(gpu["block_indices"][h], orc.block_indices[h]), f"hop {h} indices"
 
 
-@pytest.fixture(params=["chain", "cluster", "cluster16", "tiled"])
+@pytest.fixture(params=["chain", "cluster", "cluster16", "tiled", "groups"])
 def mode(request, monkeypatch):
     """Sampler launch mode (HELIOS_SAMPLE_MODE, read when a graph's workspace is allocated): the chain of
     2 + 3L kernels, or the whole batch in one launch of an 8- or 16-CTA cluster.  Same device code,
     so the same bits.  "tiled": the chain with the shared-memory tile dedup (HELIOS_SAMPLE_DEDUP=smem:
-    per-tile shared hash, bitmap ranking, tiled relabel) for every hop with a bounded fanout."""
-    monkeypatch.setenv("HELIOS_SAMPLE_MODE", "chain" if request.param == "tiled" else request.param)
+    per-tile shared hash, bitmap ranking, tiled relabel) for every hop with a bounded fanout.  "groups": the
+    chain with the round-1 power-of-two lane groups in the fill (HELIOS_FILL_SEG=0; the default packs
+    f-lane segments)."""
+    monkeypatch.setenv("HELIOS_SAMPLE_MODE", "chain" if request.param in ("tiled", "groups") else request.param)
     monkeypatch.setenv("HELIOS_SAMPLE_DEDUP", "smem" if request.param == "tiled" else "global")
+    monkeypatch.setenv("HELIOS_FILL_SEG", "0" if request.param == "groups" else "1")
     return request.param
 
 
