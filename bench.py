@@ -493,6 +493,10 @@ def main():
     seed_of = {b: torch.as_tensor(inp.batches[b]).cuda() for b in sorted(set(seq))}
     stream = torch.cuda.current_stream()
     depth = args.depth if args.depth > 0 else (24 if S > 0 else 12)
+    # gather kernels of this cache: fused lookup+gather when every row is in HBM, else the
+    # lookup, the HBM part and (with a host tier) the host part in its own kernel
+    direct = S == 0 and not file_cfg and os.environ.get("HELIOS_GATHER_DIRECT") != "0" and not os.environ.get("HELIOS_GATHER_BULK")
+    split = S > 0 and os.environ.get("HELIOS_GATHER_SPLIT_HOST") != "0"
     pflags = ((H.PLAN_NO_GRAPH if args.no_graph else 0) | (H.PLAN_SERIAL_GATHER if args.serial_gather else 0)
               | (H.PLAN_INTRA_BATCH if args.intra else 0) | (H.PLAN_LINK_STREAM if args.link_stream else 0))
     G = args.group
@@ -701,7 +705,10 @@ def main():
         # achieved = the timed launches' algorithmic bytes / the time at least one of them was running
         achieved = alg_bytes * n_timed / (gather_busy_ms * 1e6)
         peak = alg_bytes / (t_roof_ms * 1e6)
-        roof = {"bound": dominant, "kernel": "k_lookup + k_gather_lists (K3+K4)", "achieved": round(achieved, 2),
+        kname = ("k_gather_direct (K3 fused into K4: every row in HBM)" if direct else
+                 "k_lookup + k_gather_lists + k_gather_host (K3 + K4 HBM part + K4 host part)" if split else
+                 "k_lookup + k_gather_lists (K3+K4)")
+        roof = {"bound": dominant, "kernel": kname, "achieved": round(achieved, 2),
                 "peak": round(peak, 2), "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "traffic": traffic_of(cfg.name), "launch_ms": round(g_ms, 4),
                 "busy_ms": round(gather_busy_ms, 3), "launches_timed": n_timed,
@@ -754,9 +761,10 @@ def main():
                                      "as staged)"}
     value = world * steps / (max_ms / 1e3)
     e2e_val = world * steps / e2e_s
-    # per group launch: the sampling chain (3L + 2 kernels), lookup + gather (2), the staged-tier publish;
+    # per group launch: the sampling chain (3L + 2 kernels), the gather kernels, the staged-tier publish;
     # per batch: the IO kernel + its finish (file tier), the link-stream host kernel (G = 1 only)
-    per_group = 3 * L + 2 + 2 + (1 if (args.host_staged > 0 and S > 0) else 0)
+    gather_kernels = 1 if direct else (3 if split else 2)   # fused lookup+gather | lookup, HBM part, host part
+    per_group = 3 * L + 2 + gather_kernels + (1 if (args.host_staged > 0 and S > 0) else 0)
     per_batch = (2 if c.info().file_rows > 0 else 0) + (1 if plan.link else 0)
     gpu_launches = per_group * ((steps + G - 1) // G) + per_batch * steps
     out = {

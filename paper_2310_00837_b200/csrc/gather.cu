@@ -257,6 +257,121 @@ __device__ __forceinline__ void flat_rows(const GatherArgs& a, int q, int64_t cn
   }
 }
 
+// ---- fused lookup + gather for caches whose rows all live in HBM (C2: no host or file tier) -----------
+// K3 exists to split N_L into per-tier lists; with every row in the HBM tier (local or a peer shard)
+// there is nothing to split, so one kernel resolves dir[v] and copies the row, with K4's flat 16-byte
+// mapping: lanes < rw read nodes[lo + j] and dir[v] of the warp's next rows (in flight while the current
+// rows load), and out row = lo + j.  Per-tier row counts go to the ctl words (one atomic per warp
+// group); the last CTA to finish writes the stats.  Out-of-range ids latch E_RANGE and copy nothing,
+// as k_lookup does.
+struct DirectArgs {
+  const int64_t* nodes;
+  const int64_t* lo_ptr;
+  const int64_t* n_nodes;
+  const int64_t* dir;
+  int64_t V;
+  int32_t rank;
+};
+struct DirectGroup {
+  GatherArgs a[kMaxGroup];
+  DirectArgs d[kMaxGroup];
+};
+template <int VU>
+__global__ void __launch_bounds__(256, VU == 4 ? 3 : 2) k_gather_direct(const __grid_constant__ DirectGroup P) {
+  const GatherArgs& a = P.a[blockIdx.y];
+  const DirectArgs& D = P.d[blockIdx.y];
+  pdl_wait();
+  pdl_trigger();
+  TraceScope ts(a.trace_params, a.trace_idx);
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int nvec = a.R >> 4;
+  const int64_t lo = D.lo_ptr ? *D.lo_ptr : 0;
+  const int64_t cnt = *D.n_nodes - lo;
+  const int rw = max(1, 32 * VU / nvec);
+  const uint32_t inv = ((1u << 20) + (uint32_t)nvec - 1u) / (uint32_t)nvec;
+  const int64_t step = nw * rw;
+  unsigned long long n_local = 0, n_peer = 0;
+  auto resolve = [&](int64_t j, const char** sp, char** dp) {
+    *sp = nullptr;
+    *dp = nullptr;
+    if (lane < rw && j + lane < cnt) {
+      const int64_t i = lo + j + lane;
+      const int64_t v = D.nodes[i];
+      if ((uint64_t)v < (uint64_t)D.V) {
+        const uint64_t w = (uint64_t)D.dir[v];
+        const int owner = (int)((w >> 56) & 63);
+        const char* base = owner == D.rank ? a.hbm : a.peers[owner];
+        *sp = base + (int64_t)(w & ((1ull << 56) - 1)) * a.R;
+        *dp = a.out + i * (int64_t)a.R;
+        if (owner == D.rank) n_local++;
+        else n_peer++;
+      } else {
+        latch(a.err, HELIOS_E_RANGE);
+      }
+    }
+  };
+  int64_t j0 = gw * rw;
+  const char* sp = nullptr;
+  char* dp = nullptr;
+  if (j0 < cnt) resolve(j0, &sp, &dp);
+  for (; j0 < cnt; j0 += step) {
+    const char* sp_n = nullptr;
+    char* dp_n = nullptr;
+    if (j0 + step < cnt) resolve(j0 + step, &sp_n, &dp_n);
+    const int nrows = (int)min((int64_t)rw, cnt - j0);
+    const int nv = nrows * nvec;
+    for (int b0 = 0; b0 < nv; b0 += 32 * VU) {
+      int4 r[VU];
+#pragma unroll
+      for (int k = 0; k < VU; k++) {
+        const int f = b0 + lane + 32 * k;
+        const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
+        const char* src = (const char*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)sp, row);
+        if (f < nv && src) r[k] = ld_stream((const int4*)src + (f - row * nvec));
+      }
+#pragma unroll
+      for (int k = 0; k < VU; k++) {
+        const int f = b0 + lane + 32 * k;
+        const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
+        char* dst = (char*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)dp, row);
+        if (f < nv && dst) st_global_v4((int4*)dst + (f - row * nvec), r[k]);
+      }
+    }
+    sp = sp_n;
+    dp = dp_n;
+  }
+  // per-tier counts: warp sums, one atomic per warp, then the last CTA publishes the stats
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n_local += __shfl_xor_sync(0xFFFFFFFFu, n_local, o);
+    n_peer += __shfl_xor_sync(0xFFFFFFFFu, n_peer, o);
+  }
+  if (lane == 0) {
+    if (n_local) atomicAdd(&a.ctl[kListLocal], n_local);
+    if (n_peer) atomicAdd(&a.ctl[kListPeer], n_peer);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && a.stats) {
+    __threadfence();
+    const unsigned long long t = atomicAdd(&a.ctl[kCtlDone], 1ull);
+    if (t == gridDim.x - 1) {  // every CTA's counts are in
+      __threadfence();
+      const int64_t nl = (int64_t)ld_volatile_u64(&a.ctl[kListLocal]), np = (int64_t)ld_volatile_u64(&a.ctl[kListPeer]);
+      if (a.accumulate) {
+        a.stats->rows_hbm_local += nl;
+        a.stats->rows_hbm_peer += np;
+      } else {
+        a.stats->rows_hbm_local = nl;
+        a.stats->rows_hbm_peer = np;
+        a.stats->rows_host = 0;
+      }
+      a.stats->rows_file = 0;
+    }
+  }
+}
+
 // ---- bulk-copy (TMA engine) variant of the HBM / peer row copy (HELIOS_GATHER_BULK=1) ----------
 // Rows move global -> shared -> global with cp.async.bulk (SASS UBLKCP): no register staging, and up
 // to kBulkWarpBytes per warp in flight per direction.  Lane l of a warp owns row slot l of each of
@@ -989,6 +1104,18 @@ static helios_status gather_pass_group(helios_cache* c, GatherWS* const* ws, con
     PP.seq[b] = w.d_seq;
     PP.mail[b] = w.d_mail;
     staged = GP.a[b].staged;
+  }
+  if (c->direct && c->S == 0 && !c->has_file && part == kPartAll && !c->gather_bulk) {  // every row in HBM
+    DirectGroup DP{};
+    for (int b = 0; b < n; b++) {
+      DP.a[b] = GP.a[b];
+      DP.d[b] = DirectArgs{nodes[b], lo, n_nodes[b], (const int64_t*)c->dir, c->V, c->rank};
+      if (!first) HCUDA(cudaMemsetAsync(ws[b]->d_ctl + kCtlDone, 0, sizeof(unsigned long long), st));
+    }
+    if (c->gather_vu == 8) launch_pdl(k_gather_direct<8>, dim3(c->gather_ctas, n), dim3(256), st, DP);
+    else launch_pdl(k_gather_direct<4>, dim3(c->gather_ctas, n), dim3(256), st, DP);
+    HCUDA(cudaGetLastError());
+    return HELIOS_OK;
   }
   const int lg = (int)std::min<int64_t>(std::max<int64_t>(1, (max_rows + 255) / 256), (int64_t)c->sms * 2);
   launch_pdl(k_lookup, dim3(lg, n), dim3(256), st, LP);

@@ -153,7 +153,7 @@ struct SampleWS {
 // Per-gather bookkeeping (one per gather context): per-tier work lists written by the lookup
 // kernel, and the ticket / count words shared with the gather and IO kernels.
 enum : int { kListLocal = 0, kListPeer = 1, kListHost = 2, kListFile = 3, kLists = 4 };
-enum : int { kCtlSubmit = 4, kCtlComplete = 5, kCtlStageSeq = 6, kCtlHostTicket = 7, kCtlWords = 8 };
+enum : int { kCtlSubmit = 4, kCtlComplete = 5, kCtlStageSeq = 6, kCtlHostTicket = 7, kCtlDone = 8, kCtlWords = 9 };
 // Which rows a k_gather_lists launch copies: every tier (one kernel), only the HBM tiers (local +
 // peer), or only the host tier (zero-copy + staged rows; the plan's link stream).
 enum : int { kPartAll = 0, kPartHbm = 1, kPartHost = 2 };
@@ -277,6 +277,7 @@ struct helios_cache {
   int world = 1, world_rank = 0;    // the caller's world size / rank (G, rank: the directory's)
   int io_ctas = 32;
   int gather_ctas = 148;            // K4 grid (one CTA per SM with a host tier, more for HBM-only caches)
+  bool direct = true;               // HBM-only caches: lookup fused into the gather (HELIOS_GATHER_DIRECT=0: K3 + K4)
   bool split_host = true;           // host-tier rows in their own small kernel (HELIOS_GATHER_SPLIT_HOST=0: the
                                     // combined kernel, 2 host warps per 8)
   int gather_vu = 4;                // HBM / peer rows: 16-byte loads in flight per lane (HELIOS_GATHER_VU = 2/4/8/16;

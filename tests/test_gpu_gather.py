@@ -130,6 +130,28 @@ def test_io_ring_wraparound_and_fault(H, c1, c1_hot, sync):
     c.free()
 
 
+@pytest.mark.parametrize("direct", ["1", "0"])
+def test_hbm_only_direct_gather(H, c1, c1_hot, direct, monkeypatch):
+    """Caches whose rows all live in HBM run the fused lookup + gather kernel (default) instead of K3 + K4
+    (HELIOS_GATHER_DIRECT=0): same bytes, same tier counts, out-of-range ids latch E_RANGE."""
+    monkeypatch.setenv("HELIOS_GATHER_DIRECT", direct)
+    g, hot = c1_hot
+    cfg = c1.cfg
+    c = H.helios_cache_build(g, hot, cfg.R, cfg.V, 0, host_table=c1.table)
+    dref, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, cfg.V, 0)
+    rng = np.random.default_rng(11)
+    for n in (1, 31, 257, 1000, cfg.V):
+        nodes = rng.permutation(cfg.V)[:n]
+        gather_and_check(H, c, c1, nodes, oracle.lookup_counts(dref, nodes))
+    bad = torch.tensor([3, cfg.V + 5, 7], dtype=torch.int64, device="cuda")
+    out = torch.empty((3, cfg.R), dtype=torch.uint8, device="cuda")
+    H.helios_gather(c, bad, torch.tensor([3], device="cuda"), out)
+    with pytest.raises(H.HeliosError) as e:
+        H.helios_sync(c)
+    assert e.value.name == "E_RANGE"
+    c.free()
+
+
 @pytest.mark.parametrize("split", ["1", "0"])
 @pytest.mark.parametrize("staged,reserve", [(False, 0), (True, 0), (True, 0.7)])
 def test_split_host_kernel(H, c1, c1_hot, staged, reserve, split, monkeypatch):

@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, tag, q, replicated):
+def _worker(rank, world, port, tag, q, replicated, hbm_only=False):
     import faulthandler
     faulthandler.dump_traceback_later(100, exit=True)
     sys.path.insert(0, ROOT)
@@ -57,12 +57,15 @@ def _worker(rank, world, port, tag, q, replicated):
         S = cfg.V - G * Hr
         rf = H.HBM_REPLICATED if replicated else 0
         name = f"helios_mr_{tag}"
-        if rank == 0:   # creator first, then the others map it (after the barrier)
+        if hbm_only:   # every row in the (sharded) HBM tier: the fused lookup + gather path with peer rows
+            Hr, S = -(-cfg.V // world), 0
+            c = H.helios_cache_build(g, hot, cfg.R, Hr, 0, host_table=inp.table, world_size=world, rank=rank)
+        elif rank == 0:   # creator first, then the others map it (after the barrier)
             tier, m = hd.shared_array(name, (S * cfg.R,), np.uint8, create=True)
             c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=inp.table, world_size=world, rank=rank,
                                      host_tier=tier, flags=H.HOST_FILL | rf)
         dist.barrier()
-        if rank != 0:
+        if rank != 0 and not hbm_only:
             tier, m = hd.shared_array(name, (S * cfg.R,), np.uint8, create=False)
             c = H.helios_cache_build(g, hot, cfg.R, Hr, S, host_table=inp.table, world_size=world, rank=rank,
                                      host_tier=tier, flags=rf)
@@ -95,21 +98,22 @@ def _worker(rank, world, port, tag, q, replicated):
         p.free()
         c.free()
         dist.barrier()
-        if rank == 0:
+        if rank == 0 and not hbm_only:
             hd.unlink_shared(name)
         q.put((rank, bool(ok), peer_rows, len(mine)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("replicated", [False, True], ids=["sharded", "replicated"])
-def test_two_ranks_one_gpu(replicated):
+@pytest.mark.parametrize("replicated,hbm_only", [(False, False), (True, False), (False, True)],
+                         ids=["sharded", "replicated", "hbm_only_sharded"])
+def test_two_ranks_one_gpu(replicated, hbm_only):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     tag = f"{os.getpid()}_{port}"
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, tag, q, replicated)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, tag, q, replicated, hbm_only)) for r in range(2)]
     for p in ps:
         p.start()
     res = [q.get(timeout=150) for _ in ps]
