@@ -276,6 +276,39 @@ struct DirectGroup {
   GatherArgs a[kMaxGroup];
   DirectArgs d[kMaxGroup];
 };
+// Per-tier counts of a fused lookup + gather: warp sums, one atomic per warp, then the last CTA
+// publishes the stats.
+__device__ __forceinline__ void direct_counts_publish(const GatherArgs& a, unsigned long long n_local,
+                                                      unsigned long long n_peer, int lane) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n_local += __shfl_xor_sync(0xFFFFFFFFu, n_local, o);
+    n_peer += __shfl_xor_sync(0xFFFFFFFFu, n_peer, o);
+  }
+  if (lane == 0) {
+    if (n_local) atomicAdd(&a.ctl[kListLocal], n_local);
+    if (n_peer) atomicAdd(&a.ctl[kListPeer], n_peer);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && a.stats) {
+    __threadfence();
+    const unsigned long long t = atomicAdd(&a.ctl[kCtlDone], 1ull);
+    if (t == gridDim.x - 1) {  // every CTA's counts are in
+      __threadfence();
+      const int64_t nl = (int64_t)ld_volatile_u64(&a.ctl[kListLocal]), np = (int64_t)ld_volatile_u64(&a.ctl[kListPeer]);
+      if (a.accumulate) {
+        a.stats->rows_hbm_local += nl;
+        a.stats->rows_hbm_peer += np;
+      } else {
+        a.stats->rows_hbm_local = nl;
+        a.stats->rows_hbm_peer = np;
+        a.stats->rows_host = 0;
+      }
+      a.stats->rows_file = 0;
+    }
+  }
+}
+
 template <int VU>
 __global__ void __launch_bounds__(256, VU == 4 ? 3 : 2) k_gather_direct(const __grid_constant__ DirectGroup P) {
   const GatherArgs& a = P.a[blockIdx.y];
@@ -342,34 +375,130 @@ __global__ void __launch_bounds__(256, VU == 4 ? 3 : 2) k_gather_direct(const __
     sp = sp_n;
     dp = dp_n;
   }
-  // per-tier counts: warp sums, one atomic per warp, then the last CTA publishes the stats
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    n_local += __shfl_xor_sync(0xFFFFFFFFu, n_local, o);
-    n_peer += __shfl_xor_sync(0xFFFFFFFFu, n_peer, o);
-  }
-  if (lane == 0) {
-    if (n_local) atomicAdd(&a.ctl[kListLocal], n_local);
-    if (n_peer) atomicAdd(&a.ctl[kListPeer], n_peer);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && a.stats) {
-    __threadfence();
-    const unsigned long long t = atomicAdd(&a.ctl[kCtlDone], 1ull);
-    if (t == gridDim.x - 1) {  // every CTA's counts are in
-      __threadfence();
-      const int64_t nl = (int64_t)ld_volatile_u64(&a.ctl[kListLocal]), np = (int64_t)ld_volatile_u64(&a.ctl[kListPeer]);
-      if (a.accumulate) {
-        a.stats->rows_hbm_local += nl;
-        a.stats->rows_hbm_peer += np;
+  direct_counts_publish(a, n_local, n_peer, lane);
+}
+
+// ---- fused lookup + gather with the loads staged through shared memory (HELIOS_GATHER_ASYNC=D) --------
+// The same flat 16-byte mapping as k_gather_direct<VU>, but the loads are cp.async (SASS LDGSTS) into a
+// per-warp shared-memory ring of D stages instead of registers: a lane keeps D x VU 16-byte loads in
+// flight (D = 4, VU = 4: 256 B per lane, 64 KB per 256-thread CTA, four times the register path's)
+// while holding only the D groups' destination pointers in registers.  Group t is issued into stage
+// t mod D; once D groups are committed the oldest is complete (cp.async.wait_group D-1) and each lane
+// stores the vectors IT loaded (no cross-lane shared-memory traffic, so no barrier).  Node ids of
+// group t+2 and directory words of group t+1 are loaded while group t's rows are issued.  Requires
+// nvec <= 32 * VU (one pass per group: R <= 2 KB at VU = 4); larger rows take k_gather_direct.
+// Measured (C2, profiles/r02/k4_async.jsonl, gather_async_window_c2.jsonl): alone no faster than the
+// register path at the same grid (30.6 vs 30.5 us at 1 CTA per SM, 21.3 vs 20.3 at 2), and the whole
+// C2 step drops from 33.0 k to 20.6 k (D = 4) / 24.9 k (D = 8) batches/s: a 74-147 KB shared-memory
+// CTA needs an SM carve-out the sampler kernels' CTAs (little shared memory) do not share, so they
+// stop co-residing with the gather.  Kept as an opt-in ablation.
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ int4 ld_shared_v4(const int4* p) {
+  int4 r;
+  asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+  return r;
+}
+
+template <int VU, int D>
+__global__ void __launch_bounds__(256, 3) k_gather_direct_async(const __grid_constant__ DirectGroup P) {
+  extern __shared__ int4 s_ring[];  // [warp][D][VU][32] row vectors, then [warp][D][32] destination rows
+  const GatherArgs& a = P.a[blockIdx.y];
+  const DirectArgs& Dg = P.d[blockIdx.y];
+  pdl_wait();
+  pdl_trigger();
+  TraceScope ts(a.trace_params, a.trace_idx);
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  int4* ring = s_ring + wid * (D * VU * 32);
+  char** s_dst = reinterpret_cast<char**>(s_ring + (blockDim.x >> 5) * (D * VU * 32)) + wid * (D * 32);
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int nvec = a.R >> 4;
+  const int64_t lo = Dg.lo_ptr ? *Dg.lo_ptr : 0;
+  const int64_t cnt = *Dg.n_nodes - lo;
+  const int rw = max(1, 32 * VU / nvec);
+  const uint32_t inv = ((1u << 20) + (uint32_t)nvec - 1u) / (uint32_t)nvec;
+  const int64_t step = nw * rw;
+  const int64_t j0 = gw * rw;
+  const int64_t ng = (j0 < cnt) ? (cnt - j0 + step - 1) / step : 0;  // groups of this warp
+  unsigned long long n_local = 0, n_peer = 0;
+  // row of group t owned by this lane (lanes < rw): node id 2 groups ahead, pointers 1 group ahead
+  auto node_of = [&](int64_t t) -> int64_t {
+    const int64_t j = j0 + t * step + lane;
+    return (t < ng && lane < rw && j < cnt) ? Dg.nodes[lo + j] : -1;
+  };
+  auto resolve = [&](int64_t t, int64_t v, const char** sp, char** dp) {
+    *sp = nullptr;
+    *dp = nullptr;
+    const int64_t j = j0 + t * step + lane;
+    if (t < ng && lane < rw && j < cnt) {
+      if ((uint64_t)v < (uint64_t)Dg.V) {
+        const uint64_t w = (uint64_t)Dg.dir[v];
+        const int owner = (int)((w >> 56) & 63);
+        const char* base = owner == Dg.rank ? a.hbm : a.peers[owner];
+        *sp = base + (int64_t)(w & ((1ull << 56) - 1)) * a.R;
+        *dp = a.out + (lo + j) * (int64_t)a.R;
+        if (owner == Dg.rank) n_local++;
+        else n_peer++;
       } else {
-        a.stats->rows_hbm_local = nl;
-        a.stats->rows_hbm_peer = np;
-        a.stats->rows_host = 0;
+        latch(a.err, HELIOS_E_RANGE);
       }
-      a.stats->rows_file = 0;
+    }
+  };
+  const char* sp = nullptr;
+  char* dp = nullptr;
+  resolve(0, node_of(0), &sp, &dp);
+  int64_t v_n = node_of(1);
+  int s = 0;  // stage of group t
+  for (int64_t t = 0; t < ng + D - 1; t++) {
+    if (t < ng) {  // issue group t into stage s
+      const int64_t v_nn = node_of(t + 2);
+      const char* sp_n;
+      char* dp_n;
+      resolve(t + 1, v_n, &sp_n, &dp_n);
+      const int nv = (int)min((int64_t)rw, cnt - (j0 + t * step)) * nvec;
+      int4* st = ring + s * (VU * 32);
+#pragma unroll
+      for (int k = 0; k < VU; k++) {
+        const int f = lane + 32 * k;
+        const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
+        const char* src = (const char*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)sp, row);
+        if (f < nv && src) cp_async16(st + lane + 32 * k, (const int4*)src + (f - row * nvec));
+      }
+      if (lane < rw) s_dst[s * 32 + lane] = dp;
+      sp = sp_n;
+      dp = dp_n;
+      v_n = v_nn;
+    }
+    cp_async_commit();
+    s = (s + 1 == D) ? 0 : s + 1;  // = the stage of group t - (D - 1), the oldest in flight
+    const int64_t tc = t - (D - 1);
+    if (tc >= 0) {  // complete and store group tc (tc < ng always: t < ng + D - 1)
+      cp_async_wait<D - 1>();
+      __syncwarp();
+      const int nv = (int)min((int64_t)rw, cnt - (j0 + tc * step)) * nvec;
+      const int4* st = ring + s * (VU * 32);
+#pragma unroll
+      for (int k = 0; k < VU; k++) {
+        const int f = lane + 32 * k;
+        const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
+        char* dst = s_dst[s * 32 + row];
+        if (f < nv && dst) st_global_v4((int4*)dst + (f - row * nvec), ld_shared_v4(st + lane + 32 * k));
+      }
+      __syncwarp();
     }
   }
+  cp_async_wait<0>();
+  direct_counts_publish(a, n_local, n_peer, lane);
 }
 
 // ---- bulk-copy (TMA engine) variant of the HBM / peer row copy (HELIOS_GATHER_BULK=1) ----------
@@ -1075,6 +1204,16 @@ static GatherArgs make_args(helios_cache* c, GatherWS& w, void* out, helios_gath
   return a;
 }
 
+template <int VU, int D>
+static cudaError_t launch_direct_async(const DirectGroup& DP, int n, int ctas, cudaStream_t st) {
+  constexpr size_t smem = (size_t)8 * D * 32 * (VU * sizeof(int4) + sizeof(char*));  // 8 warps x D stages
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_gather_direct_async<VU, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (attr != cudaSuccess) return attr;
+  launch_pdl_smem(k_gather_direct_async<VU, D>, dim3(ctas, n), dim3(256), smem, st, DP);
+  return cudaGetLastError();
+}
+
 // One lookup + gather pass over rows [*lo, *n_nodes) (lo = NULL: all) of each of the n batches of a
 // group (one launch of each kernel, gridDim.y = n).  first: reset every count; otherwise (later
 // intra-batch passes, n = 1) only the per-pass tier counts and row tickets are reset, so the file
@@ -1112,8 +1251,15 @@ static helios_status gather_pass_group(helios_cache* c, GatherWS* const* ws, con
       DP.d[b] = DirectArgs{nodes[b], lo, n_nodes[b], (const int64_t*)c->dir, c->V, c->rank};
       if (!first) HCUDA(cudaMemsetAsync(ws[b]->d_ctl + kCtlDone, 0, sizeof(unsigned long long), st));
     }
-    if (c->gather_vu == 8) launch_pdl(k_gather_direct<8>, dim3(c->gather_ctas, n), dim3(256), st, DP);
-    else launch_pdl(k_gather_direct<4>, dim3(c->gather_ctas, n), dim3(256), st, DP);
+    if (c->gather_async && c->R / 16 <= 32 * 4) {  // loads staged through shared memory (cp.async)
+      const cudaError_t e = c->gather_async >= 8 ? launch_direct_async<4, 8>(DP, n, c->gather_ctas, st)
+                                                 : launch_direct_async<4, 4>(DP, n, c->gather_ctas, st);
+      HCUDA(e);
+    } else if (c->gather_vu == 8) {
+      launch_pdl(k_gather_direct<8>, dim3(c->gather_ctas, n), dim3(256), st, DP);
+    } else {
+      launch_pdl(k_gather_direct<4>, dim3(c->gather_ctas, n), dim3(256), st, DP);
+    }
     HCUDA(cudaGetLastError());
     return HELIOS_OK;
   }

@@ -282,6 +282,7 @@ struct helios_cache {
                                     // combined kernel, 2 host warps per 8)
   int gather_vu = 4;                // HBM / peer rows: 16-byte loads in flight per lane (HELIOS_GATHER_VU = 2/4/8/16;
                                     // 4: 80 registers, the footprint that leaves the sampler most room)
+  int gather_async = 0;             // HBM-only fused gather: loads staged through a D-stage shared ring (HELIOS_GATHER_ASYNC=D, 4 or 8)
   bool gather_bulk = false;         // HELIOS_GATHER_BULK=1: HBM rows by cp.async.bulk (ablation)
   bool io_sync = false;            // HELIOS_CACHE_IO_SYNC ablation
   bool broken = false;             // a ring / staging watchdog fired: ring state is no longer consistent

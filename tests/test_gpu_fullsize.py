@@ -94,6 +94,21 @@ def test_c2_full_size_plan(H, monkeypatch):
     b = check_batches(H, inp, g, c, dref, 20, depth=12)
     for k in a:
         assert np.array_equal(a[k][1], b[k][1])
+    monkeypatch.delenv("HELIOS_SAMPLE_DEDUP")
+    # and with the other fused-gather variants (read at cache build): 8 loads per lane, a cp.async
+    # shared-memory ring
+    for env in ({"HELIOS_GATHER_VU": "8"}, {"HELIOS_GATHER_ASYNC": "4"}):
+        for k in ("HELIOS_GATHER_VU", "HELIOS_GATHER_ASYNC"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        hot = torch.zeros(inp.cfg.V, dtype=torch.int64, device="cuda")
+        c2 = H.helios_cache_build(g, hot, inp.cfg.R, inp.cfg.V, 0, host_table=inp.table)
+        d2, _ = oracle.cache_dir(hot.cpu().numpy().astype(np.uint64), 1, inp.cfg.V, 0)
+        b = check_batches(H, inp, g, c2, d2, 20, depth=12)
+        for k in a:
+            assert np.array_equal(a[k][1], b[k][1])
+        c2.free()
     c.free()
     g.free()
 
