@@ -791,6 +791,12 @@ def main():
                                         else "split (own 64-thread kernel behind the HBM part)") if S > 0 else None,
                    "batches_in_flight": P, "plan_slots": depth, "batches_per_launch": G, "cuda_graphs": not args.no_graph, "serial_gather": bool(args.serial_gather),
                    "link_stream": bool(plan.link),
+                   "table_home": {"0": "whole table"}.get(os.environ.get("HELIOS_TABLE_HOME", ""),
+                                                         "adaptive (2^k >= 2.5 n_L of the slot's previous batch)"
+                                                         if "HELIOS_TABLE_HOME" not in os.environ else
+                                                         f"fixed {os.environ['HELIOS_TABLE_HOME']} slots"),
+                   "gather_l2_policy": "evict_first (fused HBM-only gather)" if S == 0 and os.environ.get("HELIOS_GATHER_EVICT", "1") != "0"
+                                       else "default",
                    "intra_batch_pipeline": bool(args.intra),
                    "topology": "pinned host, zero-copy (UVA)" if args.topo_host else "HBM",
                    "tiers": {"hbm_frac": cfg.hbm_frac, "host_frac": cfg.host_frac},

@@ -93,9 +93,13 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
 
 // Open-addressing (linear probing) insert-or-find of key u at edge position e: returns the slot,
 // *fresh = created here (with minpos = e); an existing slot's minpos is lowered to e if larger.
-__device__ __forceinline__ uint32_t table_insert(TableSlot* tab, uint32_t mask, uint32_t u, uint32_t e, bool* fresh) {
+// Keys are homed in the table's first hmask+1 slots (hmask <= mask, both 2^k - 1) and probe on through
+// the whole table (wrapping at mask), so any home region is correct at any load (the table is sized
+// for the worst case); a home region sized to the batch keeps its slots dense in L2 lines.
+__device__ __forceinline__ uint32_t table_insert(TableSlot* tab, uint32_t mask, uint32_t hmask, uint32_t u, uint32_t e,
+                                                 bool* fresh) {
   const unsigned long long want = ((unsigned long long)u << 32) | e;
-  uint32_t s = hash32(u) & mask;
+  uint32_t s = hash32(u) & hmask;
   for (;;) {
     unsigned long long w = ld_volatile_u64(&tab[s].km);
     if ((uint32_t)(w >> 32) == kEmpty) {

@@ -30,6 +30,27 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
   return r;
 }
 
+// Evict-first variants (L2 cache policy from createpolicy): the gather's 2 x R bytes per row stream
+// through L2 once, so marking them first-to-evict leaves the L2 to the sampler's tables and CSR sectors
+// of the other batches in flight (HELIOS_GATHER_EVICT=1, HBM-only fused gather).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int4 ld_stream_ef(const int4* p, uint64_t pol) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st_global_v4_ef(int4* p, int4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w),
+               "l"(pol)
+               : "memory");
+}
+
 // Base pointers of the four tier lists (device memory).  In staged mode the host list's directory
 // words are mirrored into pinned memory (host_w_mirror) for the host stager threads.
 struct ListPtrs {
@@ -309,7 +330,7 @@ __device__ __forceinline__ void direct_counts_publish(const GatherArgs& a, unsig
   }
 }
 
-template <int VU>
+template <int VU, bool EF>
 __global__ void __launch_bounds__(256, VU == 4 ? 3 : 2) k_gather_direct(const __grid_constant__ DirectGroup P) {
   const GatherArgs& a = P.a[blockIdx.y];
   const DirectArgs& D = P.d[blockIdx.y];
@@ -325,6 +346,7 @@ __global__ void __launch_bounds__(256, VU == 4 ? 3 : 2) k_gather_direct(const __
   const int rw = max(1, 32 * VU / nvec);
   const uint32_t inv = ((1u << 20) + (uint32_t)nvec - 1u) / (uint32_t)nvec;
   const int64_t step = nw * rw;
+  const uint64_t pol = EF ? policy_evict_first() : 0;
   unsigned long long n_local = 0, n_peer = 0;
   auto resolve = [&](int64_t j, const char** sp, char** dp) {
     *sp = nullptr;
@@ -362,14 +384,17 @@ __global__ void __launch_bounds__(256, VU == 4 ? 3 : 2) k_gather_direct(const __
         const int f = b0 + lane + 32 * k;
         const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
         const char* src = (const char*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)sp, row);
-        if (f < nv && src) r[k] = ld_stream((const int4*)src + (f - row * nvec));
+        if (f < nv && src) r[k] = EF ? ld_stream_ef((const int4*)src + (f - row * nvec), pol) : ld_stream((const int4*)src + (f - row * nvec));
       }
 #pragma unroll
       for (int k = 0; k < VU; k++) {
         const int f = b0 + lane + 32 * k;
         const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
         char* dst = (char*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)dp, row);
-        if (f < nv && dst) st_global_v4((int4*)dst + (f - row * nvec), r[k]);
+        if (f < nv && dst) {
+          if (EF) st_global_v4_ef((int4*)dst + (f - row * nvec), r[k], pol);
+          else st_global_v4((int4*)dst + (f - row * nvec), r[k]);
+        }
       }
     }
     sp = sp_n;
@@ -1256,9 +1281,11 @@ static helios_status gather_pass_group(helios_cache* c, GatherWS* const* ws, con
                                                  : launch_direct_async<4, 4>(DP, n, c->gather_ctas, st);
       HCUDA(e);
     } else if (c->gather_vu == 8) {
-      launch_pdl(k_gather_direct<8>, dim3(c->gather_ctas, n), dim3(256), st, DP);
+      if (c->gather_evict) launch_pdl(k_gather_direct<8, true>, dim3(c->gather_ctas, n), dim3(256), st, DP);
+      else launch_pdl(k_gather_direct<8, false>, dim3(c->gather_ctas, n), dim3(256), st, DP);
     } else {
-      launch_pdl(k_gather_direct<4>, dim3(c->gather_ctas, n), dim3(256), st, DP);
+      if (c->gather_evict) launch_pdl(k_gather_direct<4, true>, dim3(c->gather_ctas, n), dim3(256), st, DP);
+      else launch_pdl(k_gather_direct<4, false>, dim3(c->gather_ctas, n), dim3(256), st, DP);
     }
     HCUDA(cudaGetLastError());
     return HELIOS_OK;

@@ -132,7 +132,8 @@ struct SampleWS {
   // [scan_base, scan_base + scan_bytes) is memset per batch.
   char* scan_base = nullptr;
   size_t scan_bytes = 0;
-  unsigned* bar = nullptr;      // persistent-sampler grid barrier {arrivals, generation} (in the scan region)
+  unsigned* bar = nullptr;       // persistent-sampler grid barrier {arrivals, generation} (in the scan region)
+  uint32_t* home = nullptr;      // home-region mask of the batch table (adaptive; written by the clear kernel)
   int cluster = 0;              // > 0: the whole batch in one launch of a cluster of this many CTAs
                                 // (HELIOS_SAMPLE_MODE=cluster|cluster16|chain)
   // shared-memory tile dedup (HELIOS_SAMPLE_DEDUP=smem|global): hop h runs tiled when tile_rows[h] > 0
@@ -282,6 +283,7 @@ struct helios_cache {
                                     // combined kernel, 2 host warps per 8)
   int gather_vu = 4;                // HBM / peer rows: 16-byte loads in flight per lane (HELIOS_GATHER_VU = 2/4/8/16;
                                     // 4: 80 registers, the footprint that leaves the sampler most room)
+  bool gather_evict = true;         // HBM-only fused gather: evict-first L2 policy on its loads and stores (HELIOS_GATHER_EVICT=0: off)
   int gather_async = 0;             // HBM-only fused gather: loads staged through a D-stage shared ring (HELIOS_GATHER_ASYNC=D, 4 or 8)
   bool gather_bulk = false;         // HELIOS_GATHER_BULK=1: HBM rows by cp.async.bulk (ablation)
   bool io_sync = false;            // HELIOS_CACHE_IO_SYNC ablation

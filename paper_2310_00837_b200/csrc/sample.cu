@@ -68,6 +68,11 @@ struct SampleCtx {
   int32_t fan[HELIOS_MAX_HOPS];
   int32_t L;
   unsigned* bar;  // grid barrier {arrivals, generation} (reset with the scan state every batch)
+  // home region of the batch table (table_insert): *home & mask, written by the previous batch's clear
+  // from its node count (adaptive); home_fixed != 0 overrides it (HELIOS_TABLE_HOME)
+  const uint32_t* home;
+  uint32_t* home_next;
+  uint32_t home_fixed;
   // shared-memory tile dedup: tile_rows[h] > 0 = hop h runs the tiled fill / assign /
   // relabel; elist[E0 + j] = {global slot, tile minpos} of the tile's j-th distinct id, ndist[t] = count
   int32_t tile_rows[HELIOS_MAX_HOPS];
@@ -85,7 +90,12 @@ struct SampleGroup {
 
 // N_0 = seeds: copy into nodes, insert into the table with local id = position.  Duplicate or
 // out-of-range seeds are latched (reading 7).
-__device__ __forceinline__ void insert_seed(const SampleCtx& c, int64_t i, const int64_t* __restrict__ seeds) {
+__device__ __forceinline__ uint32_t home_mask(const SampleCtx& c) {
+  return c.home_fixed ? c.home_fixed : (ld_volatile_u32(c.home) & c.mask);
+}
+
+__device__ __forceinline__ void insert_seed(const SampleCtx& c, int64_t i, const int64_t* __restrict__ seeds,
+                                            uint32_t hm) {
   const int64_t u = seeds[i];
   c.nodes[i] = u;
   c.node_slot[i] = kEmpty;
@@ -94,7 +104,7 @@ __device__ __forceinline__ void insert_seed(const SampleCtx& c, int64_t i, const
     return;
   }
   bool fresh;
-  const uint32_t s = table_insert(c.tab, c.mask, (uint32_t)u, kEmpty, &fresh);
+  const uint32_t s = table_insert(c.tab, c.mask, hm, (uint32_t)u, kEmpty, &fresh);
   c.node_slot[i] = s;
   if (!fresh) {
     latch(c.err, HELIOS_E_INVALID);
@@ -207,15 +217,16 @@ __device__ __forceinline__ void dev_count_scan(const SampleCtx& c, int h) {
     __syncthreads();
   }
   if (h == 0) {  // side job: N_0 = seeds into the table, spread over the whole grid
+    const uint32_t hm = home_mask(c);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-      insert_seed(c, i, seeds);
+      insert_seed(c, i, seeds, hm);
   }
   if (h > 0) dev_relabel_any(c, h - 1);  // side job: hop h-1's local ids are final (its assign has completed)
 }
 
-__device__ __forceinline__ void insert_edge(const SampleCtx& c, int64_t e, uint32_t u) {
+__device__ __forceinline__ void insert_edge(const SampleCtx& c, int64_t e, uint32_t u, uint32_t hm) {
   bool fresh;
-  c.slot_of[e] = table_insert(c.tab, c.mask, u, (uint32_t)e, &fresh);
+  c.slot_of[e] = table_insert(c.tab, c.mask, hm, u, (uint32_t)e, &fresh);
 }
 
 // Hop h fill: one G-lane group per frontier row (G = power of two >= min(f, 32), >= 4).  Copy the
@@ -234,6 +245,7 @@ __device__ __forceinline__ void dev_fill_insert(const SampleCtx& c, int h) {
   int32_t* scratch = c.bi[h];
   const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
   const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+  const uint32_t hm = home_mask(c);
   for (int64_t i = grp; i < n; i += ngrp) {
     const int64_t v = c.nodes[i];
     int64_t base = 0, d = 0;
@@ -244,7 +256,7 @@ __device__ __forceinline__ void dev_fill_insert(const SampleCtx& c, int h) {
     const int64_t off = bp[i];
     const int64_t k = (f < 0) ? d : min(d, (int64_t)f);
     if (k == d) {  // every neighbour, CSR order, no RNG consumed
-      for (int64_t p = gl; p < d; p += G) insert_edge(c, off + p, (uint32_t)c.indices[base + p]);
+      for (int64_t p = gl; p < d; p += G) insert_edge(c, off + p, (uint32_t)c.indices[base + p], hm);
     } else if (k <= G) {
       uint32_t t = 0, m = 0;
       if (gl < k) {
@@ -257,7 +269,7 @@ __device__ __forceinline__ void dev_fill_insert(const SampleCtx& c, int h) {
         const unsigned hit = __ballot_sync(gmask, gl < j && P == tj);
         if (gl == j) P = hit ? (m - 1) : tj;
       }
-      if (gl < k) insert_edge(c, off + gl, (uint32_t)c.indices[base + P]);
+      if (gl < k) insert_edge(c, off + gl, (uint32_t)c.indices[base + P], hm);
     } else {  // k > G (fanout > 32): leader runs Floyd serially, positions kept in the scratch row
       if (gl == 0) {
         for (int64_t j = 0; j < k; j++) {
@@ -273,7 +285,7 @@ __device__ __forceinline__ void dev_fill_insert(const SampleCtx& c, int h) {
         }
       }
       __syncwarp(gmask);
-      for (int64_t j = gl; j < k; j += G) insert_edge(c, off + j, (uint32_t)c.indices[base + scratch[off + j]]);
+      for (int64_t j = gl; j < k; j += G) insert_edge(c, off + j, (uint32_t)c.indices[base + scratch[off + j]], hm);
       __syncwarp(gmask);
     }
   }
@@ -361,12 +373,13 @@ __device__ __forceinline__ void dev_fill_tile(const SampleCtx& c, int h) {
     }
     __syncthreads();
     // one global insert per distinct id of the tile, with the tile's first position of it
+    const uint32_t hm = home_mask(c);
     for (int q = threadIdx.x; q < kTileSlots; q += blockDim.x) {
       const uint32_t u = s_key[q];
       if (u != kEmpty) {
         bool fresh;
         const uint32_t mp = s_min[q];
-        const uint32_t gs = table_insert(c.tab, c.mask, u, mp, &fresh);
+        const uint32_t gs = table_insert(c.tab, c.mask, hm, u, mp, &fresh);
         const uint32_t j = atomicAdd(&s_cnt, 1u);
         c.elist[E0 + j] = make_uint2(gs, mp);
         s_li[q] = j;
@@ -469,6 +482,7 @@ __device__ __forceinline__ void dev_fill_seg(const SampleCtx& c, int h) {
   const int32_t* __restrict__ bp = c.bp[h];
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t hm = home_mask(c);
   for (int64_t i = warp * rpw + seg; i < n; i += nwarps * rpw) {
     const int64_t v = c.nodes[i];
     int64_t base = 0, d = 0;
@@ -479,7 +493,7 @@ __device__ __forceinline__ void dev_fill_seg(const SampleCtx& c, int h) {
     const int64_t off = bp[i];
     const int64_t k = min(d, (int64_t)f);
     if (k == d) {  // every neighbour, CSR order, no RNG consumed
-      for (int64_t p = sl; p < d; p += S) insert_edge(c, off + p, (uint32_t)c.indices[base + p]);
+      for (int64_t p = sl; p < d; p += S) insert_edge(c, off + p, (uint32_t)c.indices[base + p], hm);
     } else {  // Floyd's k-subset, lane sl owning draw sl
       uint32_t t = 0, m = 0;
       if (sl < k) {
@@ -492,7 +506,7 @@ __device__ __forceinline__ void dev_fill_seg(const SampleCtx& c, int h) {
         const unsigned hit = __ballot_sync(smask, sl < j && P == tj);
         if (sl == j) P = hit ? (m - 1) : tj;
       }
-      if (sl < k) insert_edge(c, off + sl, (uint32_t)c.indices[base + P]);
+      if (sl < k) insert_edge(c, off + sl, (uint32_t)c.indices[base + P], hm);
     }
   }
 }
@@ -557,6 +571,11 @@ __device__ __forceinline__ void dev_relabel(const SampleCtx& c, int h) { dev_rel
 // (every occupied slot belongs to one node of N_L).
 __device__ __forceinline__ void dev_table_clear(const SampleCtx& c) {
   const int64_t n = c.level_counts[c.L];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // the next batch's home region: 2^k >= 2.5 n (>= 1024 slots)
+    uint32_t hm = 1023;
+    while (hm < c.mask && (int64_t)hm + 1 < n * 5 / 2) hm = hm * 2 + 1;
+    *c.home_next = hm & c.mask;
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t s = c.node_slot[i];
     if (s != kEmpty) {
@@ -570,7 +589,8 @@ __device__ __forceinline__ void dev_insert_seeds(const SampleCtx& c) {  // L = 0
   const int64_t* seeds = (const int64_t*)c.params[2];
   const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i0 == 0) c.level_counts[0] = B;
-  for (int64_t i = i0; i < B; i += (int64_t)gridDim.x * blockDim.x) insert_seed(c, i, seeds);
+  const uint32_t hm = home_mask(c);
+  for (int64_t i = i0; i < B; i += (int64_t)gridDim.x * blockDim.x) insert_seed(c, i, seeds, hm);
 }
 
 // ---- multi-kernel path: one kernel per phase, chained with programmatic dependent launch ----
@@ -894,7 +914,7 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
   ws_free(w);
   const size_t table_bytes = (size_t)T * sizeof(TableSlot);
   const size_t status_bytes = (size_t)(tiles_r + tiles_e) * HELIOS_MAX_HOPS * 8;
-  const size_t counter_bytes = (size_t)2 * HELIOS_MAX_HOPS * 4 + 8;
+  const size_t counter_bytes = (size_t)2 * HELIOS_MAX_HOPS * 4 + 8 + 8;  // + barrier, + home word
   w.reset_bytes = table_bytes + status_bytes + counter_bytes;
   HCUDA(cudaMalloc(&w.reset_base, w.reset_bytes));
   HCUDA(cudaMalloc(&w.slot_of, (size_t)max_e * 4));
@@ -932,6 +952,8 @@ helios_status ws_ensure(helios_graph* g, SampleWS& w, int64_t B, const int32_t* 
   w.bar = (unsigned*)p;
   p += 8;
   w.scan_bytes = (size_t)(p - w.scan_base);
+  w.home = (uint32_t*)p;  // outside the per-batch reset; all-ones at allocation = home the whole table
+  p += 8;
   if (const char* e = getenv("HELIOS_SAMPLE_PERSISTENT")) w.persistent = atoi(e) != 0;
   if (const char* e = getenv("HELIOS_FILL_SEG")) w.fill_seg = atoi(e) != 0;
   if (const char* e = getenv("HELIOS_SAMPLE_MODE")) {
@@ -994,6 +1016,15 @@ static SampleCtx make_ctx(const helios_graph* g, const SampleWS& w, const int32_
   }
   c.L = L;
   c.bar = w.bar;
+  c.home = w.home;
+  c.home_next = w.home;
+  c.home_fixed = 0;
+  if (const char* e = getenv("HELIOS_TABLE_HOME")) {  // fixed home region (0: the whole table, no adaptation)
+    const long long v = atoll(e);
+    uint32_t hm = 1023;
+    while (hm < c.mask && (long long)hm + 1 < v) hm = hm * 2 + 1;
+    c.home_fixed = (v <= 0) ? c.mask : (hm & c.mask);
+  }
   const bool chain = !w.cluster && !w.persistent;  // the one-launch samplers run the global-table phases
   for (int h = 0; h < HELIOS_MAX_HOPS; h++) c.tile_rows[h] = (chain && h < L) ? w.tile_rows[h] : 0;
   c.elist = w.elist;

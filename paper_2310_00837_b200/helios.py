@@ -18,8 +18,10 @@ os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import torch  # noqa: E402
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# HELIOS_LIB=trace loads the traced build (device pipeline timeline, tools/trace_pipeline.py)
-SO_PATH = os.path.join(_HERE, "libhelios_trace.so" if os.environ.get("HELIOS_LIB") == "trace" else "libhelios.so")
+# HELIOS_LIB=trace loads the traced build (device pipeline timeline, tools/trace_pipeline.py); HELIOS_LIB=<x>
+# loads libhelios_<x>.so (same-box A/B of another build of the same ABI)
+_LIB = os.environ.get("HELIOS_LIB")
+SO_PATH = os.path.join(_HERE, f"libhelios_{_LIB}.so" if _LIB else "libhelios.so")
 if not os.path.exists(SO_PATH):
     raise ImportError(f"{SO_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
                       "(nvcc, sm_100a). There is no CPU fallback.")

@@ -130,16 +130,17 @@ def test_io_ring_wraparound_and_fault(H, c1, c1_hot, sync):
     c.free()
 
 
-@pytest.mark.parametrize("direct,async_d,vu", [("1", "0", "4"), ("1", "0", "8"), ("0", "0", "4"), ("1", "4", "4"),
-                                               ("1", "8", "4")])
-def test_hbm_only_direct_gather(H, c1, c1_hot, direct, async_d, vu, monkeypatch):
+@pytest.mark.parametrize("direct,async_d,vu,evict", [("1", "0", "4", "0"), ("1", "0", "8", "0"), ("0", "0", "4", "0"),
+                                                     ("1", "4", "4", "0"), ("1", "8", "4", "0"), ("1", "0", "4", "1")])
+def test_hbm_only_direct_gather(H, c1, c1_hot, direct, async_d, vu, evict, monkeypatch):
     """Caches whose rows all live in HBM run the fused lookup + gather kernel (default) instead of K3 + K4
     (HELIOS_GATHER_DIRECT=0), with register-staged loads (VU per lane) or a D-stage cp.async shared-memory
-    ring (HELIOS_GATHER_ASYNC=D):
+    ring (HELIOS_GATHER_ASYNC=D), optionally with an evict-first L2 policy (HELIOS_GATHER_EVICT=1):
     same bytes, same tier counts, out-of-range ids latch E_RANGE."""
     monkeypatch.setenv("HELIOS_GATHER_DIRECT", direct)
     monkeypatch.setenv("HELIOS_GATHER_ASYNC", async_d)
     monkeypatch.setenv("HELIOS_GATHER_VU", vu)
+    monkeypatch.setenv("HELIOS_GATHER_EVICT", evict)
     g, hot = c1_hot
     cfg = c1.cfg
     c = H.helios_cache_build(g, hot, cfg.R, cfg.V, 0, host_table=c1.table)

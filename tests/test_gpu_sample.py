@@ -48,7 +48,9 @@ def mode(request, monkeypatch):
     per-tile shared hash, bitmap ranking, tiled relabel) for every hop with a bounded fanout.  "groups": the
     chain with the round-1 power-of-two lane groups in the fill (HELIOS_FILL_SEG=0; the default packs
     f-lane segments)."""
-    monkeypatch.setenv("HELIOS_SAMPLE_MODE", "chain" if request.param in ("tiled", "groups") else request.param)
+    chain = ("tiled", "groups")
+    monkeypatch.setenv("HELIOS_SAMPLE_MODE", "chain" if request.param in chain else request.param)
+    monkeypatch.delenv("HELIOS_TABLE_HOME", raising=False)
     monkeypatch.setenv("HELIOS_SAMPLE_DEDUP", "smem" if request.param == "tiled" else "global")
     monkeypatch.setenv("HELIOS_FILL_SEG", "0" if request.param == "groups" else "1")
     return request.param
@@ -84,6 +86,28 @@ def test_medium_graph(H, medium, B, fanouts, mode):
         gpu = run_gpu(H, g, seeds, fanouts, key)
         orc = oracle.sample(medium.indptr, medium.indices, seeds, fanouts, key)
         assert_same(gpu, orc, len(fanouts))
+
+
+@pytest.mark.parametrize("home", ["1024", "0"])
+def test_table_home_region(H, c1, medium, home, monkeypatch):
+    """The batch table's home region changes only where keys land, never the result: keys
+    homed in the table's first 1,024 slots (long probe runs spilling over the worst-case table) or in the
+    whole table (the round-1 hashing) give the oracle's bits; the default adapts the region to the
+    previous batch's node count, so the C1 epoch also runs with regions sized from smaller batches."""
+    monkeypatch.setenv("HELIOS_TABLE_HOME", home)
+    cfg = c1.cfg
+    g = H.helios_graph_load(c1.graph.indptr, c1.graph.indices)
+    keys = workloads.batch_keys(0, len(c1.batches))
+    for b in range(0, len(c1.batches), 3):
+        gpu = run_gpu(H, g, c1.batches[b], cfg.fanouts, keys[b])
+        assert_same(gpu, oracle.sample(c1.graph.indptr, c1.graph.indices, c1.batches[b], cfg.fanouts, keys[b]),
+                    len(cfg.fanouts))
+    g = H.helios_graph_load(medium.indptr, medium.indices)
+    rng = np.random.default_rng(3)
+    for B, fanouts in ((1024, [15, 10, 5]), (333, [3, 3, 3, 3])):
+        seeds = rng.choice(medium.V, B, replace=False)
+        gpu = run_gpu(H, g, seeds, fanouts, 7)
+        assert_same(gpu, oracle.sample(medium.indptr, medium.indices, seeds, fanouts, 7), len(fanouts))
 
 
 def test_hub_and_isolated(H, mode):
