@@ -420,6 +420,7 @@ helios_status cache_build_impl(helios_graph* g, const helios_cache_desc* d, heli
     if (const char* e = getenv("HELIOS_GATHER_SPLIT_HOST")) c->split_host = atoi(e) != 0;
     if (const char* e = getenv("HELIOS_GATHER_DIRECT")) c->direct = atoi(e) != 0;
     if (const char* e = getenv("HELIOS_GATHER_EVICT")) c->gather_evict = atoi(e) != 0;
+    if (const char* e = getenv("HELIOS_GATHER_EVICT_LISTS")) c->gather_evict_lists = atoi(e) != 0;
     if (const char* e = getenv("HELIOS_GATHER_ASYNC")) c->gather_async = std::max(0, std::min(atoi(e), 8));
     if (c->gather_bulk) per_sm = 1;  // 192 KB of shared memory per CTA
     c->gather_ctas = c->sms * per_sm;

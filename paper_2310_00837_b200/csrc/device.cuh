@@ -118,6 +118,16 @@ __device__ __forceinline__ uint32_t table_insert(TableSlot* tab, uint32_t mask, 
   }
 }
 
+// CSR index read with an evict-first L2 policy (sampled adjacency positions are rarely re-read within
+// a batch; the default keeps them from displacing the batch tables in L2, HELIOS_SAMPLE_IDX_EVICT=0: off).
+__device__ __forceinline__ int32_t ld_index_ef(const int32_t* p) {
+  uint64_t pol;
+  int32_t v;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ void latch(int* err, int code) {
   if (code) atomicCAS(err, 0, code);
 }

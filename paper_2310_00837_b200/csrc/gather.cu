@@ -172,6 +172,7 @@ struct GatherArgs {
   bool vu16;                // HBM / peer rows: 16 (else 8) 16-byte loads in flight per lane
   bool vu4;                 // HBM / peer rows: 4 loads in flight per lane (smaller register footprint)
   bool vu2;                 // HBM / peer rows: 2 loads in flight per lane
+  bool evict;               // HBM / peer rows: evict-first L2 policy on the row loads and stores
   int* err;
   const char* hbm;          // this rank's shard
   char* const* peers;       // device [G]
@@ -263,14 +264,18 @@ __device__ __forceinline__ void flat_rows(const GatherArgs& a, int q, int64_t cn
         const int f = b0 + lane + 32 * k;
         const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
         const char* src = (const char*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)sp, row);
-        if (f < nv) r[k] = ld_stream((const int4*)src + (f - row * nvec));
+        if (f < nv) r[k] = a.evict ? ld_stream_ef((const int4*)src + (f - row * nvec), policy_evict_first())
+                                   : ld_stream((const int4*)src + (f - row * nvec));
       }
 #pragma unroll
       for (int k = 0; k < VU; k++) {
         const int f = b0 + lane + 32 * k;
         const int row = (rw == 1) ? 0 : min((int)(((uint32_t)f * inv) >> 20), rw - 1);
         char* dst = (char*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)dp, row);
-        if (f < nv) st_global_v4((int4*)dst + (f - row * nvec), r[k]);
+        if (f < nv) {
+          if (a.evict) st_global_v4_ef((int4*)dst + (f - row * nvec), r[k], policy_evict_first());
+          else st_global_v4((int4*)dst + (f - row * nvec), r[k]);
+        }
       }
     }
     sp = sp_n;
@@ -1219,6 +1224,7 @@ static GatherArgs make_args(helios_cache* c, GatherWS& w, void* out, helios_gath
   a.vu16 = c->gather_vu == 16;
   a.vu4 = c->gather_vu == 4;
   a.vu2 = c->gather_vu == 2;
+  a.evict = c->gather_evict_lists;
   a.err = c->d_err;
   a.hbm = c->hbm;
   a.peers = c->d_peers;

@@ -284,6 +284,7 @@ struct helios_cache {
   int gather_vu = 4;                // HBM / peer rows: 16-byte loads in flight per lane (HELIOS_GATHER_VU = 2/4/8/16;
                                     // 4: 80 registers, the footprint that leaves the sampler most room)
   bool gather_evict = true;         // HBM-only fused gather: evict-first L2 policy on its loads and stores (HELIOS_GATHER_EVICT=0: off)
+  bool gather_evict_lists = false;  // K4 (tier lists): evict-first L2 policy on HBM / peer row copies (HELIOS_GATHER_EVICT_LISTS=1)
   int gather_async = 0;             // HBM-only fused gather: loads staged through a D-stage shared ring (HELIOS_GATHER_ASYNC=D, 4 or 8)
   bool gather_bulk = false;         // HELIOS_GATHER_BULK=1: HBM rows by cp.async.bulk (ablation)
   bool io_sync = false;            // HELIOS_CACHE_IO_SYNC ablation

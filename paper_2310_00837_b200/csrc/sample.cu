@@ -79,6 +79,7 @@ struct SampleCtx {
   uint2* elist;
   uint32_t* ndist;
   int32_t fill_seg;  // fill with f-lane segments (default; HELIOS_FILL_SEG=0: power-of-two groups)
+  int32_t idx_ef;    // evict-first L2 policy on the fill's CSR index reads (default; HELIOS_SAMPLE_IDX_EVICT=0: off)
 };
 
 // The batches of one launch (a plan slot's group): the chain's kernels run with
@@ -256,7 +257,8 @@ __device__ __forceinline__ void dev_fill_insert(const SampleCtx& c, int h) {
     const int64_t off = bp[i];
     const int64_t k = (f < 0) ? d : min(d, (int64_t)f);
     if (k == d) {  // every neighbour, CSR order, no RNG consumed
-      for (int64_t p = gl; p < d; p += G) insert_edge(c, off + p, (uint32_t)c.indices[base + p], hm);
+      for (int64_t p = gl; p < d; p += G)
+        insert_edge(c, off + p, (uint32_t)(c.idx_ef ? ld_index_ef(c.indices + base + p) : c.indices[base + p]), hm);
     } else if (k <= G) {
       uint32_t t = 0, m = 0;
       if (gl < k) {
@@ -269,7 +271,7 @@ __device__ __forceinline__ void dev_fill_insert(const SampleCtx& c, int h) {
         const unsigned hit = __ballot_sync(gmask, gl < j && P == tj);
         if (gl == j) P = hit ? (m - 1) : tj;
       }
-      if (gl < k) insert_edge(c, off + gl, (uint32_t)c.indices[base + P], hm);
+      if (gl < k) insert_edge(c, off + gl, (uint32_t)(c.idx_ef ? ld_index_ef(c.indices + base + P) : c.indices[base + P]), hm);
     } else {  // k > G (fanout > 32): leader runs Floyd serially, positions kept in the scratch row
       if (gl == 0) {
         for (int64_t j = 0; j < k; j++) {
@@ -493,7 +495,8 @@ __device__ __forceinline__ void dev_fill_seg(const SampleCtx& c, int h) {
     const int64_t off = bp[i];
     const int64_t k = min(d, (int64_t)f);
     if (k == d) {  // every neighbour, CSR order, no RNG consumed
-      for (int64_t p = sl; p < d; p += S) insert_edge(c, off + p, (uint32_t)c.indices[base + p], hm);
+      for (int64_t p = sl; p < d; p += S)
+        insert_edge(c, off + p, (uint32_t)(c.idx_ef ? ld_index_ef(c.indices + base + p) : c.indices[base + p]), hm);
     } else {  // Floyd's k-subset, lane sl owning draw sl
       uint32_t t = 0, m = 0;
       if (sl < k) {
@@ -506,7 +509,7 @@ __device__ __forceinline__ void dev_fill_seg(const SampleCtx& c, int h) {
         const unsigned hit = __ballot_sync(smask, sl < j && P == tj);
         if (sl == j) P = hit ? (m - 1) : tj;
       }
-      if (sl < k) insert_edge(c, off + sl, (uint32_t)c.indices[base + P], hm);
+      if (sl < k) insert_edge(c, off + sl, (uint32_t)(c.idx_ef ? ld_index_ef(c.indices + base + P) : c.indices[base + P]), hm);
     }
   }
 }
@@ -1030,6 +1033,8 @@ static SampleCtx make_ctx(const helios_graph* g, const SampleWS& w, const int32_
   c.elist = w.elist;
   c.ndist = w.ndist;
   c.fill_seg = w.fill_seg ? 1 : 0;
+  c.idx_ef = 1;  // C2 +3.8 %, C3 within noise (profiles/r02/l2_policy_c2_c3.jsonl)
+  if (const char* e = getenv("HELIOS_SAMPLE_IDX_EVICT")) c.idx_ef = atoi(e) != 0;
   return c;
 }
 
