@@ -136,11 +136,14 @@ class ClockSampler:
 
 def traffic_of(name: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")
-    try:
-        d = json.load(open(p)).get(name)
-    except (OSError, ValueError):
-        return None
+    d = None
+    for f in ("ncu_traffic_r02.json", "ncu_traffic_r01.json"):  # latest capture of the current kernels first
+        try:
+            d = json.load(open(os.path.join(ROOT, "profiles", f))).get(name)
+        except (OSError, ValueError):
+            d = None
+        if d:
+            break
     if not d:
         return None
     return round(d["dram_bytes_read_per_launch"] + d["dram_bytes_write_per_launch"])
