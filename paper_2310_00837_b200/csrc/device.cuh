@@ -91,61 +91,6 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
   return v;
 }
 
-// Batch-table accesses.  Built with -DHELIOS_TABLE_EL (libhelios_tel.so, an A/B build) they carry an
-// evict-last L2 policy, so a slot's tables stay L2-resident from batch to batch; the default build uses
-// plain volatile / relaxed accesses.
-#ifdef HELIOS_TABLE_EL
-__device__ __forceinline__ uint64_t tab_pol() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ unsigned long long tab_ld_km(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(tab_pol()) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long tab_cas(unsigned long long* p, unsigned long long cmp, unsigned long long v) {
-  return atomicCAS(p, cmp, v);  // atom takes no L2 cache hint; the line keeps the policy of its loads
-}
-__device__ __forceinline__ void tab_min(unsigned long long* p, unsigned long long v) { atomicMin(p, v); }
-__device__ __forceinline__ uint4 tab_ld_v4(const void* p) {
-  uint4 v;
-  asm volatile("ld.relaxed.gpu.global.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(tab_pol()) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint32_t tab_ld_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(tab_pol()) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long tab_ld_km_plain(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(tab_pol()) : "memory");
-  return v;
-}
-__device__ __forceinline__ void tab_st_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(tab_pol()) : "memory");
-}
-__device__ __forceinline__ void tab_st_v4(void* p, uint4 v) {
-  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w),
-               "l"(tab_pol())
-               : "memory");
-}
-#else
-__device__ __forceinline__ unsigned long long tab_ld_km(const unsigned long long* p) { return ld_volatile_u64(p); }
-__device__ __forceinline__ unsigned long long tab_cas(unsigned long long* p, unsigned long long cmp, unsigned long long v) {
-  return atomicCAS(p, cmp, v);
-}
-__device__ __forceinline__ void tab_min(unsigned long long* p, unsigned long long v) { atomicMin(p, v); }
-__device__ __forceinline__ uint4 tab_ld_v4(const void* p) { return ld_volatile_v4u32(p); }
-__device__ __forceinline__ uint32_t tab_ld_u32(const uint32_t* p) { return *p; }
-__device__ __forceinline__ unsigned long long tab_ld_km_plain(const unsigned long long* p) { return *p; }
-__device__ __forceinline__ void tab_st_u32(uint32_t* p, uint32_t v) { *p = v; }
-__device__ __forceinline__ void tab_st_v4(void* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
-#endif
-
 // Open-addressing (linear probing) insert-or-find of key u at edge position e: returns the slot,
 // *fresh = created here (with minpos = e); an existing slot's minpos is lowered to e if larger.
 // Keys are homed in the table's first hmask+1 slots (hmask <= mask, both 2^k - 1) and probe on through
@@ -156,16 +101,16 @@ __device__ __forceinline__ uint32_t table_insert(TableSlot* tab, uint32_t mask, 
   const unsigned long long want = ((unsigned long long)u << 32) | e;
   uint32_t s = hash32(u) & hmask;
   for (;;) {
-    unsigned long long w = tab_ld_km(&tab[s].km);
+    unsigned long long w = ld_volatile_u64(&tab[s].km);
     if ((uint32_t)(w >> 32) == kEmpty) {
-      w = tab_cas(&tab[s].km, kEmptyKM, want);
+      w = atomicCAS(&tab[s].km, kEmptyKM, want);
       if (w == kEmptyKM) {
         *fresh = true;
         return s;
       }
     }
     if ((uint32_t)(w >> 32) == u) {
-      if ((uint32_t)w > e) tab_min(&tab[s].km, want);
+      if ((uint32_t)w > e) atomicMin(&tab[s].km, want);
       *fresh = false;
       return s;
     }

@@ -111,7 +111,7 @@ __device__ __forceinline__ void insert_seed(const SampleCtx& c, int64_t i, const
     latch(c.err, HELIOS_E_INVALID);
     return;
   }
-  tab_st_u32(&c.tab[s].local, (uint32_t)i);
+  c.tab[s].local = (uint32_t)i;
 }
 
 // ---- shared-memory tile dedup (north_star: "warp-cooperative dedup/relabel via a shared-memory hash
@@ -162,7 +162,7 @@ __device__ __forceinline__ void dev_relabel_any(const SampleCtx& c, int h) {
   const int64_t ep = c.edge_counts[h];
   int32_t* __restrict__ bi = c.bi[h];
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ep; e += (int64_t)gridDim.x * blockDim.x)
-    bi[e] = (int32_t)tab_ld_u32(&c.tab[c.slot_of[e]].local);
+    bi[e] = (int32_t)c.tab[c.slot_of[e]].local;
 }
 
 // Hop h degree scan: k_i = min(deg(N_h[i]), f_h), block_indptr[h] = exclusive scan (persistent tile
@@ -543,7 +543,7 @@ __device__ __forceinline__ void dev_assign(const SampleCtx& c, int h) {
       slot[q] = 0;
       if (e < eh) {
         slot[q] = c.slot_of[e];
-        const uint4 t = tab_ld_v4(&c.tab[slot[q]]);  // {minpos, key, local, pad}
+        const uint4 t = ld_volatile_v4u32(&c.tab[slot[q]]);  // {minpos, key, local, pad}
         flag[q] = (t.z == kEmpty && t.x == (uint32_t)e) ? 1 : 0;
       }
       sum += flag[q];
@@ -556,9 +556,9 @@ __device__ __forceinline__ void dev_assign(const SampleCtx& c, int h) {
     for (int q = 0; q < kScanItems; q++) {
       if (flag[q]) {
         const int64_t id = nh + run;
-        c.nodes[id] = (int64_t)(tab_ld_km_plain(&c.tab[slot[q]].km) >> 32);
+        c.nodes[id] = (int64_t)(c.tab[slot[q]].km >> 32);
         c.node_slot[id] = slot[q];
-        tab_st_u32(&c.tab[slot[q]].local, (uint32_t)id);
+        c.tab[slot[q]].local = (uint32_t)id;
         run++;
       }
     }
@@ -582,7 +582,7 @@ __device__ __forceinline__ void dev_table_clear(const SampleCtx& c) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t s = c.node_slot[i];
     if (s != kEmpty) {
-      tab_st_v4(&c.tab[s], make_uint4(kEmpty, kEmpty, kEmpty, kEmpty));
+      *reinterpret_cast<uint4*>(&c.tab[s]) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     }
   }
 }
