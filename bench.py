@@ -495,7 +495,7 @@ def main():
     seq = [my_batches[i % len(my_batches)] for i in range(need)]
     seed_of = {b: torch.as_tensor(inp.batches[b]).cuda() for b in sorted(set(seq))}
     stream = torch.cuda.current_stream()
-    depth = args.depth if args.depth > 0 else (24 if S > 0 else 12)
+    depth = args.depth if args.depth > 0 else (24 if S > 0 else 16)   # profiles/r02/retune_l2_defaults.jsonl
     # gather kernels of this cache: fused lookup+gather when every row is in HBM, else the
     # lookup, the HBM part and (with a host tier) the host part in its own kernel
     direct = S == 0 and not file_cfg and os.environ.get("HELIOS_GATHER_DIRECT") != "0" and not os.environ.get("HELIOS_GATHER_BULK")

@@ -1046,9 +1046,9 @@ static void launch_fill(const helios_graph* g, const SampleGroup& P, int n, int 
     launch_pdl(k_fill_tile<G>, dim3(grid, n), dim3(256), st, P, h);
     return;
   }
-  static const int per_sm = [] {  // fill CTAs per SM at most (HELIOS_FILL_CTAS_PER_SM, default 2: leaves SM
-    const char* e = getenv("HELIOS_FILL_CTAS_PER_SM");  // slots to the other batches' kernels)
-    return e ? std::max(1, std::min(atoi(e), 8)) : 2;
+  static const int per_sm = [] {  // fill CTAs per SM at most (HELIOS_FILL_CTAS_PER_SM, default 4; 2 was best
+    const char* e = getenv("HELIOS_FILL_CTAS_PER_SM");  // before the tables stayed L2-resident)
+    return e ? std::max(1, std::min(atoi(e), 8)) : 4;
   }();
   const int32_t f = P.c[0].fan[h];
   if (P.c[0].fill_seg && f >= 1 && f <= 32) {  // S-lane segments, floor(32 / f) rows per warp
