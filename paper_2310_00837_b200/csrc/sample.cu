@@ -1173,11 +1173,15 @@ helios_status sample_launch_group(helios_graph* g, SampleWS* const* ws, const he
       if (hs != HELIOS_OK) return hs;
     }
   }
+  static const int tail_per_sm = [] {  // relabel / clear CTAs per SM at most (HELIOS_TAIL_CTAS_PER_SM, default 2)
+    const char* e = getenv("HELIOS_TAIL_CTAS_PER_SM");
+    return e ? std::max(1, std::min(atoi(e), 8)) : 2;
+  }();
   if (L > 0) {
-    const int ge = (int)std::min<int64_t>(std::max<int64_t>(1, (edg[L - 1] + 255) / 256), (int64_t)g->sms * 2);
+    const int ge = (int)std::min<int64_t>(std::max<int64_t>(1, (edg[L - 1] + 255) / 256), (int64_t)g->sms * tail_per_sm);
     launch_pdl(k_relabel, dim3(ge, n), dim3(256), st, P, L - 1);
   }
-  const int gc = (int)std::min<int64_t>(std::max<int64_t>(1, (maxn + 255) / 256), (int64_t)g->sms * 2);
+  const int gc = (int)std::min<int64_t>(std::max<int64_t>(1, (maxn + 255) / 256), (int64_t)g->sms * tail_per_sm);
   launch_pdl(k_table_clear, dim3(gc, n), dim3(256), st, P);
   HCUDA(cudaGetLastError());
   return HELIOS_OK;
