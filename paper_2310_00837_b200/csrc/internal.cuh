@@ -90,7 +90,10 @@ inline cudaError_t launch_pdl_smem(void (*kernel)(KArgs...), dim3 grid, dim3 blo
 constexpr int kMaxGroup = 4;                // batches per plan-slot group (one launch of each kernel)
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // empty hash key / unassigned local id / no minpos
 constexpr int kScanBlock = 256;
-constexpr int kScanItems = 4;
+#ifndef HELIOS_SCAN_ITEMS
+#define HELIOS_SCAN_ITEMS 4  // items per thread of the count-scan / assign tiles (A/B builds: -DHELIOS_SCAN_ITEMS=n)
+#endif
+constexpr int kScanItems = HELIOS_SCAN_ITEMS;
 constexpr int kScanTile = kScanBlock * kScanItems;
 
 // Per-scan decoupled look-back state (reset to all-ones bytes before use).
