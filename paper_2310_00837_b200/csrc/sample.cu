@@ -574,8 +574,10 @@ __device__ __forceinline__ void dev_relabel(const SampleCtx& c, int h) { dev_rel
 // (every occupied slot belongs to one node of N_L).
 __device__ __forceinline__ void dev_table_clear(const SampleCtx& c) {
   const int64_t n = c.level_counts[c.L];
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // the next batch's home region: 2^k >= 2.5 n (>= 1024 slots)
-    uint32_t hm = 1023;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // the next batch's home region: 2^k >= 2.5 n, at least 1/8 of the
+    // worst-case table and at least half of this batch's region (it shrinks one halving per batch), which
+    // bounds the probe runs of a batch much larger than its predecessor
+    uint32_t hm = max(max(1023u, c.mask >> 3), (ld_volatile_u32(c.home) & c.mask) >> 1);
     while (hm < c.mask && (int64_t)hm + 1 < n * 5 / 2) hm = hm * 2 + 1;
     *c.home_next = hm & c.mask;
   }
